@@ -1,0 +1,198 @@
+"""CPU oracle for the view-tied splatting hot path — TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py` (its `cpu_baseline` leg and
+`--impl reference`) may import this package.  The product package `paper_2506_02741_b200`
+never imports it, and it never imports the product package: the two share no code.
+
+This module is argument marshalling (numpy ↔ ctypes) around `oracle/vtgs_oracle.c`, whose
+header lists what each function computes and which PAPER.md / SPEC.md passage it follows.
+`mode="f32"` takes every decision in fp32 (the kernel's precision) and
+accumulates values in fp64; `mode="f64"` is fp64 throughout (finite-difference pins).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = [os.path.join(_HERE, "vtgs_oracle.c"), os.path.join(_HERE, "oracle_impl.inc")]
+_LIB_PATH = os.path.join(_HERE, "libvtgs_oracle.so")
+_lib = None
+
+_D = ctypes.POINTER(ctypes.c_double)
+_I64 = ctypes.POINTER(ctypes.c_int64)
+_I32 = ctypes.POINTER(ctypes.c_int32)
+_U8 = ctypes.POINTER(ctypes.c_uint8)
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (no FMA contraction, no fast-math)."""
+    stale = not os.path.exists(_LIB_PATH) or any(
+        os.path.getmtime(s) > os.path.getmtime(_LIB_PATH) for s in _SRC)
+    if force or stale:
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
+               _SRC[0], "-o", _LIB_PATH + ".tmp", "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB_PATH + ".tmp", _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB_PATH)
+        for m in ("f32", "f64"):
+            f = getattr(lib, f"or_instantiate_{m}")
+            f.restype = ctypes.c_int64
+            f.argtypes = [_D, _D, _D, ctypes.c_int, _D, ctypes.c_int, ctypes.c_int, _D, ctypes.c_double, _D, _D]
+            f = getattr(lib, f"or_project_{m}")
+            f.restype = None
+            f.argtypes = [_D, ctypes.c_int64, _D, _D, ctypes.c_int, ctypes.c_int, _D, _D, _I32, _I32]
+            f = getattr(lib, f"or_tile_lists_{m}")
+            f.restype = ctypes.c_int64
+            f.argtypes = [_D, ctypes.c_int64, _D, _D, ctypes.c_int, ctypes.c_int, _I64, _I64, ctypes.c_int64]
+            f = getattr(lib, f"or_render_{m}")
+            f.restype = ctypes.c_int
+            f.argtypes = [_D, _D, ctypes.c_int64, _D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                          _D, _D, _D, _D, _I32, _I32, _I64, _U8, ctypes.POINTER(ctypes.c_uint64)]
+            f = getattr(lib, f"or_render_bwd_{m}")
+            f.restype = ctypes.c_int
+            f.argtypes = [_D, _D, ctypes.c_int64, _D, _D, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D, _D, _D, _D]
+        f = lib.or_l1_upstream
+        f.restype = ctypes.c_double
+        f.argtypes = [_D, _D, _D, _D, _D, _U8, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                      ctypes.c_int, ctypes.c_int, ctypes.c_int, _D, _D, _D, _I32]
+        _lib = lib
+    return _lib
+
+
+def _d(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _p(a, t=_D):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _intr(intr) -> np.ndarray:
+    return _d([intr.fx, intr.fy, intr.cx, intr.cy])
+
+
+def instantiate(depth, rgb, poses, intr, opacity=None, opacity_default=0.5, mode="f32"):
+    """(a1) depth [K,H,W], rgb [K,H,W,3], poses [K,7] → pos_rad [N,4], col_opa [N,4], n_valid."""
+    lib = _load()
+    depth = _d(depth)
+    K, H, W = depth.shape
+    rgb, poses = _d(rgb), _d(poses).reshape(K, 7)
+    opa = None if opacity is None else _d(opacity)
+    N = K * H * W
+    pos_rad = np.zeros((N, 4))
+    col_opa = np.zeros((N, 4))
+    n = getattr(lib, f"or_instantiate_{mode}")(_p(depth), _p(rgb), _p(poses), K, _p(_intr(intr)), W, H,
+                                                _p(opa), float(opacity_default), _p(pos_rad), _p(col_opa))
+    return pos_rad, col_opa, int(n)
+
+
+def project(pos_rad, view, intr, mode="f32"):
+    """(a2) → dict(proj [N,4] (u,v,z,σ), xc [N,3], rect [N,4] (x0,y0,x1,y1), status [N])."""
+    lib = _load()
+    pos_rad = _d(pos_rad).reshape(-1, 4)
+    N = pos_rad.shape[0]
+    proj = np.zeros((N, 4))
+    xc = np.zeros((N, 3))
+    rect = np.zeros((N, 4), dtype=np.int32)
+    status = np.zeros(N, dtype=np.int32)
+    getattr(lib, f"or_project_{mode}")(_p(pos_rad), N, _p(_d(view)), _p(_intr(intr)), intr.width, intr.height,
+                                       _p(proj), _p(xc), _p(rect, _I32), _p(status, _I32))
+    return {"proj": proj, "xc": xc, "rect": rect, "status": status}
+
+
+def tile_lists(pos_rad, view, intr, mode="f32"):
+    """(a3) → (tile_start [T+1] int64, gid [P] int64)."""
+    lib = _load()
+    pos_rad = _d(pos_rad).reshape(-1, 4)
+    N = pos_rad.shape[0]
+    ntiles = ((intr.width + 15) // 16) * ((intr.height + 15) // 16)
+    start = np.zeros(ntiles + 1, dtype=np.int64)
+    fn = getattr(lib, f"or_tile_lists_{mode}")
+    P = fn(_p(pos_rad), N, _p(_d(view)), _p(_intr(intr)), intr.width, intr.height, _p(start, _I64), None, 0)
+    if P < 0:
+        raise MemoryError("oracle tile lists")
+    gid = np.zeros(max(P, 1), dtype=np.int64)
+    fn(_p(pos_rad), N, _p(_d(view)), _p(_intr(intr)), intr.width, intr.height, _p(start, _I64), _p(gid, _I64), P)
+    return start, gid[:P]
+
+
+def render(pos_rad, col_opa, view, intr, rows=None, mode="f32", want_tainted=False):
+    """(a4) → dict(color [H,W,3], depth, sil, T_final, n_comp, flags [H,W], stats (E_eval,
+    E_comp, P), trace [H,W] (hash of every per-pixel decision), tainted [N] bool or None).
+    `rows=(r0, r1)` renders only those rows."""
+    lib = _load()
+    pos_rad = _d(pos_rad).reshape(-1, 4)
+    col_opa = _d(col_opa).reshape(-1, 4)
+    N = pos_rad.shape[0]
+    W, H = intr.width, intr.height
+    r0, r1 = (0, H) if rows is None else rows
+    color = np.zeros((H, W, 3))
+    depth = np.zeros((H, W))
+    sil = np.zeros((H, W))
+    T_final = np.ones((H, W))
+    n_comp = np.zeros((H, W), dtype=np.int32)
+    flags = np.zeros((H, W), dtype=np.int32)
+    stats = np.zeros(3, dtype=np.int64)
+    tainted = np.zeros(max(N, 1), dtype=np.uint8) if want_tainted else None
+    trace = np.zeros((H, W), dtype=np.uint64)
+    rc = getattr(lib, f"or_render_{mode}")(_p(pos_rad), _p(col_opa), N, _p(_d(view)), _p(_intr(intr)), W, H, r0, r1,
+                                           _p(color), _p(depth), _p(sil), _p(T_final), _p(n_comp, _I32),
+                                           _p(flags, _I32), _p(stats, _I64), _p(tainted, _U8),
+                                           _p(trace, ctypes.POINTER(ctypes.c_uint64)))
+    if rc:
+        raise MemoryError("oracle render")
+    return {"color": color, "depth": depth, "sil": sil, "T_final": T_final, "n_comp": n_comp,
+            "flags": flags.astype(bool), "stats": stats, "trace": trace,
+            "tainted": None if tainted is None else tainted[:N].astype(bool)}
+
+
+def render_bwd(pos_rad, col_opa, view, intr, gC=None, gD=None, gS=None, mode="f32"):
+    """(a5) → dict(d_col_opa [N,4], d_radius [N], d_pose [7], d_geom [N,4] (du,dv,dσ,dz))."""
+    lib = _load()
+    pos_rad = _d(pos_rad).reshape(-1, 4)
+    col_opa = _d(col_opa).reshape(-1, 4)
+    N = pos_rad.shape[0]
+    W, H = intr.width, intr.height
+    gC = None if gC is None else _d(gC).reshape(H, W, 3)
+    gD = None if gD is None else _d(gD).reshape(H, W)
+    gS = None if gS is None else _d(gS).reshape(H, W)
+    d_col_opa = np.zeros((max(N, 1), 4))
+    d_rad = np.zeros(max(N, 1))
+    d_pose = np.zeros(7)
+    d_geom = np.zeros((max(N, 1), 4))
+    rc = getattr(lib, f"or_render_bwd_{mode}")(_p(pos_rad), _p(col_opa), N, _p(_d(view)), _p(_intr(intr)), W, H,
+                                               _p(gC), _p(gD), _p(gS), _p(d_col_opa), _p(d_rad), _p(d_pose),
+                                               _p(d_geom))
+    if rc:
+        raise MemoryError("oracle render_bwd")
+    return {"d_col_opa": d_col_opa[:N], "d_radius": d_rad[:N], "d_pose": d_pose, "d_geom": d_geom[:N]}
+
+
+def l1_upstream(color, depth, sil, target_rgb, target_depth, vis=None, w_color=1.0, w_depth=0.5,
+                color_mask_mode=0, depth_mask_mode=0, normalize=0):
+    """Masked L1 of Eq. 1 / Eq. 2 (no SSIM) → (loss, gC [H,W,3], gD, gS, flags)."""
+    lib = _load()
+    C, D, S = _d(color), _d(depth), _d(sil)
+    tC, tD = _d(target_rgb), _d(target_depth)
+    H, W = D.shape
+    v = None if vis is None else np.ascontiguousarray(np.asarray(vis, dtype=np.uint8))
+    gC = np.zeros((H, W, 3))
+    gD = np.zeros((H, W))
+    gS = np.zeros((H, W))
+    fl = np.zeros((H, W), dtype=np.int32)
+    loss = lib.or_l1_upstream(_p(C), _p(D), _p(S), _p(tC), _p(tD), _p(v, _U8), H * W, float(w_color),
+                              float(w_depth), int(color_mask_mode), int(depth_mask_mode), int(normalize),
+                              _p(gC), _p(gD), _p(gS), _p(fl, _I32))
+    return float(loss), gC, gD, gS, fl.astype(bool)
