@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""bench.py — fwd+bwd render throughput of the view-tied splatting hot path on B200.
+
+Metric (BASELINE.json): "fwd+bwd render Mpix/s & Gaussians/s at 1/2/4/8 B200; fraction of
+roofline".  One STEP = one pass of the whole hot path over one batch of synthetic input:
+projection + tile binning + per-tile sort + compositing (forward), the fused masked-L1 loss,
+and the reverse-order backward to colour / opacity / radius gradients, per rank one
+1200×680 view of BASELINE.json configs[1] (5 keyframes, 4.08M view-tied Gaussians), plus —
+for N > 1 — the NCCL all-reduce of the 5N fp32 gradient buffer over NVLink (batched mapping,
+SURVEY.md §8(e)).  Weak scaling: every rank renders one view per step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config 2]
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the reference arm of
+this tier) on a bounded row band of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "fwd+bwd render Mpix/s & Gaussians/s at 1/2/4/8 B200; fraction of roofline"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0        # B200_PROFILING.md fallback
+SM_COUNT = 148
+FP32_LANES_PER_SM = 128
+# Algorithmic work per unit: FP32 flops per (pixel, Gaussian)
+# evaluation in the forward and per composited pair in the backward (an FMA counts 2).
+FLOPS_PER_EVAL_FWD = 20.0
+FLOPS_PER_COMP_BWD = 60.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="vtgs", choices=["vtgs", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[2, 4, 5])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no clocks / cpu baseline)")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": FALLBACK_HBM_GBS, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------------------
+# reference arm / cpu_baseline: the CPU oracle as it stands, on a bounded row band
+# ----------------------------------------------------------------------------------------
+def oracle_step(cfg, state, view, rows):
+    import oracle
+    pr, co = state
+    tg = cfg.targets[0]
+    wc, wd = cfg.loss_weights
+    r0, r1 = rows
+    img = oracle.render(pr, co, view, cfg.intr, rows=rows)
+    loss, gC, gD, gS, _ = oracle.l1_upstream(img["color"], img["depth"], img["sil"], tg.rgb, tg.depth, None,
+                                              wc, wd, 0, 0, 0)
+    band = np.zeros(img["depth"].shape, dtype=bool)
+    band[r0:r1] = True
+    gC[~band] = 0.0
+    gD[~band] = 0.0
+    g = oracle.render_bwd(pr, co, view, cfg.intr, gC, gD, gS)
+    return loss, g
+
+
+def time_oracle(cfg, steps, warmup, rows):
+    import oracle
+    pr, co, _ = oracle.instantiate(cfg.depth_stack(), cfg.rgb_stack(), cfg.pose_stack(), cfg.intr, cfg.opacity)
+    view = np.asarray(cfg.views[0], dtype=np.float32).astype(np.float64)
+    for _ in range(warmup):
+        oracle_step(cfg, (pr, co), view, rows)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        oracle_step(cfg, (pr, co), view, rows)
+    dt = (time.perf_counter() - t0) / max(steps, 1)
+    px = (rows[1] - rows[0]) * cfg.intr.width
+    return dt, px
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from synth.scenes import make_config
+    cfg = make_config(args.config, args.seed)
+    rows = (cfg.intr.height // 2 - 8, cfg.intr.height // 2 + 8)
+    dt, px = time_oracle(cfg, args.steps, args.warmup, rows)
+    mpix = px / dt / 1e6
+    sample = (f"rows {rows[0]}-{rows[1] - 1} of view 0 ({px} px) per step; full projection + tile lists of all "
+              f"{cfg.n_slots} slots every step (oracle/vtgs_oracle.c, single thread, -O2)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": mpix, "unit": "Mpix/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 decisions / f64 values", "data": "synthetic",
+        "config": workload_config(cfg, args),
+        "gaussians_per_s": cfg.n_slots * (px / (cfg.intr.width * cfg.intr.height)) / dt,
+        "cpu_baseline": {"value": mpix, "unit": "Mpix/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": mpix, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(cfg, args):
+    return {"workload": f"config{args.config}_{cfg.name}_{cfg.intr.width}x{cfg.intr.height}_K{cfg.K}",
+            "n_gaussians": cfg.n_slots, "image": [cfg.intr.width, cfg.intr.height], "views_per_rank": 1,
+            "loss": f"{cfg.loss_weights[0]}*L1(C) + {cfg.loss_weights[1]}*U*L1(D), sum form",
+            "grads": "colour, opacity, radius", "seed": args.seed,
+            "l2": "flushed between timed steps (256 MiB write outside the step events)",
+            "parallelism": f"dp{args.gpus} (view-sharded mapping, NCCL all-reduce of 5N fp32 grads)"}
+
+
+# ----------------------------------------------------------------------------------------
+# the product arm
+# ----------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    from paper_2506_02741_b200 import vtgs
+    from synth.scenes import make_config
+
+    ws, rank, local = dist_env()
+    if args.gpus > 1 and ws == 1:
+        print("for --gpus > 1 launch with torchrun (one rank per GPU)", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = make_config(args.config, args.seed)
+    W, H = cfg.intr.width, cfg.intr.height
+    N = cfg.n_slots
+    R = vtgs.Renderer(local, N, W, H)
+    # the section's Gaussians: every rank instantiates the same keyframes (no broadcast needed)
+    pr, co = R.instantiate(torch.from_numpy(cfg.depth_stack()).to(dev), torch.from_numpy(cfg.rgb_stack()).to(dev),
+                           vtgs.pose_tensor(cfg.pose_stack(), dev), cfg.intr, torch.from_numpy(cfg.opacity).to(dev))
+    # this rank's view: configs 4/5 list their batch of views; config 2 renders its keyframe 2 view at N=1
+    # and, with more ranks, keyframe (2 + rank) mod K (one view per rank, weak scaling)
+    if args.config == 2:
+        k = (2 + rank) % cfg.K
+        view_np = np.asarray(cfg.keyframes[k].pose, dtype=np.float32)
+        tgt = cfg.keyframes[k]
+    else:
+        k = rank % len(cfg.views)
+        view_np = np.asarray(cfg.views[k], dtype=np.float32)
+        tgt = cfg.targets[k]
+    view = vtgs.pose_tensor(view_np, dev)
+    t_rgb = torch.from_numpy(tgt.rgb).to(dev)
+    t_depth = torch.from_numpy(tgt.depth).to(dev)
+    wc, wd = cfg.loss_weights
+    loss_spec = dict(target_rgb=t_rgb, target_depth=t_depth, w_color=wc, w_depth=wd, color_mask_mode=0,
+                     depth_mask_mode=0, normalize=0)
+    grads = torch.zeros(5 * N, device=dev)                  # d_col_opa (4N) | d_radius (N): one all-reduce
+    d_co = grads[:4 * N].view(N, 4)
+    d_r = grads[4 * N:]
+    out = (torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev), torch.empty((H, W), device=dev))
+    loss_out = torch.zeros(1, device=dev)
+    want = vtgs.VTGS_GRAD_ATTR
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        grads.zero_()
+        R.render_fwd(pr, co, view, cfg.intr, out=out)
+        R.render_bwd(want, d_col_opa=d_co, d_radius=d_r, loss=loss_spec, loss_out=loss_out)
+        if ws > 1:
+            dist.all_reduce(grads)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    st = R.stats()
+    assert st["overflow"] == 0, "tile-pair capacity exceeded"
+
+    # ---------------- timed region
+    R.set_profiling(True)
+    R.profile()                                            # reset
+    launches0 = R.stats()["launches"]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local) if not args.profile_run else None
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    for i in range(args.steps):
+        flush.fill_(float(i))                               # evict L2 between steps (not timed)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+    launches = R.stats()["launches"] - launches0
+    prof = R.profile()
+    R.set_profiling(False)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(sum(step_ms) / len(step_ms))
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    px_per_step = ws * W * H
+    value = px_per_step / (ms_max * 1e-3) / 1e6
+    gps = ws * N / (ms_max * 1e-3)
+
+    # ---------------- roofline of the dominant kernel (event-timed inside the timed region)
+    stats = R.stats()
+    peaks, peak_src = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = SM_COUNT * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12       # TFLOP/s at max clock
+    hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
+    per_launch = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
+    P = stats["n_pairs"]
+    HW = W * H
+    # algorithmic work per launch
+    work = {
+        "project_count": ("hbm", (16 + 16 + 8) * N),                 # pos_rad in, proj + rect out
+        "emit_pairs": ("hbm", 24 * N + 8 * P),                       # proj + rect in, (key, gid) out
+        "tile_sort": ("hbm", 12 * P),                                # (key, gid) in, gid out
+        "composite_fwd": ("alu", FLOPS_PER_EVAL_FWD * stats["e_eval"]),
+        "composite_bwd": ("alu", FLOPS_PER_COMP_BWD * stats["e_comp"]),
+    }
+    stage_json = {}
+    for k, (ms_k, cnt) in prof.items():
+        if cnt == 0:
+            continue
+        e = {"ms_per_launch": per_launch[k], "launches": cnt, "share": ms_k / max(sum(v[0] for v in prof.values()), 1e-9)}
+        if k in work:
+            bound, units = work[k]
+            if bound == "hbm":
+                ach = units / (per_launch[k] * 1e-3) / 1e9
+                e.update(bound="hbm", achieved=ach, unit="GB/s", frac=ach / hbm_peak)
+            else:
+                ach = units / (per_launch[k] * 1e-3) / 1e12
+                e.update(bound="alu", achieved=ach, unit="TFLOP/s", frac=ach / fp32_peak)
+        stage_json[k] = e
+    dom = max((k for k in stage_json if k in work), key=lambda k: stage_json[k]["share"])
+    d = stage_json[dom]
+    roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"],
+                "peak": hbm_peak if d["bound"] == "hbm" else fp32_peak, "unit": d["unit"], "frac": d["frac"],
+                "traffic": None,
+                "peak_source": (f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
+                                f"FP32 {SM_COUNT} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz "
+                                f"(B200_PROFILING.md unit counts, max clock)")}
+
+    # ---------------- e2e: the same step through the C-ABI with HOST buffers
+    e2e = None
+    if not args.profile_run:
+        h_rgb = torch.from_numpy(tgt.rgb).pin_memory()
+        h_depth = torch.from_numpy(tgt.depth).pin_memory()
+        h_view = torch.from_numpy(view_np.reshape(7).copy()).pin_memory()
+        for _ in range(2):
+            grads.zero_()
+            R.step_host(pr, co, h_view, cfg.intr, h_rgb, h_depth, wc, wd, 0, 0, 0, want, (0, N), out, d_co, d_r)
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            grads.zero_()
+            R.step_host(pr, co, h_view, cfg.intr, h_rgb, h_depth, wc, wd, 0, 0, 0, want, (0, N), out, d_co, d_r)
+            if ws > 1:
+                dist.all_reduce(grads)
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        te = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = float(te.item())
+        e2e = {"value": px_per_step / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(h_rgb.numel() * 4 + h_depth.numel() * 4 + 28),
+               "d2h_bytes_per_step": 4,
+               "api": "vtgs_step_host (host target RGB-D + pose in, host loss out)"}
+
+    # ---------------- cpu baseline (oracle as it stands, bounded sample, rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_run:
+        rows = (H // 2 - 8, H // 2 + 8)
+        dt, px = time_oracle(cfg, 1, 0, rows)
+        cpu = {"value": px / dt / 1e6, "unit": "Mpix/s", "cores": 1, "kind": "oracle",
+               "sample": f"rows {rows[0]}-{rows[1] - 1} ({px} px) of the same view; projection + tile lists of all "
+                         f"{N} slots, render, L1, backward; single-threaded C (oracle/vtgs_oracle.c)",
+               "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded procedural rooms, ray-cast RGB-D; stands in for Replica/TUM/ScanNet)",
+            "config": workload_config(cfg, args),
+            "gaussians_per_s": gps,
+            "roofline": roofline,
+            "stages": stage_json,
+            "work": {"n_pairs": P, "e_eval": stats["e_eval"], "e_comp": stats["e_comp"], "max_tile": stats["max_tile"]},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+            "gpu_launches": int(launches),
+            "loss": float(loss_out.item()),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -59,10 +59,10 @@ def _load():
             f = getattr(lib, f"or_render_{m}")
             f.restype = ctypes.c_int
             f.argtypes = [_D, _D, ctypes.c_int64, _D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                          _D, _D, _D, _D, _I32, _I32, _I64, _U8, ctypes.POINTER(ctypes.c_uint64)]
+                          _D, _D, _D, _D, _I32, _I32, _I64, _U8, ctypes.POINTER(ctypes.c_uint64), _I32]
             f = getattr(lib, f"or_render_bwd_{m}")
             f.restype = ctypes.c_int
-            f.argtypes = [_D, _D, ctypes.c_int64, _D, _D, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D, _D, _D, _D]
+            f.argtypes = [_D, _D, ctypes.c_int64, _D, _D, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D, _D, _D, _D, _D]
         f = lib.or_l1_upstream
         f.restype = ctypes.c_double
         f.argtypes = [_D, _D, _D, _D, _D, _U8, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
@@ -128,10 +128,11 @@ def tile_lists(pos_rad, view, intr, mode="f32"):
     return start, gid[:P]
 
 
-def render(pos_rad, col_opa, view, intr, rows=None, mode="f32", want_tainted=False):
+def render(pos_rad, col_opa, view, intr, rows=None, mode="f32", want_tainted=False, extra_flags=None):
     """(a4) → dict(color [H,W,3], depth, sil, T_final, n_comp, flags [H,W], stats (E_eval,
     E_comp, P), trace [H,W] (hash of every per-pixel decision), tainted [N] bool or None).
-    `rows=(r0, r1)` renders only those rows."""
+    `rows=(r0, r1)` renders only those rows; `extra_flags` [H,W] marks further pixels flagged
+    (their Gaussians are tainted too)."""
     lib = _load()
     pos_rad = _d(pos_rad).reshape(-1, 4)
     col_opa = _d(col_opa).reshape(-1, 4)
@@ -147,19 +148,23 @@ def render(pos_rad, col_opa, view, intr, rows=None, mode="f32", want_tainted=Fal
     stats = np.zeros(3, dtype=np.int64)
     tainted = np.zeros(max(N, 1), dtype=np.uint8) if want_tainted else None
     trace = np.zeros((H, W), dtype=np.uint64)
+    ext = None if extra_flags is None else np.ascontiguousarray(np.asarray(extra_flags, dtype=np.int32))
     rc = getattr(lib, f"or_render_{mode}")(_p(pos_rad), _p(col_opa), N, _p(_d(view)), _p(_intr(intr)), W, H, r0, r1,
                                            _p(color), _p(depth), _p(sil), _p(T_final), _p(n_comp, _I32),
                                            _p(flags, _I32), _p(stats, _I64), _p(tainted, _U8),
-                                           _p(trace, ctypes.POINTER(ctypes.c_uint64)))
+                                           _p(trace, ctypes.POINTER(ctypes.c_uint64)), _p(ext, _I32))
     if rc:
         raise MemoryError("oracle render")
+    if ext is not None:
+        flags |= ext != 0
     return {"color": color, "depth": depth, "sil": sil, "T_final": T_final, "n_comp": n_comp,
             "flags": flags.astype(bool), "stats": stats, "trace": trace,
             "tainted": None if tainted is None else tainted[:N].astype(bool)}
 
 
 def render_bwd(pos_rad, col_opa, view, intr, gC=None, gD=None, gS=None, mode="f32"):
-    """(a5) → dict(d_col_opa [N,4], d_radius [N], d_pose [7], d_geom [N,4] (du,dv,dσ,dz))."""
+    """(a5) → dict(d_col_opa [N,4], d_radius [N], d_pose [7], d_geom [N,4] (du,dv,dσ,dz),
+    d_abs [N,5] (Σ of |per-pixel contributions| to dc0..2, do, dr))."""
     lib = _load()
     pos_rad = _d(pos_rad).reshape(-1, 4)
     col_opa = _d(col_opa).reshape(-1, 4)
@@ -172,12 +177,14 @@ def render_bwd(pos_rad, col_opa, view, intr, gC=None, gD=None, gS=None, mode="f3
     d_rad = np.zeros(max(N, 1))
     d_pose = np.zeros(7)
     d_geom = np.zeros((max(N, 1), 4))
+    d_abs = np.zeros((max(N, 1), 5))
     rc = getattr(lib, f"or_render_bwd_{mode}")(_p(pos_rad), _p(col_opa), N, _p(_d(view)), _p(_intr(intr)), W, H,
                                                _p(gC), _p(gD), _p(gS), _p(d_col_opa), _p(d_rad), _p(d_pose),
-                                               _p(d_geom))
+                                               _p(d_geom), _p(d_abs))
     if rc:
         raise MemoryError("oracle render_bwd")
-    return {"d_col_opa": d_col_opa[:N], "d_radius": d_rad[:N], "d_pose": d_pose, "d_geom": d_geom[:N]}
+    return {"d_col_opa": d_col_opa[:N], "d_radius": d_rad[:N], "d_pose": d_pose, "d_geom": d_geom[:N],
+            "d_abs": d_abs[:N]}
 
 
 def l1_upstream(color, depth, sil, target_rgb, target_depth, vis=None, w_color=1.0, w_depth=0.5,

@@ -59,7 +59,7 @@
  * count ("mean absolute difference over masked pixels"; empty mask → 0).
  * Upstream gradients are the subgradient with sgn(0) = 0.
  * Returns the loss value; writes gC (H×W×3), gD, gS (gS ≡ 0).  `flag` (H×W, may be NULL) is
- * set where a residual is nonzero but within 1e-5 of 0, or S within 1e-5 of 0.99, i.e. where
+ * set where a residual is nonzero but within 5e-5 of 0, or S within 1e-5 of 0.99, i.e. where
  * the kernel's fp32 render could take the other branch of sgn or of the mask.  (A residual
  * that is exactly 0 — e.g. a clipped black target rendered from black Gaussians — is exactly 0
  * in fp32 too.)
@@ -87,12 +87,12 @@ double or_l1_upstream(const double *C, const double *D, const double *S, const d
         int fl = (color_mask_mode || depth_mask_mode) && U && fabs(S[p] - 0.99) < 1e-5;
         for (int c = 0; c < 3; ++c) {
             const double r = C[3 * p + c] - tC[3 * p + c];
-            if (mc && r != 0.0 && fabs(r) < 1e-5) fl = 1;
+            if (mc && r != 0.0 && fabs(r) < 5e-5) fl = 1;
             gC[3 * p + c] = mc ? w_color * sc * (double)((r > 0) - (r < 0)) : 0.0;
             loss += mc ? w_color * sc * fabs(r) : 0.0;
         }
         const double r = D[p] - tD[p];
-        if (md && r != 0.0 && fabs(r) < 1e-5) fl = 1;
+        if (md && r != 0.0 && fabs(r) < 5e-5) fl = 1;
         gD[p] = md ? w_depth * sd * (double)((r > 0) - (r < 0)) : 0.0;
         loss += md ? w_depth * sd * fabs(r) : 0.0;
         gS[p] = 0.0;

@@ -1,0 +1,368 @@
+// abi.cu — the C ABI of include/vtgs.h: argument validation, context / scratch ownership,
+// error capture.  No arithmetic of the method lives here; every step runs in the kernels of
+// instantiate.cu, forward.cu and backward.cu.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "vtgs_internal.cuh"
+
+using vtgs::Ctx;
+
+struct vtgs_ctx {
+    Ctx c;
+};
+
+namespace {
+
+vtgs_status fail(vtgs_ctx *ctx, vtgs_status s, const char *fmt, ...) __attribute__((format(printf, 3, 4)));
+
+vtgs_status fail(vtgs_ctx *ctx, vtgs_status s, const char *fmt, ...) {
+    if (ctx) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(ctx->c.last_error, sizeof(ctx->c.last_error), fmt, ap);
+        va_end(ap);
+    }
+    return s;
+}
+
+vtgs_status cuda_fail(vtgs_ctx *ctx, cudaError_t e, const char *where) {
+    return fail(ctx, VTGS_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+vtgs_status check_intr(vtgs_ctx *ctx, const vtgs_intrinsics &in) {
+    if (in.width <= 0 || in.height <= 0 || in.width > ctx->c.max_w || in.height > ctx->c.max_h)
+        return fail(ctx, VTGS_ERR_SHAPE, "image %dx%d outside the context's 1..%dx%d", in.width, in.height,
+                    ctx->c.max_w, ctx->c.max_h);
+    if (!(in.fx > 0.0f) || !(in.fy > 0.0f) || !(in.cx > 0.0f) || !(in.cx < (float)in.width) ||
+        !(in.cy > 0.0f) || !(in.cy < (float)in.height))
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "intrinsics need fx, fy > 0, 0 < cx < W, 0 < cy < H (SPEC.md:25)");
+    return VTGS_OK;
+}
+
+template <typename T>
+cudaError_t dalloc(T **p, size_t n) {
+    return cudaMalloc((void **)p, sizeof(T) * (n ? n : 1));
+}
+
+void free_all(Ctx &c) {
+    void *ptrs[] = {c.proj, c.rect, c.tile_count, c.tile_start, c.tile_cursor, c.keys, c.vals, c.keys2,
+                    c.vals2, c.offs, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t vtgs_abi_version(void) { return VTGS_ABI_VERSION; }
+
+const char *vtgs_status_string(vtgs_status s) {
+    switch (s) {
+        case VTGS_OK: return "ok";
+        case VTGS_ERR_INVALID_ARG: return "invalid argument";
+        case VTGS_ERR_SHAPE: return "shape / size out of range";
+        case VTGS_ERR_CAPACITY: return "tile-pair capacity exceeded";
+        case VTGS_ERR_CUDA: return "CUDA error";
+        case VTGS_ERR_STATE: return "backward without a forward";
+        case VTGS_ERR_NO_DEVICE: return "no CUDA device (there is no CPU fallback)";
+        default: return "unknown status";
+    }
+}
+
+const char *vtgs_last_error(const vtgs_ctx *ctx) { return ctx ? ctx->c.last_error : ""; }
+
+vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, int32_t max_width,
+                        int32_t max_height, int64_t max_pairs) {
+    if (!out) return VTGS_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (max_gaussians < 0 || max_gaussians > 0xffffffffLL || max_width <= 0 || max_height <= 0 ||
+        max_width > 65535 || max_height > 65535)
+        return VTGS_ERR_SHAPE;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return VTGS_ERR_NO_DEVICE;
+    }
+    if (device < 0 || device >= ndev) return VTGS_ERR_INVALID_ARG;
+    if (max_pairs <= 0) max_pairs = 4 * (max_gaussians > 0 ? max_gaussians : 1);
+    if (max_pairs > 0xfffffff0LL) max_pairs = 0xfffffff0LL;
+    vtgs_ctx *ctx = new (std::nothrow) vtgs_ctx();
+    if (!ctx) return VTGS_ERR_CUDA;
+    Ctx &c = ctx->c;
+    c.device = device;
+    c.max_gaussians = max_gaussians;
+    c.max_w = max_width;
+    c.max_h = max_height;
+    c.max_pairs = max_pairs;
+    c.max_tiles = ((max_width + 15) / 16) * ((max_height + 15) / 16);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaError_t e = cudaSetDevice(device);
+    const size_t px = (size_t)max_width * max_height;
+    if (!e) e = cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (!e) e = dalloc(&c.proj, (size_t)max_gaussians);
+    if (!e) e = dalloc(&c.rect, (size_t)max_gaussians);
+    if (!e) e = dalloc(&c.tile_count, (size_t)c.max_tiles);
+    if (!e) e = dalloc(&c.tile_start, (size_t)c.max_tiles + 1);
+    if (!e) e = dalloc(&c.tile_cursor, (size_t)c.max_tiles);
+    if (!e) e = dalloc(&c.keys, (size_t)max_pairs);
+    if (!e) e = dalloc(&c.vals, (size_t)max_pairs);
+    if (!e) e = dalloc(&c.keys2, (size_t)max_pairs);
+    if (!e) e = dalloc(&c.vals2, (size_t)max_pairs);
+    if (!e) e = dalloc(&c.offs, (size_t)max_pairs);
+    if (!e) e = dalloc(&c.T_final, px);
+    if (!e) e = dalloc(&c.last, px);
+    if (!e) e = dalloc(&c.partials, (size_t)c.max_tiles * 16);
+    if (!e) e = dalloc(&c.dev, 1);
+    if (!e) e = dalloc(&c.host_io, 4 * px + 64);
+    if (!e) e = dalloc(&c.view_copy, 1);
+    if (!e) e = cudaMemset(c.dev, 0, sizeof(vtgs::DevScalars));
+    if (!e) e = cudaMemset(c.tile_count, 0, sizeof(uint32_t) * c.max_tiles);
+    if (!e) e = cudaMemset(c.tile_start, 0, sizeof(uint32_t) * (c.max_tiles + 1));
+    if (!e) e = vtgs::forward_set_attributes();
+    if (!e) e = cudaDeviceSynchronize();
+    cudaSetDevice(prev);
+    if (e) {
+        cudaGetLastError();
+        free_all(c);
+        delete ctx;
+        return e == cudaErrorMemoryAllocation ? VTGS_ERR_CAPACITY : VTGS_ERR_CUDA;
+    }
+    *out = ctx;
+    return VTGS_OK;
+}
+
+vtgs_status vtgs_destroy(vtgs_ctx *ctx) {
+    if (!ctx) return VTGS_OK;
+    cudaSetDevice(ctx->c.device);
+    cudaDeviceSynchronize();
+    for (auto *v : {&ctx->c.prof, &ctx->c.prof_free})
+        for (auto &ev : *v) {
+            cudaEventDestroy(ev.a);
+            cudaEventDestroy(ev.b);
+        }
+    free_all(ctx->c);
+    delete ctx;
+    return VTGS_OK;
+}
+
+vtgs_status vtgs_instantiate(vtgs_ctx *ctx, const float *depth, const float *rgb,
+                             const vtgs_pose *kf_poses, int32_t K, vtgs_intrinsics intr,
+                             const float *opacity_init, float opacity_default, float *pos_rad,
+                             float *col_opa, void *stream) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    ctx->c.last_error[0] = 0;
+    vtgs_status st = check_intr(ctx, intr);
+    if (st) return st;
+    if (K < 0) return fail(ctx, VTGS_ERR_SHAPE, "K = %d < 0", K);
+    const int64_t N = (int64_t)K * intr.width * intr.height;
+    if (N > ctx->c.max_gaussians)
+        return fail(ctx, VTGS_ERR_SHAPE, "K·H·W = %lld exceeds max_gaussians %lld", (long long)N,
+                    (long long)ctx->c.max_gaussians);
+    if (K == 0) return VTGS_OK;
+    if (!depth || !rgb || !kf_poses || !pos_rad || !col_opa)
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "NULL depth / rgb / kf_poses / pos_rad / col_opa");
+    if (!aligned16(pos_rad) || !aligned16(col_opa))
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "pos_rad / col_opa must be 16-byte aligned float4 arrays");
+    cudaSetDevice(ctx->c.device);
+    cudaError_t e = vtgs::launch_instantiate(ctx->c, depth, rgb, kf_poses, K, intr, opacity_init, opacity_default,
+                                             (float4 *)pos_rad, (float4 *)col_opa, (cudaStream_t)stream);
+    return e ? cuda_fail(ctx, e, "vtgs_instantiate") : VTGS_OK;
+}
+
+vtgs_status vtgs_render_fwd(vtgs_ctx *ctx, const float *pos_rad, const float *col_opa, int64_t N,
+                            const vtgs_pose *view, vtgs_intrinsics intr, float *color, float *depth,
+                            float *silhouette, void *stream) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    c.last_error[0] = 0;
+    vtgs_status st = check_intr(ctx, intr);
+    if (st) return st;
+    if (N < 0 || N > c.max_gaussians)
+        return fail(ctx, VTGS_ERR_SHAPE, "N = %lld outside 0..max_gaussians %lld", (long long)N,
+                    (long long)c.max_gaussians);
+    if ((N > 0 && (!pos_rad || !col_opa)) || !view || !color || !depth || !silhouette)
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "NULL state / view / output pointer");
+    if (!aligned16(pos_rad) || !aligned16(col_opa))
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "pos_rad / col_opa must be 16-byte aligned float4 arrays");
+    c.have_fwd = false;
+    c.pos_rad = (const float4 *)pos_rad;
+    c.col_opa = (const float4 *)col_opa;
+    c.N = N;
+    c.view = view;
+    c.intr = intr;
+    c.color = color;
+    c.depth = depth;
+    c.sil = silhouette;
+    cudaSetDevice(c.device);
+    cudaError_t e = vtgs::launch_forward(c, (cudaStream_t)stream);
+    if (e) return cuda_fail(ctx, e, "vtgs_render_fwd");
+    c.have_fwd = true;
+    return VTGS_OK;
+}
+
+vtgs_status vtgs_render_bwd(vtgs_ctx *ctx, const float *dL_dcolor, const float *dL_ddepth,
+                            const float *dL_dsil, const vtgs_l1_loss *loss, uint32_t want,
+                            int64_t learn_begin, int64_t learn_end, float *d_col_opa,
+                            float *d_radius, float *d_pose, float *loss_out, void *stream) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    c.last_error[0] = 0;
+    if (!c.have_fwd) return fail(ctx, VTGS_ERR_STATE, "vtgs_render_bwd before any vtgs_render_fwd");
+    if (want & ~0xfu) return fail(ctx, VTGS_ERR_INVALID_ARG, "unknown bits in want = 0x%x", want);
+    if (loss && (dL_dcolor || dL_ddepth || dL_dsil))
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "pass either upstream gradients or a fused loss, not both");
+    if (loss && (!loss->target_rgb || !loss->target_depth))
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "fused loss needs target_rgb and target_depth");
+    if (loss_out && !loss) return fail(ctx, VTGS_ERR_INVALID_ARG, "loss_out requires a fused loss");
+    if ((want & (VTGS_GRAD_COLOR | VTGS_GRAD_OPACITY)) && !d_col_opa)
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "colour/opacity gradients wanted but d_col_opa is NULL");
+    if ((want & VTGS_GRAD_RADIUS) && !d_radius)
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "radius gradient wanted but d_radius is NULL");
+    if ((want & VTGS_GRAD_POSE) && !d_pose)
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "pose gradient wanted but d_pose is NULL");
+    if (d_col_opa && !aligned16(d_col_opa))
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "d_col_opa must be a 16-byte aligned float4 array");
+    if (learn_begin < 0) learn_begin = 0;
+    if (learn_end > c.N) learn_end = c.N;
+    cudaSetDevice(c.device);
+    cudaError_t e = vtgs::launch_backward(c, dL_dcolor, dL_ddepth, dL_dsil, loss, want, learn_begin, learn_end,
+                                          (float4 *)d_col_opa, d_radius, d_pose, loss_out, (cudaStream_t)stream);
+    return e ? cuda_fail(ctx, e, "vtgs_render_bwd") : VTGS_OK;
+}
+
+vtgs_status vtgs_pose_adam_step(vtgs_ctx *ctx, vtgs_pose *pose, const float *d_pose, float *adam_state,
+                                float lr_rot, float lr_trans, void *stream) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    ctx->c.last_error[0] = 0;
+    if (!pose || !d_pose || !adam_state) return fail(ctx, VTGS_ERR_INVALID_ARG, "NULL pose / d_pose / state");
+    cudaSetDevice(ctx->c.device);
+    cudaError_t e = vtgs::launch_pose_adam(ctx->c, pose, d_pose, adam_state, lr_rot, lr_trans, (cudaStream_t)stream);
+    return e ? cuda_fail(ctx, e, "vtgs_pose_adam_step") : VTGS_OK;
+}
+
+vtgs_status vtgs_get_stats(vtgs_ctx *ctx, vtgs_stats *out, void *stream) {
+    if (!ctx || !out) return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    vtgs::DevScalars d;
+    cudaError_t e = cudaMemcpyAsync(&d, c.dev, sizeof(d), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e) return cuda_fail(ctx, e, "vtgs_get_stats");
+    out->n_gaussians = c.N;
+    out->n_pairs = (int64_t)d.n_pairs;
+    out->e_eval = (int64_t)d.e_eval;
+    out->e_comp = (int64_t)d.e_comp;
+    out->max_tile = d.max_tile;
+    out->overflow = d.overflow;
+    out->launches = c.launches;
+    return d.overflow ? fail(ctx, VTGS_ERR_CAPACITY, "P = %llu pairs > max_pairs %lld", d.n_pairs,
+                             (long long)c.max_pairs)
+                      : VTGS_OK;
+}
+
+vtgs_status vtgs_set_profiling(vtgs_ctx *ctx, int32_t enable) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    ctx->c.profiling = enable != 0;
+    return VTGS_OK;
+}
+
+vtgs_status vtgs_get_profile(vtgs_ctx *ctx, double *ms, int64_t *counts, void *stream) {
+    if (!ctx || !ms) return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    cudaSetDevice(c.device);
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (!e) e = cudaDeviceSynchronize();
+    if (e) return cuda_fail(ctx, e, "vtgs_get_profile");
+    for (int i = 0; i < VTGS_NUM_STAGES; ++i) ms[i] = 0.0;
+    for (auto &ev : c.prof) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, ev.a, ev.b) == cudaSuccess) ms[ev.stage] += t;
+        c.prof_free.push_back(ev);
+    }
+    cudaGetLastError();
+    c.prof.clear();
+    for (int i = 0; i < VTGS_NUM_STAGES; ++i) {
+        if (counts) counts[i] = c.prof_counts[i];
+        c.prof_counts[i] = 0;
+    }
+    return VTGS_OK;
+}
+
+vtgs_status vtgs_check(vtgs_ctx *ctx, void *stream) {
+    vtgs_stats s;
+    return vtgs_get_stats(ctx, &s, stream);
+}
+
+vtgs_status vtgs_export_tiles(vtgs_ctx *ctx, int64_t *tile_start, int32_t *sorted_gid, int64_t cap,
+                              int64_t *P_out, void *stream) {
+    if (!ctx || !tile_start || !P_out) return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    if (!c.have_fwd) return fail(ctx, VTGS_ERR_STATE, "no forward to export");
+    const int T = ((c.intr.width + 15) / 16) * ((c.intr.height + 15) / 16);
+    cudaSetDevice(c.device);
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t *st = new uint32_t[T + 1];
+    cudaError_t e = cudaMemcpyAsync(st, c.tile_start, sizeof(uint32_t) * (T + 1), cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (e) {
+        delete[] st;
+        return cuda_fail(ctx, e, "vtgs_export_tiles");
+    }
+    for (int i = 0; i <= T; ++i) tile_start[i] = st[i];
+    const int64_t P = st[T];
+    delete[] st;
+    *P_out = P;
+    if (sorted_gid && P <= cap && P > 0) {
+        e = cudaMemcpyAsync(sorted_gid, c.vals, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, s);
+        if (!e) e = cudaStreamSynchronize(s);
+        if (e) return cuda_fail(ctx, e, "vtgs_export_tiles");
+    }
+    return vtgs_check(ctx, stream);
+}
+
+vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col_opa, int64_t N,
+                           const vtgs_pose *view_host, vtgs_intrinsics intr,
+                           const float *target_rgb_host, const float *target_depth_host, float w_color,
+                           float w_depth, int32_t color_mask_mode, int32_t depth_mask_mode,
+                           int32_t normalize, uint32_t want, int64_t learn_begin, int64_t learn_end,
+                           float *color, float *depth, float *silhouette, float *d_col_opa,
+                           float *d_radius, float *loss_host, float *d_pose_host, void *stream) {
+    if (!ctx || !view_host || !target_rgb_host || !target_depth_host || !loss_host)
+        return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    vtgs_status st = check_intr(ctx, intr);
+    if (st) return st;
+    const size_t px = (size_t)intr.width * intr.height;
+    float *d_rgb = c.host_io;                       // 3·px
+    float *d_dep = c.host_io + 3 * px;              // px
+    float *d_misc = c.host_io + 4 * px;             // 64 floats: pose(8) | loss(1) | d_pose(7)
+    vtgs_pose *d_view = (vtgs_pose *)d_misc;
+    float *d_loss = d_misc + 8;
+    float *d_dpose = d_misc + 16;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaSetDevice(c.device);
+    cudaError_t e = cudaMemcpyAsync(d_rgb, target_rgb_host, sizeof(float) * 3 * px, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemcpyAsync(d_dep, target_depth_host, sizeof(float) * px, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemcpyAsync(d_view, view_host, sizeof(vtgs_pose), cudaMemcpyHostToDevice, s);
+    if (e) return cuda_fail(ctx, e, "vtgs_step_host (H2D)");
+    st = vtgs_render_fwd(ctx, pos_rad, col_opa, N, d_view, intr, color, depth, silhouette, stream);
+    if (st) return st;
+    vtgs_l1_loss L{d_rgb, d_dep, nullptr, w_color, w_depth, color_mask_mode, depth_mask_mode, normalize};
+    st = vtgs_render_bwd(ctx, nullptr, nullptr, nullptr, &L, want, learn_begin, learn_end, d_col_opa, d_radius,
+                         (want & VTGS_GRAD_POSE) ? d_dpose : nullptr, d_loss, stream);
+    if (st) return st;
+    e = cudaMemcpyAsync(loss_host, d_loss, sizeof(float), cudaMemcpyDeviceToHost, s);
+    if (!e && d_pose_host && (want & VTGS_GRAD_POSE))
+        e = cudaMemcpyAsync(d_pose_host, d_dpose, sizeof(float) * 7, cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    return e ? cuda_fail(ctx, e, "vtgs_step_host (D2H)") : VTGS_OK;
+}
+
+}  // extern "C"

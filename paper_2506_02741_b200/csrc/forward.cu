@@ -1,0 +1,525 @@
+// (2)–(4) Forward render: projection + 16×16 tile binning, per-tile depth sort, per-tile
+// front-to-back compositing.  PAPER.md:146 (Eq. 1 `splat`), SPEC.md:124-150, :169-175,
+// BASELINE.json north_star parts (2)-(4).
+//
+// Launch sequence (all on the caller's stream, no host synchronisation, graph-capturable):
+//   memset(tile_count) → k_project_count → k_scan_tiles → k_emit_pairs → k_tile_sort
+//   → k_composite_fwd
+// Pairs are bucketed by tile with warp-aggregated atomics (one global atomic per distinct tile
+// per warp), then each tile's bucket is sorted in shared memory by (z bits, gid) — one
+// bucket-scatter pass plus an on-chip sort instead of a multi-pass global 64-bit radix sort
+// (K4/K5).
+#include "vtgs_internal.cuh"
+
+namespace vtgs {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ------------------------------------------------------------------------------------------
+// K2: projection, culling, footprint rect, tile counts.  DESIGN.md §3 steps 3-5.
+// ------------------------------------------------------------------------------------------
+struct Footprint {
+    bool vis;
+    float u, v, z, s;
+    bool clamped;
+    int x0, y0, x1, y1;
+};
+
+__device__ __forceinline__ Footprint project_one(float4 pr, const PoseR &P, const vtgs_intrinsics &in,
+                                                 float fmean, float Wm1, float Hm1) {
+    Footprint f;
+    f.vis = false;
+    float xc[3];
+    view_transform(P.R, P.t, pr, xc);
+    const float z = xc[2];
+    if (!(pr.w > 0.0f) || !(z > kNearClip)) return f;
+    const float u = __fadd_rn(__fdiv_rn(__fmul_rn(in.fx, xc[0]), z), in.cx);
+    const float v = __fadd_rn(__fdiv_rn(__fmul_rn(in.fy, xc[1]), z), in.cy);
+    if (!isfinite(u) || !isfinite(v)) return f;
+    const float s0 = __fdiv_rn(__fmul_rn(fmean, pr.w), z);
+    const bool clamped = s0 < kSigmaMin;
+    const float s = clamped ? kSigmaMin : s0;
+    const float e = __fmul_rn(3.0f, s);
+    if (__fadd_rn(u, e) < 0.0f || __fsub_rn(u, e) > Wm1 || __fadd_rn(v, e) < 0.0f || __fsub_rn(v, e) > Hm1)
+        return f;
+    const float cx0 = ceilf(__fsub_rn(u, e)), cx1 = floorf(__fadd_rn(u, e));
+    const float cy0 = ceilf(__fsub_rn(v, e)), cy1 = floorf(__fadd_rn(v, e));
+    f.x0 = cx0 < 0.0f ? 0 : (int)cx0;
+    f.x1 = cx1 > Wm1 ? (int)Wm1 : (int)cx1;
+    f.y0 = cy0 < 0.0f ? 0 : (int)cy0;
+    f.y1 = cy1 > Hm1 ? (int)Hm1 : (int)cy1;
+    if (f.x0 > f.x1 || f.y0 > f.y1) return f;
+    f.vis = true;
+    f.u = u; f.v = v; f.z = z; f.s = s; f.clamped = clamped;
+    return f;
+}
+
+__global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict__ pos_rad, int64_t N,
+                                                       const vtgs_pose *__restrict__ view,
+                                                       vtgs_intrinsics in, int ntx,
+                                                       float4 *__restrict__ proj,
+                                                       uint2 *__restrict__ rect,
+                                                       uint32_t *__restrict__ tile_count) {
+    __shared__ PoseR P;
+    if (threadIdx.x == 0) pose_rotation(*view, P);
+    __syncthreads();
+    const float fmean = __fmul_rn(0.5f, __fadd_rn(in.fx, in.fy));
+    const float Wm1 = (float)(in.width - 1), Hm1 = (float)(in.height - 1);
+    const int64_t Nr = (N + 31) & ~(int64_t)31;  // whole warps iterate together
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < Nr; g += stride) {
+        Footprint f;
+        f.vis = false;
+        if (g < N) {
+            f = project_one(pos_rad[g], P, in, fmean, Wm1, Hm1);
+            proj[g] = f.vis ? make_float4(f.u, f.v, f.z, f.clamped ? -f.s : f.s) : make_float4(0.f, 0.f, 0.f, 0.f);
+            rect[g] = f.vis ? make_uint2((uint32_t)f.x0 | ((uint32_t)f.x1 << 16), (uint32_t)f.y0 | ((uint32_t)f.y1 << 16))
+                            : make_uint2(0xffffffffu, 0xffffffffu);
+        }
+        const int tx0 = f.vis ? f.x0 >> 4 : 0, ty0 = f.vis ? f.y0 >> 4 : 0;
+        const int ntg = f.vis ? (f.x1 >> 4) - tx0 + 1 : 0;
+        const int cnt = f.vis ? ntg * ((f.y1 >> 4) - ty0 + 1) : 0;
+        for (int k = 0; __any_sync(kFull, k < cnt); ++k) {
+            int tile = -1;
+            if (k < cnt) {
+                const int dy = k / ntg;
+                tile = (ty0 + dy) * ntx + tx0 + (k - dy * ntg);
+            }
+            const unsigned peers = __match_any_sync(kFull, tile);
+            if (tile >= 0 && (int)lane_id() == __ffs(peers) - 1) atomicAdd(&tile_count[tile], (uint32_t)__popc(peers));
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K3: exclusive scan of the tile counts (one CTA; ≤ a few thousand tiles).  On capacity
+// overflow every count is zeroed (the render is empty) and the overflow flag is raised.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t *__restrict__ tile_count,
+                                                     uint32_t *__restrict__ tile_start,
+                                                     uint32_t *__restrict__ cursor, int T,
+                                                     unsigned long long cap,
+                                                     DevScalars *__restrict__ dev,
+                                                     const vtgs_pose *__restrict__ view,
+                                                     vtgs_pose *__restrict__ view_copy) {
+    if (threadIdx.x == 0) *view_copy = *view;  // the backward reads the copy (caller may reuse view)
+    __shared__ unsigned long long warp_sum[32];
+    __shared__ unsigned int warp_max[32];
+    __shared__ unsigned long long total_s;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int per = (T + 1023) / 1024;
+    const int b = tid * per, e = min(b + per, T);
+    unsigned long long s = 0;
+    unsigned int mx = 0;
+    for (int i = b; i < e; ++i) {
+        s += tile_count[i];
+        mx = max(mx, tile_count[i]);
+    }
+    unsigned long long incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+    if (lane == 31) warp_sum[w] = incl;
+    if (lane == 0) warp_max[w] = mx;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long v = warp_sum[lane];
+        unsigned int m = warp_max[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(kFull, v, o);
+            if (lane >= o) v += y;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
+        warp_sum[lane] = v;
+        if (lane == 31) {
+            total_s = v;
+            dev->n_pairs = v;
+            dev->max_tile = m;
+            dev->overflow = v > cap ? 1u : 0u;
+        }
+    }
+    __syncthreads();
+    const bool overflow = total_s > cap;
+    unsigned long long run = incl - s + (w > 0 ? warp_sum[w - 1] : 0ull);
+    for (int i = b; i < e; ++i) {
+        const uint32_t c = tile_count[i];
+        tile_start[i] = overflow ? 0u : (uint32_t)run;
+        cursor[i] = overflow ? 0u : (uint32_t)run;
+        if (overflow) tile_count[i] = 0;
+        run += c;
+    }
+    if (tid == 0) tile_start[T] = overflow ? 0u : (uint32_t)total_s;
+}
+
+// ------------------------------------------------------------------------------------------
+// K4: scatter (z bits, gid) into each tile's bucket (order inside a bucket is arbitrary; the
+// per-tile sort below makes it (z, gid)).
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_emit_pairs(const float4 *__restrict__ proj,
+                                                    const uint2 *__restrict__ rect, int64_t N, int ntx,
+                                                    uint32_t *__restrict__ cursor,
+                                                    uint32_t *__restrict__ keys,
+                                                    uint32_t *__restrict__ vals,
+                                                    const DevScalars *__restrict__ dev) {
+    if (dev->overflow) return;
+    const int64_t Nr = (N + 31) & ~(int64_t)31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const unsigned lane = lane_id();
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < Nr; g += stride) {
+        int cnt = 0, ntg = 1, tx0 = 0, ty0 = 0;
+        uint32_t zb = 0;
+        if (g < N) {
+            const uint2 r = rect[g];
+            if (r.x != 0xffffffffu) {
+                const int x0 = r.x & 0xffff, x1 = r.x >> 16, y0 = r.y & 0xffff, y1 = r.y >> 16;
+                tx0 = x0 >> 4;
+                ty0 = y0 >> 4;
+                ntg = (x1 >> 4) - tx0 + 1;
+                cnt = ntg * ((y1 >> 4) - ty0 + 1);
+                zb = __float_as_uint(proj[g].z);
+            }
+        }
+        for (int k = 0; __any_sync(kFull, k < cnt); ++k) {
+            int tile = -1;
+            if (k < cnt) {
+                const int dy = k / ntg;
+                tile = (ty0 + dy) * ntx + tx0 + (k - dy * ntg);
+            }
+            const unsigned peers = __match_any_sync(kFull, tile);
+            const int leader = __ffs(peers) - 1;
+            uint32_t base = 0;
+            if (tile >= 0 && (int)lane == leader) base = atomicAdd(&cursor[tile], (uint32_t)__popc(peers));
+            base = __shfl_sync(kFull, base, leader);
+            if (tile >= 0) {
+                const uint32_t slot = base + __popc(peers & lanemask_lt());
+                keys[slot] = zb;
+                vals[slot] = (uint32_t)g;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K5: per-tile sort by (z bits, gid).  Stable LSD radix sort on the z bits that vary inside
+// the tile (8-bit digits; in-warp stable ranking with 8 ballots per digit; digit-major scan over
+// the 8 warps' histograms), then runs of equal z are ordered by gid.  Buffers are shared memory
+// for lists ≤ kSortCap, global scratch above that.
+// ------------------------------------------------------------------------------------------
+template <typename OffT>
+__device__ __forceinline__ int block_sort_zgid(uint32_t *K0, uint32_t *V0, uint32_t *K1, uint32_t *V1,
+                                               OffT *OFF, uint32_t *HIST, uint32_t *red, int n) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint32_t o = 0, a = 0xffffffffu;
+    for (int i = tid; i < n; i += kBlock) {
+        const uint32_t k = K0[i];
+        o |= k;
+        a &= k;
+    }
+    o = __reduce_or_sync(kFull, o);
+    a = __reduce_and_sync(kFull, a);
+    if (lane == 0) { red[w] = o; red[8 + w] = a; }
+    __syncthreads();
+    o = 0; a = 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { o |= red[i]; a &= red[8 + i]; }
+    const uint32_t diff = o ^ a;
+    const int lo = diff ? __ffs(diff) - 1 : 0;
+    const int hi = diff ? 32 - __clz(diff) : 0;
+    const int npass = (hi - lo + 7) >> 3;
+    const int S = ((n + 8 * 32 - 1) / (8 * 32)) * 32;  // items per warp segment
+    const int seg0 = min(w * S, n), seg1 = min(seg0 + S, n);
+    uint32_t *Ks = K0, *Vs = V0, *Kd = K1, *Vd = V1;
+    uint32_t *H = HIST + w * 256;
+    for (int p = 0; p < npass; ++p) {
+        const int shift = lo + 8 * p;
+        for (int d = lane; d < 256; d += 32) H[d] = 0;
+        __syncwarp();
+        for (int base = seg0; base < seg1; base += 32) {
+            const int i = base + lane;
+            const bool valid = i < seg1;
+            const uint32_t d = valid ? (Ks[i] >> shift) & 255u : 0u;
+            unsigned m = __ballot_sync(kFull, valid);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const bool bit = (d >> b) & 1u;
+                const unsigned bb = __ballot_sync(kFull, bit);
+                m &= bit ? bb : ~bb;
+            }
+            const uint32_t rank = __popc(m & lanemask_lt());
+            const uint32_t cnt0 = valid ? H[d] : 0u;
+            __syncwarp();
+            if (valid && rank == 0) H[d] = cnt0 + __popc(m);
+            __syncwarp();
+            if (valid) OFF[i] = (OffT)(cnt0 + rank);
+        }
+        __syncthreads();
+        {   // digit-major exclusive scan over (digit, warp)
+            const int d = tid;  // kBlock == 256 digits
+            uint32_t c[8], tot = 0;
+#pragma unroll
+            for (int ww = 0; ww < 8; ++ww) { c[ww] = HIST[ww * 256 + d]; tot += c[ww]; }
+            uint32_t incl = tot;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, incl, off);
+                if (lane >= off) incl += y;
+            }
+            if (lane == 31) red[16 + w] = incl;
+            __syncthreads();
+            uint32_t wpre = 0;
+#pragma unroll
+            for (int ww = 0; ww < 8; ++ww) wpre += ww < w ? red[16 + ww] : 0u;
+            uint32_t run = wpre + incl - tot;
+#pragma unroll
+            for (int ww = 0; ww < 8; ++ww) { HIST[ww * 256 + d] = run; run += c[ww]; }
+        }
+        __syncthreads();
+        for (int i = seg0 + lane; i < seg1; i += 32) {
+            const uint32_t k = Ks[i];
+            const uint32_t dst = H[(k >> shift) & 255u] + (uint32_t)OFF[i];
+            Kd[dst] = k;
+            Vd[dst] = Vs[i];
+        }
+        __syncthreads();
+        uint32_t *t = Ks; Ks = Kd; Kd = t;
+        t = Vs; Vs = Vd; Vd = t;
+    }
+    // equal z: ascending gid (the tie-break of SPEC.md:171)
+    for (int i = tid; i < n; i += kBlock) {
+        const uint32_t k = Ks[i];
+        if ((i == 0 || Ks[i - 1] != k) && i + 1 < n && Ks[i + 1] == k) {
+            int j = i + 1;
+            while (j < n && Ks[j] == k) ++j;
+            for (int x = i + 1; x < j; ++x) {
+                const uint32_t v = Vs[x];
+                int y = x - 1;
+                while (y >= i && Vs[y] > v) { Vs[y + 1] = Vs[y]; --y; }
+                Vs[y + 1] = v;
+            }
+        }
+    }
+    __syncthreads();
+    return npass & 1;
+}
+
+__global__ void __launch_bounds__(kBlock) k_tile_sort(const uint32_t *__restrict__ tile_count,
+                                                      const uint32_t *__restrict__ tile_start,
+                                                      uint32_t *keys, uint32_t *vals, uint32_t *keys2,
+                                                      uint32_t *vals2, uint32_t *offs) {
+    extern __shared__ uint32_t sm[];
+    __shared__ uint32_t hist[8 * 256];
+    __shared__ uint32_t red[32];
+    const int tile = blockIdx.x;
+    const int n = (int)tile_count[tile];
+    if (n <= 1) return;
+    const uint32_t base = tile_start[tile];
+    if (n <= kSortCap) {
+        uint32_t *K0 = sm, *V0 = sm + kSortCap, *K1 = sm + 2 * kSortCap, *V1 = sm + 3 * kSortCap;
+        uint16_t *OFF = reinterpret_cast<uint16_t *>(sm + 4 * kSortCap);
+        for (int i = threadIdx.x; i < n; i += kBlock) { K0[i] = keys[base + i]; V0[i] = vals[base + i]; }
+        __syncthreads();
+        const int odd = block_sort_zgid<uint16_t>(K0, V0, K1, V1, OFF, hist, red, n);
+        const uint32_t *Vr = odd ? V1 : V0;
+        for (int i = threadIdx.x; i < n; i += kBlock) vals[base + i] = Vr[i];
+    } else {
+        const int odd = block_sort_zgid<uint32_t>(keys + base, vals + base, keys2 + base, vals2 + base,
+                                                  offs + base, hist, red, n);
+        if (odd)
+            for (int i = threadIdx.x; i < n; i += kBlock) vals[base + i] = vals2[base + i];
+    }
+}
+
+constexpr size_t kSortSmem = 4 * kSortCap * sizeof(uint32_t) + kSortCap * sizeof(uint16_t);
+
+// ------------------------------------------------------------------------------------------
+// K6: per-tile front-to-back compositing.  One CTA per 16×16 tile, one thread per pixel; warp w
+// owns the 8×4 sub-tile (w&1, w>>1).  The tile list is staged through shared memory 256
+// entries at a time; each warp compacts (ballot) the entries whose footprint rect touches its
+// sub-tile into a private list together with the 32-bit mask of its pixels inside the rect,
+// then all lanes walk that list in order.  DESIGN.md §3 step 7.
+// ------------------------------------------------------------------------------------------
+struct FwdArgs {
+    const float4 *proj;
+    const uint2 *rect;
+    const float4 *col_opa;
+    const uint32_t *tile_count;
+    const uint32_t *tile_start;
+    const uint32_t *sorted;
+    int W, H, ntx;
+    float *color, *depth, *sil, *T_final;
+    uint32_t *last;
+    DevScalars *dev;
+};
+
+__device__ __forceinline__ unsigned subtile_mask(uint2 r, int sx, int sy) {
+    const int x0 = (int)(r.x & 0xffffu) - sx, x1 = (int)(r.x >> 16) - sx;
+    const int y0 = (int)(r.y & 0xffffu) - sy, y1 = (int)(r.y >> 16) - sy;
+    const int cx0 = max(x0, 0), cx1 = min(x1, 7), cy0 = max(y0, 0), cy1 = min(y1, 3);
+    if (cx0 > cx1 || cy0 > cy1) return 0u;
+    const unsigned col = (0xffu >> (7 - cx1)) & (0xffu << cx0);
+    const unsigned rows = (0xffffffffu >> (8 * (3 - cy1))) & (0xffffffffu << (8 * cy0));
+    return (col * 0x01010101u) & rows;
+}
+
+__global__ void __launch_bounds__(kBlock) k_composite_fwd(FwdArgs p) {
+    __shared__ float4 sA[kChunk];  // u, v, 9σ², −log2(e)/(2σ²)
+    __shared__ float4 sB[kChunk];  // colour, opacity
+    __shared__ float sZ[kChunk];
+    __shared__ uint2 sR[kChunk];
+    __shared__ uint16_t sIdx[8][kChunk];
+    __shared__ unsigned sMsk[8][kChunk];
+
+    const int tile = blockIdx.x;
+    const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
+    const int tid = threadIdx.x, w = tid >> 5;
+    const unsigned lane = lane_id();
+    const int sx = tx * kTile + (w & 1) * 8, sy = ty * kTile + (w >> 1) * 4;
+    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const bool inside = px < p.W && py < p.H;
+    const float pxf = (float)px, pyf = (float)py;
+    const int n = (int)p.tile_count[tile];
+    const uint32_t start = p.tile_start[tile];
+
+    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f, S = 0.f;
+    uint32_t lastc = 0, ne = 0, nc = 0;
+    bool done = !inside;
+    unsigned active = __ballot_sync(kFull, !done);
+
+    for (int cb = 0; cb < n; cb += kChunk) {
+        const int m = min(kChunk, n - cb);
+        if (tid < m) {
+            const uint32_t g = p.sorted[start + cb + tid];
+            const float4 pr = p.proj[g];
+            const float s = fabsf(pr.w);
+            const float s2 = __fmul_rn(s, s);
+            sA[tid] = make_float4(pr.x, pr.y, __fmul_rn(9.0f, s2), __fdividef(-0.5f * kLog2e, s2));
+            sB[tid] = p.col_opa[g];
+            sZ[tid] = pr.z;
+            sR[tid] = p.rect[g];
+        }
+        __syncthreads();
+        if (active) {
+            int cnt = 0;
+            for (int j = 0; j < m; j += 32) {
+                const int e = j + (int)lane;
+                const unsigned msk = e < m ? subtile_mask(sR[e], sx, sy) & active : 0u;
+                const unsigned b = __ballot_sync(kFull, msk != 0u);
+                if (msk) {
+                    const int pos = cnt + __popc(b & lanemask_lt());
+                    sIdx[w][pos] = (uint16_t)e;
+                    sMsk[w][pos] = msk;
+                }
+                cnt += __popc(b);
+            }
+            __syncwarp();
+            for (int k = 0; k < cnt; ++k) {
+                const int e = sIdx[w][k];
+                const unsigned msk = sMsk[w][k];
+                if (((msk >> lane) & 1u) && !done) {
+                    const float4 A = sA[e];
+                    const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
+                    const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+                    if (d2 <= A.z) {
+                        ++ne;
+                        const float4 B = sB[e];
+                        const float a = fminf(__fmul_rn(B.w, fast_exp2(d2 * A.w)), kAlphaMax);
+                        if (a >= 1.0f / 255.0f) {
+                            const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
+                            if (Tn < kTMin) {
+                                done = true;
+                            } else {
+                                const float om = a * T;
+                                C0 = fmaf(B.x, om, C0);
+                                C1 = fmaf(B.y, om, C1);
+                                C2 = fmaf(B.z, om, C2);
+                                D = fmaf(sZ[e], om, D);
+                                S += om;
+                                T = Tn;
+                                lastc = (uint32_t)(cb + e + 1);
+                                ++nc;
+                            }
+                        }
+                    }
+                }
+                if ((k & 7) == 7) {
+                    active = __ballot_sync(kFull, !done);
+                    if (!active) break;
+                }
+            }
+            active = __ballot_sync(kFull, !done);
+        }
+        if (!__syncthreads_or(active != 0u)) break;
+    }
+    if (inside) {
+        const int pix = py * p.W + px;
+        p.color[3 * pix + 0] = C0;
+        p.color[3 * pix + 1] = C1;
+        p.color[3 * pix + 2] = C2;
+        p.depth[pix] = D;
+        p.sil[pix] = S;
+        p.T_final[pix] = T;
+        p.last[pix] = lastc;
+    }
+    unsigned long long a = ne, b = nc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(kFull, a, o);
+        b += __shfl_xor_sync(kFull, b, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&p.dev->e_eval, a);
+        atomicAdd(&p.dev->e_comp, b);
+    }
+}
+
+cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
+    const int W = c.intr.width, H = c.intr.height;
+    const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile, T = ntx * nty;
+    cudaError_t err;
+    if ((err = cudaMemsetAsync(c.tile_count, 0, sizeof(uint32_t) * T, s))) return err;
+    if ((err = cudaMemsetAsync(c.dev, 0, sizeof(DevScalars), s))) return err;
+    const int64_t N = c.N;
+    int gN = (int)((N + 255) / 256);
+    if (gN > c.num_sms * 16) gN = c.num_sms * 16;
+    if (N > 0) {
+        LaunchScope ls(&c, kProject, s);
+        k_project_count<<<gN, 256, 0, s>>>(c.pos_rad, N, c.view, c.intr, ntx, c.proj, c.rect, c.tile_count);
+        if ((err = cudaGetLastError())) return err;
+    }
+    {
+        LaunchScope ls(&c, kScan, s);
+        k_scan_tiles<<<1, 1024, 0, s>>>(c.tile_count, c.tile_start, c.tile_cursor, T,
+                                         (unsigned long long)c.max_pairs, c.dev, c.view, c.view_copy);
+    }
+    if ((err = cudaGetLastError())) return err;
+    if (N > 0) {
+        LaunchScope ls(&c, kEmit, s);
+        k_emit_pairs<<<gN, 256, 0, s>>>(c.proj, c.rect, N, ntx, c.tile_cursor, c.keys, c.vals, c.dev);
+        if ((err = cudaGetLastError())) return err;
+    }
+    {
+        LaunchScope ls(&c, kSort, s);
+        k_tile_sort<<<T, kBlock, kSortSmem, s>>>(c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2,
+                                                 c.offs);
+    }
+    if ((err = cudaGetLastError())) return err;
+    FwdArgs a{c.proj, c.rect, c.col_opa, c.tile_count, c.tile_start, c.vals, W, H, ntx,
+              c.color, c.depth, c.sil, c.T_final, c.last, c.dev};
+    {
+        LaunchScope ls(&c, kCompFwd, s);
+        k_composite_fwd<<<T, kBlock, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t forward_set_attributes() {
+    return cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem);
+}
+
+}  // namespace vtgs

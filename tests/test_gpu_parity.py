@@ -1,0 +1,476 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle, element by element, on
+the same seeded inputs (task rule ③).  Bars (BASELINE.json north_star):
+  * instantiation and tile lists / sort order: bit-exact;
+  * colour, depth, silhouette: within 1e-4 absolute (fp32) on every pixel the oracle does not
+    flag as near a decision threshold ("near-threshold flags");
+  * gradients: within 1e-3 relative or 1e-5 absolute on every Gaussian not evaluated at a
+    flagged pixel (plus, for the handful of sums that cancel by κ > 1e3, the fp32 summation
+    floor 16·2⁻²⁴·Σ|terms| — DESIGN.md §3 R23 — counted and capped); the pose gradient within
+    1e-3 of its norm.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+from synth.scenes import Intrinsics, cached_config, micro_scene
+from vtgs_testlib import close, gpu_instantiate, oracle_instantiate, report, view32
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def vt():
+    from paper_2506_02741_b200 import vtgs
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return vtgs
+
+
+def _renderer(vt, cfg, **kw):
+    return vt.Renderer(0, cfg.n_slots, cfg.intr.width, cfg.intr.height, **kw)
+
+
+def _view(cfg):
+    return view32(cfg.views[0])
+
+
+def _loss_of(cfg):
+    wc, wd = cfg.loss_weights
+    mode = 1 if cfg.mode == "tracking" else 0
+    return dict(w_color=wc, w_depth=wd, color_mask_mode=mode, depth_mask_mode=mode, normalize=0)
+
+
+def _render_gpu(vt, R, cfg, pos_rad, col_opa, view=None):
+    """Forward; the view pose and the output images are kept alive on the renderer because the
+    context reads them again in the backward (vtgs.h: they must stay valid until render_bwd)."""
+    v = vt.pose_tensor(_view(cfg) if view is None else view, "cuda")
+    out = R.render_fwd(pos_rad, col_opa, v, cfg.intr)
+    R._keep = (v, out, pos_rad, col_opa)
+    torch.cuda.synchronize()
+    return v, out
+
+
+# ------------------------------------------------------------------------------ (a1)
+@pytest.mark.parametrize("which", [1, 2, 3])
+def test_instantiate_bitexact(vt, which):
+    cfg = cached_config(which)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    opr, oco = oracle_instantiate(cfg)
+    assert np.array_equal(pr.cpu().numpy(), opr.astype(np.float32))
+    assert np.array_equal(co.cpu().numpy(), oco.astype(np.float32))
+
+
+# ------------------------------------------------------------------------------ (a2)/(a3)
+@pytest.mark.parametrize("which,view", [(1, "view"), (1, "kf"), (2, "view"), (3, "view"), (4, "view")])
+def test_tile_lists_bitexact(vt, which, view):
+    cfg = cached_config(which)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    v = view32(cfg.keyframes[0].pose) if view == "kf" else _view(cfg)
+    _render_gpu(vt, R, cfg, pr, co, v)
+    start, gid = R.export_tiles(cfg.intr)
+    opr, _ = oracle_instantiate(cfg)
+    ostart, ogid = oracle.tile_lists(opr, v, cfg.intr)
+    assert np.array_equal(start, ostart), "tile offsets differ"
+    assert np.array_equal(gid.astype(np.int64), ogid), "sorted tile lists differ"
+    st = R.stats()
+    assert st["n_pairs"] == len(ogid) and st["max_tile"] == int(np.diff(ostart).max())
+
+
+def test_tile_lists_micro_scenes(vt):
+    """Random micro scenes (non-unit q, fx ≠ fy, σ 0.8–2.2 px, many overlaps)."""
+    for seed in range(10):
+        m = micro_scene(seed, n=200, width=45, height=37)
+        R = vt.Renderer(0, 200, 45, 37)
+        pr = torch.from_numpy(m["pos_rad"]).cuda()
+        co = torch.from_numpy(m["col_opa"]).cuda()
+        v = vt.pose_tensor(view32(m["view"]), "cuda")
+        R.render_fwd(pr, co, v, m["intr"])
+        start, gid = R.export_tiles(m["intr"])
+        ostart, ogid = oracle.tile_lists(m["pos_rad"], view32(m["view"]), m["intr"])
+        assert np.array_equal(start, ostart) and np.array_equal(gid.astype(np.int64), ogid)
+
+
+# ------------------------------------------------------------------------------ (a4)
+def _check_images(out, ref, flags, atol=1e-4, max_flagged=5e-3):
+    color, depth, sil = (t.cpu().numpy().astype(np.float64) for t in out)
+    ok = ~flags
+    assert flags.mean() < max_flagged, f"too many flagged pixels: {flags.sum()}"
+    for name, g, r in (("color", color[ok], ref["color"][ok]), ("depth", depth[ok], ref["depth"][ok]),
+                       ("sil", sil[ok], ref["sil"][ok])):
+        good = np.abs(g - r) <= atol
+        assert good.all(), report(name, good, g, r)
+
+
+@pytest.mark.parametrize("which", [1, 2, 3])
+def test_forward_parity(vt, which):
+    cfg = cached_config(which)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    _, out = _render_gpu(vt, R, cfg, pr, co)
+    opr, oco = oracle_instantiate(cfg)
+    ref = oracle.render(opr, oco, _view(cfg), cfg.intr)
+    _check_images(out, ref, ref["flags"])
+    st = R.stats()
+    assert st["overflow"] == 0
+    assert st["n_pairs"] == ref["stats"][2]
+    # composited / evaluated pair counts agree up to the flagged pixels
+    assert abs(st["e_comp"] - ref["stats"][1]) <= max(10, 2e-4 * ref["stats"][1])
+    assert abs(st["e_eval"] - ref["stats"][0]) <= max(10, 2e-4 * ref["stats"][0])
+
+
+def test_forward_parity_config4_sampled_rows(vt):
+    """Config 4 (16 keyframes, 4.9M slots) at full size, oracle on sampled row bands."""
+    cfg = cached_config(4)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    opr, oco = oracle_instantiate(cfg)
+    for k in (0, 3):
+        v = view32(cfg.views[k])
+        _, out = _render_gpu(vt, R, cfg, pr, co, v)
+        for r0 in (0, 200, 464):
+            ref = oracle.render(opr, oco, v, cfg.intr, rows=(r0, r0 + 16))
+            sl = slice(r0, r0 + 16)
+            sub = tuple(t[sl] for t in out)
+            _check_images(sub, {kk: ref[kk][sl] for kk in ("color", "depth", "sil")}, ref["flags"][sl])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_forward_parity_micro_ragged(vt, seed):
+    """Ragged image sizes (not multiples of 16), dense overlaps, σ clamp cases."""
+    W, H = [(45, 37), (17, 16), (16, 17), (33, 1), (1, 40), (100, 61)][seed]
+    m = micro_scene(seed, n=300, width=max(W, 4), height=max(H, 4))
+    intr = Intrinsics(m["intr"].fx, m["intr"].fy, W / 2 - 0.25, H / 2 - 0.25, W, H) \
+        if min(W, H) > 1 else Intrinsics(14.0, 15.0, W / 2, H / 2, W, H)
+    R = vt.Renderer(0, 300, W, H)
+    pr = torch.from_numpy(m["pos_rad"]).cuda()
+    co = torch.from_numpy(m["col_opa"]).cuda()
+    v = view32(m["view"])
+    vv = vt.pose_tensor(v, "cuda")
+    out = R.render_fwd(pr, co, vv, intr)
+    ref = oracle.render(m["pos_rad"], m["col_opa"], v, intr)
+    _check_images(out, ref, ref["flags"])
+
+
+# ------------------------------------------------------------------------------ (a5)
+def _oracle_grads(cfg, opr, oco, v, gC, gD, gS, extra_flags=None):
+    ref = oracle.render(opr, oco, v, cfg.intr, want_tainted=True, extra_flags=extra_flags)
+    g = oracle.render_bwd(opr, oco, v, cfg.intr, gC, gD, gS)
+    return ref, g
+
+
+def _check_grads(want, dco, drad, dpose, g, tainted, vt, learn=None):
+    N = len(tainted)
+    keep = ~tainted
+    if learn is not None:
+        lo, hi = learn
+        idx = np.arange(N)
+        outside = (idx < lo) | (idx >= hi)
+        assert not dco[outside].any() and not drad[outside].any()
+        keep &= ~outside
+    if want & (vt.VTGS_GRAD_COLOR | vt.VTGS_GRAD_OPACITY):
+        st = {}
+        ok = close(dco[keep], g["d_col_opa"][keep], absum=g["d_abs"][keep, :4], stats=st)
+        assert ok.all(), report("d_col_opa", ok, dco[keep], g["d_col_opa"][keep])
+        assert st["floor_only"] <= 5 + 1e-5 * st["n"], st
+    if want & vt.VTGS_GRAD_RADIUS:
+        st = {}
+        ok = close(drad[keep], g["d_radius"][keep], absum=g["d_abs"][keep, 4], stats=st)
+        assert ok.all(), report("d_radius", ok, drad[keep], g["d_radius"][keep])
+        assert st["floor_only"] <= 5 + 1e-5 * st["n"], st
+    if want & vt.VTGS_GRAD_POSE:
+        ref = g["d_pose"]
+        err = np.linalg.norm(dpose - ref)
+        assert err <= 1e-3 * np.linalg.norm(ref), f"d_pose gpu={dpose} oracle={ref}"
+
+
+def _run_bwd(vt, R, cfg, want, n, **kw):
+    dco = torch.zeros((n, 4), device="cuda")
+    drad = torch.zeros(n, device="cuda")
+    dpose = torch.zeros(7, device="cuda")
+    R.render_bwd(want, d_col_opa=dco, d_radius=drad, d_pose=dpose, **kw)
+    torch.cuda.synchronize()
+    return dco.cpu().numpy().astype(np.float64), drad.cpu().numpy().astype(np.float64), \
+        dpose.cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("which", [1, 2, 3])
+def test_backward_parity_upstream(vt, which):
+    """Explicit per-pixel upstream gradients (a seeded random linear functional of C, D, S)."""
+    cfg = cached_config(which)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    _render_gpu(vt, R, cfg, pr, co)
+    H, W = cfg.intr.height, cfg.intr.width
+    rng = np.random.default_rng(which)
+    gC = rng.normal(size=(H, W, 3)).astype(np.float32)
+    gD = rng.normal(size=(H, W)).astype(np.float32)
+    gS = rng.normal(size=(H, W)).astype(np.float32)
+    want = vt.VTGS_GRAD_ALL
+    dco, drad, dpose = _run_bwd(vt, R, cfg, want, cfg.n_slots, dL_dcolor=torch.from_numpy(gC).cuda(),
+                                dL_ddepth=torch.from_numpy(gD).cuda(), dL_dsil=torch.from_numpy(gS).cuda())
+    opr, oco = oracle_instantiate(cfg)
+    ref, g = _oracle_grads(cfg, opr, oco, _view(cfg), gC, gD, gS)
+    _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt)
+
+
+@pytest.mark.parametrize("which", [1, 2, 3])
+def test_backward_parity_fused_l1(vt, which):
+    """The config's own objective: masked L1 of Eq. 1 (tracking) / L1 terms of Eq. 2 (mapping),
+    sum form (SURVEY §8(c) pin note), fused into the backward."""
+    cfg = cached_config(which)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    _render_gpu(vt, R, cfg, pr, co)
+    tg = cfg.targets[0]
+    L = _loss_of(cfg)
+    want = {"full": vt.VTGS_GRAD_ALL, "mapping": vt.VTGS_GRAD_ATTR, "tracking": vt.VTGS_GRAD_POSE}[cfg.mode]
+    loss_out = torch.zeros(1, device="cuda")
+    dco, drad, dpose = _run_bwd(vt, R, cfg, want, cfg.n_slots, loss=dict(
+        target_rgb=torch.from_numpy(tg.rgb).cuda(), target_depth=torch.from_numpy(tg.depth).cuda(), **L),
+        loss_out=loss_out)
+    opr, oco = oracle_instantiate(cfg)
+    v = _view(cfg)
+    img = oracle.render(opr, oco, v, cfg.intr)
+    loss, gC, gD, gS, lflags = oracle.l1_upstream(img["color"], img["depth"], img["sil"], tg.rgb, tg.depth, None,
+                                                   L["w_color"], L["w_depth"], L["color_mask_mode"],
+                                                   L["depth_mask_mode"], 0)
+    assert abs(float(loss_out.item()) - loss) <= 1e-4 * abs(loss) + 1e-6
+    ref, g = _oracle_grads(cfg, opr, oco, v, gC, gD, gS, extra_flags=lflags)
+    _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt)
+
+
+def test_backward_learn_range_and_accumulate(vt):
+    """Only gids in [learn_begin, learn_end) get attribute gradients; gradients
+    accumulate (+=) across calls (multi-view mapping is a loop)."""
+    cfg = cached_config(1)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    _render_gpu(vt, R, cfg, pr, co)
+    H, W = cfg.intr.height, cfg.intr.width
+    rng = np.random.default_rng(3)
+    gC = torch.from_numpy(rng.normal(size=(H, W, 3)).astype(np.float32)).cuda()
+    lo, hi = 700, 2100
+    dco, drad, _ = _run_bwd(vt, R, cfg, vt.VTGS_GRAD_ATTR, cfg.n_slots, dL_dcolor=gC, learn=(lo, hi))
+    opr, oco = oracle_instantiate(cfg)
+    ref, g = _oracle_grads(cfg, opr, oco, _view(cfg), gC.cpu().numpy(), None, None)
+    _check_grads(vt.VTGS_GRAD_ATTR, dco, drad, None, g, ref["tainted"], vt, learn=(lo, hi))
+    acc = torch.zeros((cfg.n_slots, 4), device="cuda")
+    accr = torch.zeros(cfg.n_slots, device="cuda")
+    R.render_bwd(vt.VTGS_GRAD_ATTR, d_col_opa=acc, d_radius=accr, dL_dcolor=gC)
+    R.render_bwd(vt.VTGS_GRAD_ATTR, d_col_opa=acc, d_radius=accr, dL_dcolor=gC)
+    one = torch.zeros((cfg.n_slots, 4), device="cuda")
+    R.render_bwd(vt.VTGS_GRAD_ATTR, d_col_opa=one, d_radius=torch.zeros_like(accr), dL_dcolor=gC)
+    torch.cuda.synchronize()
+    assert torch.allclose(acc, 2 * one, rtol=1e-6, atol=1e-7)
+
+
+# ------------------------------------------------------------------------------ invariants on GPU
+def test_loss_at_optimum_zero_gradient(vt):
+    """Target = the GPU's own render → every residual is exactly 0 → all gradients exactly 0."""
+    cfg = cached_config(1)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    v, (C, D, S) = _render_gpu(vt, R, cfg, pr, co)
+    tC, tD = C.clone(), D.clone()
+    dco, drad, dpose = _run_bwd(vt, R, cfg, vt.VTGS_GRAD_ALL, cfg.n_slots,
+                                loss=dict(target_rgb=tC, target_depth=tD, w_color=1.0, w_depth=0.5))
+    assert not dco.any() and not drad.any() and not dpose.any()
+
+
+def test_deterministic_forward_and_pose(vt):
+    cfg = cached_config(3)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    tg = cfg.targets[0]
+    L = dict(target_rgb=torch.from_numpy(tg.rgb).cuda(), target_depth=torch.from_numpy(tg.depth).cuda(),
+             **_loss_of(cfg))
+    outs = []
+    for _ in range(2):
+        _, img = _render_gpu(vt, R, cfg, pr, co)
+        dp = torch.zeros(7, device="cuda")
+        R.render_bwd(vt.VTGS_GRAD_POSE, d_pose=dp, loss=L)
+        torch.cuda.synchronize()
+        outs.append([t.clone() for t in img] + [dp.clone()])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_zero_opacity_background(vt):
+    cfg = cached_config(1)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    co[:, 3] = 0.0
+    _, (C, D, S) = _render_gpu(vt, R, cfg, pr, co)
+    assert not C.any() and not D.any() and not S.any()
+
+
+# ------------------------------------------------------------------------------ edge cases
+def test_edge_empty_and_invalid(vt):
+    intr = Intrinsics(60.0, 60.0, 32.0, 24.0, 64, 48)
+    R = vt.Renderer(0, 64 * 48, 64, 48)
+    v = vt.pose_tensor([1, 0, 0, 0, 0, 0, 0], "cuda")
+    e = torch.zeros((0, 4), device="cuda")
+    C, D, S = R.render_fwd(e, e, v, intr, N=0)
+    torch.cuda.synchronize()
+    assert not C.any() and not D.any() and not S.any()
+    dp = torch.zeros(7, device="cuda")
+    R.render_bwd(vt.VTGS_GRAD_POSE, d_pose=dp, dL_dcolor=torch.ones((48, 64, 3), device="cuda"))
+    torch.cuda.synchronize()
+    assert not dp.any()
+    # all-invalid depth → every slot r = 0 → empty render
+    depth = torch.zeros((1, 48, 64), device="cuda")
+    rgb = torch.rand((1, 48, 64, 3), device="cuda")
+    pr, co = R.instantiate(depth, rgb, v, intr)
+    assert not pr.any() and not co.any()
+    C, D, S = R.render_fwd(pr, co, v, intr)
+    torch.cuda.synchronize()
+    assert not S.any()
+    # everything behind the camera → culled
+    depth = torch.full((1, 48, 64), 2.0, device="cuda")
+    pr, co = R.instantiate(depth, rgb, v, intr)
+    back = vt.pose_tensor([0, 0, 1, 0, 0, 0, 0], "cuda")   # 180° about y: looks the other way
+    C, D, S = R.render_fwd(pr, co, back, intr)
+    torch.cuda.synchronize()
+    assert not S.any() and R.stats()["n_pairs"] == 0
+
+
+def test_edge_single_gaussian_closed_form(vt):
+    intr = Intrinsics(10.0, 10.0, 8.0, 8.0, 16, 16)
+    R = vt.Renderer(0, 1, 16, 16)
+    pr = torch.tensor([[0.0, 0.0, 2.0, 0.2]], device="cuda")
+    co = torch.tensor([[0.2, 0.5, 0.9, 0.6]], device="cuda")
+    v = vt.pose_tensor([1, 0, 0, 0, 0, 0, 0], "cuda")
+    C, D, S = R.render_fwd(pr, co, v, intr)
+    torch.cuda.synchronize()
+    assert S[8, 8].item() == pytest.approx(0.6, abs=1e-6)
+    assert D[8, 8].item() == pytest.approx(1.2, abs=1e-6)
+    assert S[8, 9].item() == pytest.approx(0.6 * np.exp(-0.5), abs=1e-6)
+    assert S[8, 12].item() == 0.0
+
+
+def test_edge_errors(vt):
+    intr = Intrinsics(60.0, 60.0, 32.0, 24.0, 64, 48)
+    R = vt.Renderer(0, 3072, 64, 48, max_pairs=100)
+    v = vt.pose_tensor([1, 0, 0, 0, 0, 0, 0], "cuda")
+    with pytest.raises(vt.VtgsError) as e:
+        R.render_bwd(vt.VTGS_GRAD_POSE, d_pose=torch.zeros(7, device="cuda"),
+                     dL_dcolor=torch.zeros((48, 64, 3), device="cuda"))
+    assert e.value.status == vt.VTGS_ERR_STATE
+    bad = Intrinsics(60.0, 60.0, 64.0, 24.0, 64, 48)   # cx not inside (0, W)
+    e4 = torch.zeros((1, 4), device="cuda")
+    with pytest.raises(vt.VtgsError) as e:
+        R.render_fwd(e4, e4, v, bad)
+    assert e.value.status == vt.VTGS_ERR_INVALID_ARG
+    big = Intrinsics(60.0, 60.0, 32.0, 24.0, 65, 48)
+    with pytest.raises(vt.VtgsError) as e:
+        R.render_fwd(e4, e4, v, big)
+    assert e.value.status == vt.VTGS_ERR_SHAPE
+    # capacity: 3,072 Gaussians need > 100 pairs → deferred VTGS_ERR_CAPACITY, empty render
+    cfg = cached_config(1)
+    pr, co = gpu_instantiate(R, cfg)
+    C, D, S = R.render_fwd(pr, co, vt.pose_tensor(_view(cfg), "cuda"), cfg.intr)
+    with pytest.raises(vt.VtgsError) as e:
+        R.check()
+    assert e.value.status == vt.VTGS_ERR_CAPACITY
+    assert not S.any()
+
+
+def test_edge_max_image_size_and_all_layers(vt):
+    """Maximum context size exactly, and long tile lists through the global-memory sort path
+    (> 4096 entries per tile)."""
+    W, H = 48, 32
+    intr = Intrinsics(40.0, 40.0, 23.5, 15.5, W, H)
+    K = 64                              # 64 stacked fronto-parallel layers → ~64·(16+6)² per tile
+    R = vt.Renderer(0, K * W * H, W, H)
+    depth = torch.linspace(1.0, 3.0, K, device="cuda")[:, None, None].expand(K, H, W).contiguous()
+    rgb = torch.rand((K, H, W, 3), device="cuda", generator=torch.Generator("cuda").manual_seed(0))
+    poses = vt.pose_tensor(np.tile([1, 0, 0, 0, 0, 0, 0], (K, 1)), "cuda")
+    opa = torch.full((K, H, W), 0.05, device="cuda")
+    pr, co = R.instantiate(depth, rgb, poses, intr, opa)
+    v = view32([1, 0.01, -0.01, 0, 0.01, 0, 0])
+    out = R.render_fwd(pr, co, vt.pose_tensor(v, "cuda"), intr)
+    st = R.stats()
+    assert st["max_tile"] > 4096
+    start, gid = R.export_tiles(intr)
+    opr, oco, _ = oracle.instantiate(depth.cpu().numpy(), rgb.cpu().numpy(), np.tile([1, 0, 0, 0, 0, 0, 0], (K, 1)),
+                                     intr, opa.cpu().numpy())
+    ostart, ogid = oracle.tile_lists(opr, v, intr)
+    assert np.array_equal(start, ostart) and np.array_equal(gid.astype(np.int64), ogid)
+    ref = oracle.render(opr, oco, v, intr)
+    # 64 uniform low-opacity layers end every pixel near the 1e-4 cut-off at once, so the
+    # near-threshold flag legitimately covers a few percent of this scene
+    _check_images(out, ref, ref["flags"], max_flagged=0.05)
+
+
+# ------------------------------------------------------------------------------ tracking loop
+def test_tracking_loop_graph_matches_eager_and_converges(vt):
+    """Config 3: 40 iterations of fwd + bwd(pose) + device Adam; the CUDA-graph capture gives
+    the same pose as eager launches, and the pose error shrinks."""
+    cfg = cached_config(3)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    tg = cfg.targets[0]
+    L = dict(target_rgb=torch.from_numpy(tg.rgb).cuda(), target_depth=torch.from_numpy(tg.depth).cuda(),
+             w_color=0.5, w_depth=1.0, color_mask_mode=1, depth_mask_mode=1, normalize=1)
+    iters = cfg.extra["iterations"]
+
+    def run(graph: bool):
+        pose = vt.pose_tensor(_view(cfg), "cuda")
+        state = torch.zeros(16, device="cuda")
+        dp = torch.zeros(7, device="cuda")
+        out = (torch.empty((480, 640, 3), device="cuda"), torch.empty((480, 640), device="cuda"),
+               torch.empty((480, 640), device="cuda"))
+
+        def body(stream=None):
+            for _ in range(iters):
+                R.render_fwd(pr, co, pose, cfg.intr, out=out, stream=stream)
+                R.render_bwd(vt.VTGS_GRAD_POSE, d_pose=dp, loss=L, stream=stream)
+                R.pose_adam_step(pose, dp, state, cfg.extra["lr_rot"], cfg.extra["lr_trans"], stream=stream)
+        if graph:
+            s = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                body(stream=s)
+            pose.copy_(vt.pose_tensor(_view(cfg), "cuda"))
+            state.zero_()
+            g.replay()
+        else:
+            body()
+        torch.cuda.synchronize()
+        return pose.cpu().numpy()[0]
+
+    pe = run(False)
+    pg = run(True)
+    assert np.array_equal(pe, pg)
+    gt = cfg.extra["gt_pose"]
+    init = _view(cfg)
+    assert np.linalg.norm(pe[4:] - gt[4:]) < np.linalg.norm(init[4:] - gt[4:])
+
+
+def test_step_host_matches_device_path(vt):
+    cfg = cached_config(2)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    tg = cfg.targets[0]
+    H, W = cfg.intr.height, cfg.intr.width
+    out = tuple(torch.empty(s, device="cuda") for s in ((H, W, 3), (H, W), (H, W)))
+    d1 = torch.zeros((cfg.n_slots, 4), device="cuda")
+    r1 = torch.zeros(cfg.n_slots, device="cuda")
+    loss_h = R.step_host(pr, co, torch.from_numpy(view32(cfg.views[0]).astype(np.float32)), cfg.intr,
+                         torch.from_numpy(tg.rgb).pin_memory(), torch.from_numpy(tg.depth).pin_memory(),
+                         0.8, 1.0, 0, 0, 0, vt.VTGS_GRAD_ATTR, (0, cfg.n_slots), out, d1, r1)
+    v, _ = _render_gpu(vt, R, cfg, pr, co)
+    d2 = torch.zeros_like(d1)
+    r2 = torch.zeros_like(r1)
+    lo = torch.zeros(1, device="cuda")
+    R.render_bwd(vt.VTGS_GRAD_ATTR, d_col_opa=d2, d_radius=r2,
+                 loss=dict(target_rgb=torch.from_numpy(tg.rgb).cuda(), target_depth=torch.from_numpy(tg.depth).cuda(),
+                           w_color=0.8, w_depth=1.0), loss_out=lo)
+    torch.cuda.synchronize()
+    assert loss_h == pytest.approx(lo.item(), rel=1e-6)
+    assert torch.allclose(d1, d2, rtol=1e-5, atol=1e-6)
