@@ -51,7 +51,7 @@ cudaError_t dalloc(T **p, size_t n) {
 
 void free_all(Ctx &c) {
     void *ptrs[] = {c.proj, c.rect, c.tile_count, c.tile_start, c.tile_cursor, c.keys, c.vals, c.keys2,
-                    c.vals2, c.offs, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy};
+                    c.vals2, c.offs, c.sub_lists, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -116,9 +116,11 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = dalloc(&c.keys2, (size_t)max_pairs);
     if (!e) e = dalloc(&c.vals2, (size_t)max_pairs);
     if (!e) e = dalloc(&c.offs, (size_t)max_pairs);
+    if (!e) e = dalloc(&c.sub_lists, (size_t)8 * max_pairs);
+    if (!e) e = dalloc(&c.sub_count, (size_t)8 * c.max_tiles);
     if (!e) e = dalloc(&c.T_final, px);
     if (!e) e = dalloc(&c.last, px);
-    if (!e) e = dalloc(&c.partials, (size_t)c.max_tiles * 16);
+    if (!e) e = dalloc(&c.partials, (size_t)c.max_tiles * 8 * 16);
     if (!e) e = dalloc(&c.dev, 1);
     if (!e) e = dalloc(&c.host_io, 4 * px + 64);
     if (!e) e = dalloc(&c.view_copy, 1);
@@ -126,6 +128,7 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = cudaMemset(c.tile_count, 0, sizeof(uint32_t) * c.max_tiles);
     if (!e) e = cudaMemset(c.tile_start, 0, sizeof(uint32_t) * (c.max_tiles + 1));
     if (!e) e = vtgs::forward_set_attributes();
+    if (!e) e = vtgs::backward_set_attributes();
     if (!e) e = cudaDeviceSynchronize();
     cudaSetDevice(prev);
     if (e) {

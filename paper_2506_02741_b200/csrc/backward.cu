@@ -11,11 +11,11 @@
 //   * pose gradient (tracking): each lane chains its pairs straight into 12 register
 //     accumulators (Σ g, Σ X_c gᵀ), reduced per CTA in fp64 into a per-tile partial; a
 //     one-CTA kernel sums the partials in a fixed order and applies the rotation chain.
-#include "vtgs_internal.cuh"
+#include "composite_common.cuh"
 
 namespace vtgs {
 
-constexpr unsigned kFull = 0xffffffffu;
+constexpr unsigned kFull = kFullMask;
 
 struct BwdArgs {
     const float4 *proj;
@@ -24,7 +24,8 @@ struct BwdArgs {
     const float4 *pos_rad;
     const uint32_t *tile_count;
     const uint32_t *tile_start;
-    const uint32_t *sorted;
+    const uint32_t *sub_lists;
+    const uint32_t *sub_count;
     int W, H, ntx;
     const float *color, *depth, *sil, *T_final;
     const uint32_t *last;
@@ -43,44 +44,44 @@ struct BwdArgs {
     double *partials;
 };
 
-__device__ __forceinline__ unsigned subtile_mask_b(uint2 r, int sx, int sy) {
-    const int x0 = (int)(r.x & 0xffffu) - sx, x1 = (int)(r.x >> 16) - sx;
-    const int y0 = (int)(r.y & 0xffffu) - sy, y1 = (int)(r.y >> 16) - sy;
-    const int cx0 = max(x0, 0), cx1 = min(x1, 7), cy0 = max(y0, 0), cy1 = min(y1, 3);
-    if (cx0 > cx1 || cy0 > cy1) return 0u;
-    const unsigned col = (0xffu >> (7 - cx1)) & (0xffu << cx0);
-    const unsigned rows = (0xffffffffu >> (8 * (3 - cy1))) & (0xffffffffu << (8 * cy0));
-    return (col * 0x01010101u) & rows;
-}
-
 __device__ __forceinline__ float sgnf(float r) { return (float)((r > 0.0f) - (r < 0.0f)); }
 
-template <bool ATTR, bool POSE, bool LOSS>
-__global__ void __launch_bounds__(kBlock) k_composite_bwd(BwdArgs p) {
-    __shared__ float4 sA[kChunk];  // u, v, 9σ², −log2(e)/(2σ²)
-    __shared__ float4 sB[kChunk];  // colour, opacity
-    __shared__ float4 sX[kChunk];  // X_c (pose) ; .w = ±σ (−: clamped)
-    __shared__ float sZ[kChunk];
-    __shared__ uint2 sR[kChunk];
-    __shared__ uint32_t sGid[kChunk];
-    __shared__ float sAcc[ATTR ? 5 * kChunk : 1];
-    __shared__ uint16_t sIdx[8][kChunk];
-    __shared__ unsigned sMsk[8][kChunk];
-    __shared__ PoseR P;
-    __shared__ uint32_t sMax[8];
-    __shared__ double sRed[8][13];
+// Per batch of 32 sub-list entries the backward runs in two phases (composite_common.cuh):
+//   phase 1 — lane i = pixel walks ITS candidate entries back to front, recovering T_i and the
+//             behind-accumulators, and writes (ω = α_i T_i, dL/dα_i·[α unclamped]) into the
+//             warp's 32×32 matrix M[entry][pixel] (0 for pairs that were not composited);
+//   phase 2 — lane j = entry walks the pixels its footprint covers and sums that entry's
+//             colour / opacity / σ / (u, v, z) gradient from M and the per-pixel upstream — a
+//             per-Gaussian reduction with no shuffles; attribute gradients leave with one
+//             float4 + one float global atomic per (Gaussian, sub-tile), the pose chain is
+//             applied per (Gaussian, sub-tile) into the lane's 12 accumulators.
+// One warp per 8×4 sub-tile, kBwdWarps warps per CTA, no block barriers.
+constexpr int kBwdWarps = 4;
 
-    const int tile = blockIdx.x;
+template <bool ATTR, bool POSE, bool LOSS>
+__global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
+    __shared__ float4 sA[kBwdWarps][32];
+    __shared__ float4 sB[kBwdWarps][32];
+    __shared__ float sZ[kBwdWarps][32];
+    __shared__ float4 sX[kBwdWarps][POSE ? 32 : 1];  // X_c and ±σ (−: σ clamped)
+    __shared__ float4 sG[kBwdWarps][32];             // per pixel (g_C, g_D)
+    extern __shared__ float2 sMdyn[];                 // [kBwdWarps][32 entries][33 (pad)]
+
+    const int tile = blockIdx.x >> 1;
+    const int wl_ = threadIdx.x >> 5;
+    const int sub = (blockIdx.x & 1) * kBwdWarps + wl_;  // sub-tile 0..7 of the tile
+    float2 (*M)[33] = reinterpret_cast<float2 (*)[33]>(sMdyn + (size_t)wl_ * 32 * 33);
     const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
-    const int tid = threadIdx.x, w = tid >> 5;
     const unsigned lane = lane_id();
-    const int sx = tx * kTile + (w & 1) * 8, sy = ty * kTile + (w >> 1) * 4;
+    const int sx = tx * kTile + (sub & 1) * 8, sy = ty * kTile + (sub >> 1) * 4;
     const int px = sx + (lane & 7), py = sy + (lane >> 3);
     const bool inside = px < p.W && py < p.H;
     const float pxf = (float)px, pyf = (float)py;
     const int n = (int)p.tile_count[tile];
-    const uint32_t start = p.tile_start[tile];
-    if (POSE && tid == 0) pose_rotation(*p.view, P);
+    const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
+    const int cnt = (int)p.sub_count[tile * 8 + sub];
+    PoseR P;
+    if (POSE) pose_rotation(*p.view, P);
 
     // ---- per-pixel upstream gradient (explicit, or the fused masked-L1 prologue) ----
     float g0 = 0.f, g1 = 0.f, g2 = 0.f, gD = 0.f, gS = 0.f, T = 1.0f;
@@ -102,18 +103,18 @@ __global__ void __launch_bounds__(kBlock) k_composite_bwd(BwdArgs p) {
                 sd = p.dev->count_d ? 1.0f / (float)p.dev->count_d : 0.0f;
             }
             if (mc) {
-                const float r0 = p.color[3 * pix] - p.tC[3 * pix];
-                const float r1 = p.color[3 * pix + 1] - p.tC[3 * pix + 1];
-                const float r2 = p.color[3 * pix + 2] - p.tC[3 * pix + 2];
+                const float e0 = p.color[3 * pix] - p.tC[3 * pix];
+                const float e1 = p.color[3 * pix + 1] - p.tC[3 * pix + 1];
+                const float e2 = p.color[3 * pix + 2] - p.tC[3 * pix + 2];
                 const float k = p.wc * sc;
-                g0 = k * sgnf(r0); g1 = k * sgnf(r1); g2 = k * sgnf(r2);
-                lossv += (double)k * ((double)fabsf(r0) + (double)fabsf(r1) + (double)fabsf(r2));
+                g0 = k * sgnf(e0); g1 = k * sgnf(e1); g2 = k * sgnf(e2);
+                lossv += (double)k * ((double)fabsf(e0) + (double)fabsf(e1) + (double)fabsf(e2));
             }
             if (md) {
-                const float r = p.depth[pix] - tDv;
+                const float e = p.depth[pix] - tDv;
                 const float k = p.wd * sd;
-                gD = k * sgnf(r);
-                lossv += (double)k * (double)fabsf(r);
+                gD = k * sgnf(e);
+                lossv += (double)k * (double)fabsf(e);
             }
         } else {
             if (p.dC) { g0 = p.dC[3 * pix]; g1 = p.dC[3 * pix + 1]; g2 = p.dC[3 * pix + 2]; }
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kBlock) k_composite_bwd(BwdArgs p) {
         }
         T = p.T_final[pix];
         L = p.last[pix];
-        // reference colour / depth of the pixel (its normalised render): the "behind"
+        // reference colour / depth of the pixel (its normalised render): the behind-
         // accumulators are kept relative to it, so c − c̄ and z − z̄ — differences of nearly
         // equal values when view-tied layers sit on one surface — keep fp32 relative precision
         const float Sv = p.sil[pix];
@@ -134,13 +135,9 @@ __global__ void __launch_bounds__(kBlock) k_composite_bwd(BwdArgs p) {
     }
     const bool on = inside && L > 0 && (g0 != 0.f || g1 != 0.f || g2 != 0.f || gD != 0.f || gS != 0.f);
     if (!on) L = 0;
-    const unsigned onmask = __ballot_sync(kFull, on);
-    const uint32_t wl = __reduce_max_sync(kFull, L);
-    if (lane == 0) sMax[w] = wl;
-    __syncthreads();
-    uint32_t nmax = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) nmax = max(nmax, sMax[i]);
+    sG[wl_][lane] = make_float4(g0, g1, g2, gD);
+    const unsigned onmask = __ballot_sync(kFullMask, on);
+    const int wmax = (int)__reduce_max_sync(kFullMask, L);  // sub-list positions < wmax matter
 
     // behind-accumulators relative to the references: Xb = Σ_{j behind} w_j (x_j − x_ref) with
     // w_j = α_j T_j / T_{i+1}, and Tb = 1 − Σ w_j = Π (1 − α_j) (so x_i − x̄ = (x_i − x_ref) − Xb +
@@ -150,148 +147,115 @@ __global__ void __launch_bounds__(kBlock) k_composite_bwd(BwdArgs p) {
     float K00 = 0.f, K01 = 0.f, K02 = 0.f, K10 = 0.f, K11 = 0.f, K12 = 0.f, K20 = 0.f, K21 = 0.f, K22 = 0.f;
     const float fmean = 0.5f * (p.in.fx + p.in.fy);
 
-    for (int cb = nmax > 0 ? (int)((nmax - 1) / kChunk) * kChunk : -kChunk; cb >= 0; cb -= kChunk) {
-        const int m = min(kChunk, n - cb);
-        if (tid < m) {
-            const uint32_t g = p.sorted[start + cb + tid];
-            const float4 pr = p.proj[g];
-            const float s = fabsf(pr.w);
-            const float s2 = __fmul_rn(s, s);
-            sA[tid] = make_float4(pr.x, pr.y, __fmul_rn(9.0f, s2), __fdividef(-0.5f * kLog2e, s2));
-            sB[tid] = p.col_opa[g];
-            sZ[tid] = pr.z;
-            sR[tid] = p.rect[g];
-            sGid[tid] = g;
+    const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
+    EntryRegs nxt;
+    fetch_entry(nxt, list, bb_top + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    for (int bb = bb_top; bb >= 0; bb -= 32) {
+        const EntryRegs cur = nxt;
+        fetch_entry(nxt, list, bb - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);  // next (lower) batch
+        const int jj = bb + (int)lane;
+        unsigned mj = 0u;
+        float4 Aj = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (jj < wmax) {   // wmax ≤ cnt
+            Aj = entry_geom(cur.pr);
+            sA[wl_][lane] = Aj;
+            sB[wl_][lane] = cur.co;
+            sZ[wl_][lane] = cur.pr.z;
             if (POSE) {
                 float xc[3];
-                view_transform(P.R, P.t, p.pos_rad[g], xc);
-                sX[tid] = make_float4(xc[0], xc[1], xc[2], pr.w);
-            } else {
-                sX[tid] = make_float4(0.f, 0.f, 0.f, pr.w);
+                view_transform(P.R, P.t, __ldg(p.pos_rad + cur.g), xc);
+                sX[wl_][lane] = make_float4(xc[0], xc[1], xc[2], cur.pr.w);
             }
-            if (ATTR) {
-#pragma unroll
-                for (int q = 0; q < 5; ++q) sAcc[q * kChunk + tid] = 0.0f;
-            }
+            mj = lane_mask(Aj, cur.r, sx, sy) & onmask;
         }
-        __syncthreads();
-        if (wl > (uint32_t)cb) {
-            int cnt = 0;
-            for (int j = 0; j < m; j += 32) {
-                const int e = j + (int)lane;
-                const unsigned msk = (e < m && (uint32_t)(cb + e) < wl) ? subtile_mask_b(sR[e], sx, sy) & onmask : 0u;
-                const unsigned b = __ballot_sync(kFull, msk != 0u);
-                if (msk) {
-                    const int pos = cnt + __popc(b & lanemask_lt());
-                    sIdx[w][pos] = (uint16_t)e;
-                    sMsk[w][pos] = msk;
-                }
-                cnt += __popc(b);
-            }
-            __syncwarp();
-            for (int k = cnt - 1; k >= 0; --k) {
-                const int e = sIdx[w][k];
-                const unsigned msk = sMsk[w][k];
-                bool proc = false;
-                float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, dsg = 0.f;
-                if (((msk >> lane) & 1u) && (uint32_t)(cb + e) < L) {
-                    const float4 A = sA[e];
-                    const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
-                    const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-                    if (d2 <= A.z) {
-                        const float4 B = sB[e];
-                        const float wgt = fast_exp2(d2 * A.w);
-                        const float raw = __fmul_rn(B.w, wgt);
-                        const bool aclamp = raw > kAlphaMax;
-                        const float a = aclamp ? kAlphaMax : raw;
-                        if (a >= 1.0f / 255.0f) {
-                            proc = true;
-                            const float z = sZ[e];
-                            const float Ti = __fdividef(T, 1.0f - a);
-                            const float om = a * Ti;
-                            dc0 = g0 * om; dc1 = g1 * om; dc2 = g2 * om;
-                            const float e0 = B.x - r0, e1 = B.y - r1, e2 = B.z - r2, ez = z - rz;
-                            const float fpart = g0 * (e0 - Cb0 + r0 * Tb) + g1 * (e1 - Cb1 + r1 * Tb) +
-                                                g2 * (e2 - Cb2 + r2 * Tb) + gD * (ez - Db + rz * Tb) + gS * Tb;
-                            const float dA = Ti * fpart;
-                            const float oma = 1.0f - a;
-                            Cb0 = a * e0 + oma * Cb0;
-                            Cb1 = a * e1 + oma * Cb1;
-                            Cb2 = a * e2 + oma * Cb2;
-                            Db = a * ez + oma * Db;
-                            Tb = oma * Tb;
-                            T = Ti;
-                            float gww = 0.f;
-                            if (!aclamp) {
-                                dop = dA * wgt;
-                                gww = dA * B.w * wgt;  // dL/dw · w
-                            }
-                            const float4 X = sX[e];
-                            const float s = fabsf(X.w);
-                            const float inv_s2 = __fdividef(1.0f, s * s);
-                            const float du = gww * dx * inv_s2;   // ∂w/∂u = w (x − u) / σ²
-                            const float dv = gww * dy * inv_s2;
-                            dsg = gww * d2 * inv_s2 / s;          // ∂w/∂σ = w d² / σ³
-                            if (POSE) {
-                                const float iz = 1.0f / z;
-                                float dzt = gD * om - (du * (A.x - p.in.cx) + dv * (A.y - p.in.cy)) * iz;
-                                if (X.w > 0.f) dzt -= dsg * s * iz;  // ∂σ/∂z = −σ/z (unclamped)
-                                const float gx = du * p.in.fx * iz, gy = dv * p.in.fy * iz, gz = dzt;
-                                h0 += gx; h1 += gy; h2 += gz;
-                                K00 = fmaf(X.x, gx, K00); K01 = fmaf(X.x, gy, K01); K02 = fmaf(X.x, gz, K02);
-                                K10 = fmaf(X.y, gx, K10); K11 = fmaf(X.y, gy, K11); K12 = fmaf(X.y, gz, K12);
-                                K20 = fmaf(X.z, gx, K20); K21 = fmaf(X.z, gy, K21); K22 = fmaf(X.z, gz, K22);
-                            }
-                        }
-                    }
-                }
-                if (ATTR) {
-                    const unsigned pm = __ballot_sync(kFull, proc);
-                    if (pm) {
-                        if (__popc(pm) == 1) {
-                            if (proc) {
-                                atomicAdd(&sAcc[0 * kChunk + e], dc0);
-                                atomicAdd(&sAcc[1 * kChunk + e], dc1);
-                                atomicAdd(&sAcc[2 * kChunk + e], dc2);
-                                atomicAdd(&sAcc[3 * kChunk + e], dop);
-                                atomicAdd(&sAcc[4 * kChunk + e], dsg);
-                            }
-                        } else {
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) {
-                                dc0 += __shfl_xor_sync(kFull, dc0, o);
-                                dc1 += __shfl_xor_sync(kFull, dc1, o);
-                                dc2 += __shfl_xor_sync(kFull, dc2, o);
-                                dop += __shfl_xor_sync(kFull, dop, o);
-                                dsg += __shfl_xor_sync(kFull, dsg, o);
-                            }
-                            if (lane == 0) {
-                                atomicAdd(&sAcc[0 * kChunk + e], dc0);
-                                atomicAdd(&sAcc[1 * kChunk + e], dc1);
-                                atomicAdd(&sAcc[2 * kChunk + e], dc2);
-                                atomicAdd(&sAcc[3 * kChunk + e], dop);
-                                atomicAdd(&sAcc[4 * kChunk + e], dsg);
-                            }
-                        }
+        __syncwarp();
+        unsigned bits = transpose32(mj, lane);
+        // ---- phase 1: lane = pixel, back to front ----
+        while (bits) {
+            const int k = 31 - __clz(bits);
+            bits &= ~(1u << k);
+            float om = 0.f, dAe = 0.f;
+            if (bb + k < (int)L) {
+                const float4 A = sA[wl_][k];
+                const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
+                const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+                if (d2 <= A.z) {
+                    const float4 B = sB[wl_][k];
+                    const float raw = __fmul_rn(B.w, fast_exp2(d2 * A.w));
+                    const bool aclamp = raw > kAlphaMax;
+                    const float a = aclamp ? kAlphaMax : raw;
+                    if (a >= 1.0f / 255.0f) {
+                        const float oma = 1.0f - a;
+                        const float Ti = __fdividef(T, oma);
+                        om = a * Ti;
+                        const float e0 = B.x - r0, e1 = B.y - r1, e2 = B.z - r2, ez = sZ[wl_][k] - rz;
+                        const float fpart = g0 * (e0 - Cb0 + r0 * Tb) + g1 * (e1 - Cb1 + r1 * Tb) +
+                                            g2 * (e2 - Cb2 + r2 * Tb) + gD * (ez - Db + rz * Tb) + gS * Tb;
+                        dAe = aclamp ? 0.f : Ti * fpart;
+                        Cb0 = a * e0 + oma * Cb0;
+                        Cb1 = a * e1 + oma * Cb1;
+                        Cb2 = a * e2 + oma * Cb2;
+                        Db = a * ez + oma * Db;
+                        Tb = oma * Tb;
+                        T = Ti;
                     }
                 }
             }
+            M[k][lane] = make_float2(om, dAe);
         }
-        __syncthreads();
-        if (ATTR && tid < m) {
-            const uint32_t g = sGid[tid];
-            if ((int64_t)g >= p.learn_begin && (int64_t)g < p.learn_end) {
-                const float a0 = sAcc[tid], a1 = sAcc[kChunk + tid], a2 = sAcc[2 * kChunk + tid];
-                const float a3 = sAcc[3 * kChunk + tid], a4 = sAcc[4 * kChunk + tid];
+        __syncwarp();
+        // ---- phase 2: lane = entry, over the pixels its footprint covers ----
+        if (mj) {
+            const float4 B = cur.co;
+            const float z = cur.pr.z;
+            float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, sw2 = 0.f, swx = 0.f, swy = 0.f, dzd = 0.f;
+            unsigned mm = mj;
+            while (mm) {
+                const int i = __ffs(mm) - 1;
+                mm &= mm - 1u;
+                const float2 md = M[lane][i];
+                if (md.x == 0.f) continue;  // not composited (ω > 0 for every composited pair)
+                const float4 gp = sG[wl_][i];
+                dc0 = fmaf(gp.x, md.x, dc0);
+                dc1 = fmaf(gp.y, md.x, dc1);
+                dc2 = fmaf(gp.z, md.x, dc2);
+                dzd = fmaf(gp.w, md.x, dzd);
+                if (md.y != 0.f) {
+                    const float dx = (float)(sx + (i & 7)) - Aj.x, dy = (float)(sy + (i >> 3)) - Aj.y;
+                    const float d2 = dx * dx + dy * dy;
+                    const float dw = md.y * fast_exp2(d2 * Aj.w);  // dL/dα · w  (= ∂L/∂o contribution)
+                    dop += dw;
+                    sw2 = fmaf(dw, d2, sw2);
+                    swx = fmaf(dw, dx, swx);
+                    swy = fmaf(dw, dy, swy);
+                }
+            }
+            // dL/dw·w = dL/dα·o·w;  ∂w/∂σ = w d²/σ³, ∂w/∂u = w (x−u)/σ², ∂w/∂v = w (y−v)/σ²
+            const float s = fabsf(cur.pr.w);
+            const float inv_s2 = __fdividef(1.0f, s * s);
+            const float dsg = B.w * sw2 * inv_s2 / s;
+            if (ATTR && (int64_t)cur.g >= p.learn_begin && (int64_t)cur.g < p.learn_end) {
                 const bool wc = p.want & VTGS_GRAD_COLOR, wo = p.want & VTGS_GRAD_OPACITY;
-                if ((wc && (a0 != 0.f || a1 != 0.f || a2 != 0.f)) || (wo && a3 != 0.f))
-                    atomicAdd(&p.d_col_opa[g], make_float4(wc ? a0 : 0.f, wc ? a1 : 0.f, wc ? a2 : 0.f, wo ? a3 : 0.f));
-                const float4 X = sX[tid];
-                if ((p.want & VTGS_GRAD_RADIUS) && X.w > 0.f && a4 != 0.f)
-                    atomicAdd(&p.d_radius[g], a4 * fmean / sZ[tid]);  // ∂σ/∂r = f/z
+                if ((wc && (dc0 != 0.f || dc1 != 0.f || dc2 != 0.f)) || (wo && dop != 0.f))
+                    atomicAdd(&p.d_col_opa[cur.g],
+                              make_float4(wc ? dc0 : 0.f, wc ? dc1 : 0.f, wc ? dc2 : 0.f, wo ? dop : 0.f));
+                if ((p.want & VTGS_GRAD_RADIUS) && cur.pr.w > 0.f && dsg != 0.f)
+                    atomicAdd(&p.d_radius[cur.g], dsg * fmean / z);  // ∂σ/∂r = f/z
+            }
+            if (POSE) {
+                const float4 X = sX[wl_][lane];
+                const float du = B.w * swx * inv_s2, dv = B.w * swy * inv_s2;
+                const float iz = 1.0f / z;
+                float dzt = dzd - (du * (Aj.x - p.in.cx) + dv * (Aj.y - p.in.cy)) * iz;
+                if (X.w > 0.f) dzt -= dsg * s * iz;  // ∂σ/∂z = −σ/z (unclamped)
+                const float gx = du * p.in.fx * iz, gy = dv * p.in.fy * iz, gz = dzt;
+                h0 += gx; h1 += gy; h2 += gz;
+                K00 = fmaf(X.x, gx, K00); K01 = fmaf(X.x, gy, K01); K02 = fmaf(X.x, gz, K02);
+                K10 = fmaf(X.y, gx, K10); K11 = fmaf(X.y, gy, K11); K12 = fmaf(X.y, gz, K12);
+                K20 = fmaf(X.z, gx, K20); K21 = fmaf(X.z, gy, K21); K22 = fmaf(X.z, gz, K22);
             }
         }
-        if (ATTR) __syncthreads();
+        __syncwarp();
     }
 
     if (POSE || LOSS) {
@@ -299,17 +263,13 @@ __global__ void __launch_bounds__(kBlock) k_composite_bwd(BwdArgs p) {
 #pragma unroll
         for (int q = 0; q < 13; ++q) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(kFull, v[q], o);
+            for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(kFullMask, v[q], o);
         }
-        if (lane == 0)
+        if (lane < 13) {
+            double out = 0.0;
 #pragma unroll
-            for (int q = 0; q < 13; ++q) sRed[w][q] = v[q];
-        __syncthreads();
-        if (tid < 13) {
-            double s = 0.0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) s += sRed[i][tid];
-            p.partials[(size_t)tile * 16 + tid] = s;
+            for (int q = 0; q < 13; ++q) out = (int)lane == q ? v[q] : out;
+            p.partials[((size_t)tile * 8 + sub) * 16 + lane] = out;
         }
     }
 }
@@ -392,9 +352,29 @@ __global__ void __launch_bounds__(256) k_pose_finalize(const double *__restrict_
     }
 }
 
+constexpr size_t kBwdDynSmem = sizeof(float2) * kBwdWarps * 32 * 33;
+
 template <bool A, bool P, bool L>
 static void launch_bwd_t(const BwdArgs &a, int T, cudaStream_t s) {
-    k_composite_bwd<A, P, L><<<T, kBlock, 0, s>>>(a);
+    k_composite_bwd<A, P, L><<<T * (8 / kBwdWarps), kBwdWarps * 32, kBwdDynSmem, s>>>(a);
+}
+
+template <bool A, bool P, bool L>
+static cudaError_t set_bwd_attr() {
+    return cudaFuncSetAttribute(k_composite_bwd<A, P, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kBwdDynSmem);
+}
+
+cudaError_t backward_set_attributes() {
+    cudaError_t e = set_bwd_attr<false, false, false>();
+    if (!e) e = set_bwd_attr<false, false, true>();
+    if (!e) e = set_bwd_attr<false, true, false>();
+    if (!e) e = set_bwd_attr<false, true, true>();
+    if (!e) e = set_bwd_attr<true, false, false>();
+    if (!e) e = set_bwd_attr<true, false, true>();
+    if (!e) e = set_bwd_attr<true, true, false>();
+    if (!e) e = set_bwd_attr<true, true, true>();
+    return e;
 }
 
 cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const float *dS,
@@ -406,7 +386,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     cudaError_t err;
     BwdArgs a{};
     a.proj = c.proj; a.rect = c.rect; a.col_opa = c.col_opa; a.pos_rad = c.pos_rad;
-    a.tile_count = c.tile_count; a.tile_start = c.tile_start; a.sorted = c.vals;
+    a.tile_count = c.tile_count; a.tile_start = c.tile_start; a.sub_lists = c.sub_lists; a.sub_count = c.sub_count;
     a.W = W; a.H = H; a.ntx = ntx;
     a.color = c.color; a.depth = c.depth; a.sil = c.sil; a.T_final = c.T_final; a.last = c.last;
     a.dC = dC; a.dD = dD; a.dS = dS;
@@ -446,7 +426,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     if ((err = cudaGetLastError())) return err;
     if (P || (L && loss_out)) {
         LaunchScope ls(&c, kFinalize, s);
-        k_pose_finalize<<<1, 256, 0, s>>>(c.partials, T, c.view_copy, P ? d_pose : nullptr, L ? loss_out : nullptr);
+        k_pose_finalize<<<1, 256, 0, s>>>(c.partials, T * 8, c.view_copy, P ? d_pose : nullptr, L ? loss_out : nullptr);
         if ((err = cudaGetLastError())) return err;
     }
     return cudaSuccess;

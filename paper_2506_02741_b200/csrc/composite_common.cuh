@@ -1,0 +1,98 @@
+// composite_common.cuh — machinery shared by the forward and backward compositing kernels.
+//
+// Work decomposition (DESIGN.md §4 K6/K7).  Every 16×16 tile is split into eight 8×4 sub-tiles
+// and the tile sort also emits, per sub-tile, the (depth-ordered) sub-list of the tile entries
+// whose footprint rect touches that sub-tile.  One WARP owns one sub-tile (lane = pixel) and
+// walks its sub-list independently of every other warp — no block barriers, so a warp whose
+// pixels are all saturated stops at once.  The sub-list is consumed 32 entries at a time:
+//   1. lane j gathers entry j (prefetched one batch ahead through registers) and builds the
+//      32-bit mask of the warp's pixels inside the entry's rect and, conservatively, inside its
+//      3σ disc;
+//   2. the 32×32 bit matrix is transposed across the warp (5 shuffle stages), so lane i holds
+//      the bits of exactly the entries that can touch ITS pixel;
+//   3. each lane walks only its own candidates (the forward front to back; the backward back
+//      to front, then a second phase where lane j sums entry j's gradient over its pixels).
+#pragma once
+
+#include "vtgs_internal.cuh"
+
+namespace vtgs {
+
+constexpr unsigned kFullMask = 0xffffffffu;
+
+// One sub-list entry held in registers (gathered one batch ahead).
+struct EntryRegs {
+    uint32_t g;
+    float4 pr;
+    float4 co;
+    uint2 r;
+};
+
+__device__ __forceinline__ void fetch_entry(EntryRegs &er, const uint32_t *__restrict__ list, int idx, int n,
+                                            const float4 *__restrict__ proj, const float4 *__restrict__ col,
+                                            const uint2 *__restrict__ rect) {
+    if (idx >= 0 && idx < n) {
+        er.g = __ldg(list + idx);
+        er.pr = __ldg(proj + er.g);
+        er.co = __ldg(col + er.g);
+        er.r = __ldg(rect + er.g);
+    }
+}
+
+// (u, v, 9σ² exact fp32 — the truncation threshold, −log2(e)/(2σ²))
+__device__ __forceinline__ float4 entry_geom(const float4 pr) {
+    const float s = fabsf(pr.w);
+    const float s2 = __fmul_rn(s, s);
+    return make_float4(pr.x, pr.y, __fmul_rn(9.0f, s2), __fdividef(-0.5f * kLog2e, s2));
+}
+
+// Mask of the warp's 32 pixels (bit = (y−sy)·8 + (x−sx)) inside the entry's rect and,
+// conservatively, inside its disc d² ≤ 9σ².  The exact fp32 test is re-done per pixel in the
+// compositing loops; this mask only has to be a superset of the pixels that pass it: row y
+// is kept iff fl(dy·dy) ≤ 9σ² (the same fp32 dy² the exact test adds to a non-negative dx²),
+// and its columns are widened by 0.01 px around u ± √(9σ² − dy²).
+__device__ __forceinline__ unsigned lane_mask(const float4 A, const uint2 r, int sx, int sy) {
+    const int x0 = max((int)(r.x & 0xffffu), sx), x1 = min((int)(r.x >> 16), sx + 7);
+    const int y0 = max((int)(r.y & 0xffffu), sy), y1 = min((int)(r.y >> 16), sy + 3);
+    unsigned m = 0;
+    if (x0 > x1) return 0u;
+    for (int y = y0; y <= y1; ++y) {
+        const float dy = __fsub_rn((float)y, A.y);
+        const float dy2 = __fmul_rn(dy, dy);
+        if (!(dy2 <= A.z)) continue;
+        const float hw = sqrtf(A.z - dy2) + 0.01f;
+        const int xa = max(x0, (int)ceilf(A.x - hw)), xb = min(x1, (int)floorf(A.x + hw));
+        if (xa > xb) continue;
+        const unsigned row = (0xffu >> (7 - (xb - sx))) & (0xffu << (xa - sx));
+        m |= row << (8 * (y - sy));
+    }
+    return m;
+}
+
+// 32×32 bit-matrix transpose across the warp: lane j holds row j on entry, lane i holds
+// column i on exit (bit j of the result = bit i of lane j's input).
+__device__ __forceinline__ unsigned transpose32(unsigned x, unsigned lane) {
+    const unsigned M[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int s = 16 >> i;
+        const unsigned y = __shfl_xor_sync(kFullMask, x, s);
+        x = (lane & s) ? ((x & ~M[i]) | ((y & ~M[i]) >> s)) : ((x & M[i]) | ((y & M[i]) << s));
+    }
+    return x;
+}
+
+// Bit s (s = 2k + c) set iff the rect touches sub-tile (c, k) = pixels
+// [tx0 + 8c, tx0 + 8c + 7] × [ty0 + 4k, ty0 + 4k + 3] of the tile at (tx0, ty0).
+__device__ __forceinline__ unsigned subtile_bits(uint2 r, int tx0, int ty0) {
+    const int x0 = (int)(r.x & 0xffffu), x1 = (int)(r.x >> 16);
+    const int y0 = (int)(r.y & 0xffffu), y1 = (int)(r.y >> 16);
+    const unsigned cols = (x0 <= tx0 + 7 ? 1u : 0u) | (x1 >= tx0 + 8 ? 2u : 0u);
+    unsigned wm = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (y0 <= ty0 + 4 * k + 3 && y1 >= ty0 + 4 * k) wm |= cols << (2 * k);
+    return wm;
+}
+
+}  // namespace vtgs

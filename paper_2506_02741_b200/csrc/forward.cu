@@ -9,7 +9,7 @@
 // per warp), then each tile's bucket is sorted in shared memory by (z bits, gid) — one
 // bucket-scatter pass plus an on-chip sort instead of a multi-pass global 64-bit radix sort
 // (K4/K5).
-#include "vtgs_internal.cuh"
+#include "composite_common.cuh"
 
 namespace vtgs {
 
@@ -308,175 +308,85 @@ __device__ __forceinline__ int block_sort_zgid(uint32_t *K0, uint32_t *V0, uint3
     return npass & 1;
 }
 
+// Sub-lists of the sorted tile list: sub-tile s (8×4 pixels, composite_common.cuh) gets, in
+// tile-list order, every entry whose rect touches it.  Stored at out + s·n (capacity n each);
+// counts at sub_count[0..7].  Stable block-wide compaction, 256 entries per round.
+__device__ __forceinline__ void build_sublists(const uint32_t *V, int n, const uint2 *__restrict__ rect, int tx0,
+                                               int ty0, uint32_t *__restrict__ out,
+                                               uint32_t *__restrict__ sub_count, uint32_t *sh) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint32_t *wcnt = sh;        // [8 warps][8 sub-tiles]
+    uint32_t *run = sh + 64;    // [8] running totals
+    if (tid < 8) run[tid] = 0;
+    __syncthreads();
+    for (int r0 = 0; r0 < n; r0 += kBlock) {
+        const int i = r0 + tid;
+        uint32_t g = 0, bits = 0;
+        if (i < n) {
+            g = V[i];
+            bits = subtile_bits(__ldg(rect + g), tx0, ty0);
+        }
+        unsigned b[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            b[s] = __ballot_sync(kFull, (bits >> s) & 1u);
+            if (lane == 0) wcnt[w * 8 + s] = __popc(b[s]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            if ((bits >> s) & 1u) {
+                uint32_t pos = run[s] + __popc(b[s] & lanemask_lt());
+                for (int ww = 0; ww < w; ++ww) pos += wcnt[ww * 8 + s];
+                out[(size_t)s * n + pos] = g;
+            }
+        }
+        __syncthreads();
+        if (tid < 8) {
+            uint32_t t = 0;
+            for (int ww = 0; ww < 8; ++ww) t += wcnt[ww * 8 + tid];
+            run[tid] += t;
+        }
+        __syncthreads();
+    }
+    if (tid < 8) sub_count[tid] = run[tid];
+}
+
 __global__ void __launch_bounds__(kBlock) k_tile_sort(const uint32_t *__restrict__ tile_count,
                                                       const uint32_t *__restrict__ tile_start,
                                                       uint32_t *keys, uint32_t *vals, uint32_t *keys2,
-                                                      uint32_t *vals2, uint32_t *offs) {
+                                                      uint32_t *vals2, uint32_t *offs,
+                                                      const uint2 *__restrict__ rect, int ntx,
+                                                      uint32_t *__restrict__ sub_lists,
+                                                      uint32_t *__restrict__ sub_count) {
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t hist[8 * 256];
     __shared__ uint32_t red[32];
     const int tile = blockIdx.x;
     const int n = (int)tile_count[tile];
-    if (n <= 1) return;
     const uint32_t base = tile_start[tile];
+    const int ty = tile / ntx, tx = tile - ty * ntx;
+    uint32_t *out = sub_lists + (size_t)8 * base;
     if (n <= kSortCap) {
         uint32_t *K0 = sm, *V0 = sm + kSortCap, *K1 = sm + 2 * kSortCap, *V1 = sm + 3 * kSortCap;
         uint16_t *OFF = reinterpret_cast<uint16_t *>(sm + 4 * kSortCap);
         for (int i = threadIdx.x; i < n; i += kBlock) { K0[i] = keys[base + i]; V0[i] = vals[base + i]; }
         __syncthreads();
-        const int odd = block_sort_zgid<uint16_t>(K0, V0, K1, V1, OFF, hist, red, n);
-        const uint32_t *Vr = odd ? V1 : V0;
+        const uint32_t *Vr = V0;
+        if (n > 1) Vr = block_sort_zgid<uint16_t>(K0, V0, K1, V1, OFF, hist, red, n) ? V1 : V0;
         for (int i = threadIdx.x; i < n; i += kBlock) vals[base + i] = Vr[i];
+        build_sublists(Vr, n, rect, tx * kTile, ty * kTile, out, sub_count + 8 * tile, hist);
     } else {
         const int odd = block_sort_zgid<uint32_t>(keys + base, vals + base, keys2 + base, vals2 + base,
                                                   offs + base, hist, red, n);
         if (odd)
             for (int i = threadIdx.x; i < n; i += kBlock) vals[base + i] = vals2[base + i];
+        __syncthreads();
+        build_sublists(vals + base, n, rect, tx * kTile, ty * kTile, out, sub_count + 8 * tile, hist);
     }
 }
 
 constexpr size_t kSortSmem = 4 * kSortCap * sizeof(uint32_t) + kSortCap * sizeof(uint16_t);
-
-// ------------------------------------------------------------------------------------------
-// K6: per-tile front-to-back compositing.  One CTA per 16×16 tile, one thread per pixel; warp w
-// owns the 8×4 sub-tile (w&1, w>>1).  The tile list is staged through shared memory 256
-// entries at a time; each warp compacts (ballot) the entries whose footprint rect touches its
-// sub-tile into a private list together with the 32-bit mask of its pixels inside the rect,
-// then all lanes walk that list in order.  DESIGN.md §3 step 7.
-// ------------------------------------------------------------------------------------------
-struct FwdArgs {
-    const float4 *proj;
-    const uint2 *rect;
-    const float4 *col_opa;
-    const uint32_t *tile_count;
-    const uint32_t *tile_start;
-    const uint32_t *sorted;
-    int W, H, ntx;
-    float *color, *depth, *sil, *T_final;
-    uint32_t *last;
-    DevScalars *dev;
-};
-
-__device__ __forceinline__ unsigned subtile_mask(uint2 r, int sx, int sy) {
-    const int x0 = (int)(r.x & 0xffffu) - sx, x1 = (int)(r.x >> 16) - sx;
-    const int y0 = (int)(r.y & 0xffffu) - sy, y1 = (int)(r.y >> 16) - sy;
-    const int cx0 = max(x0, 0), cx1 = min(x1, 7), cy0 = max(y0, 0), cy1 = min(y1, 3);
-    if (cx0 > cx1 || cy0 > cy1) return 0u;
-    const unsigned col = (0xffu >> (7 - cx1)) & (0xffu << cx0);
-    const unsigned rows = (0xffffffffu >> (8 * (3 - cy1))) & (0xffffffffu << (8 * cy0));
-    return (col * 0x01010101u) & rows;
-}
-
-__global__ void __launch_bounds__(kBlock) k_composite_fwd(FwdArgs p) {
-    __shared__ float4 sA[kChunk];  // u, v, 9σ², −log2(e)/(2σ²)
-    __shared__ float4 sB[kChunk];  // colour, opacity
-    __shared__ float sZ[kChunk];
-    __shared__ uint2 sR[kChunk];
-    __shared__ uint16_t sIdx[8][kChunk];
-    __shared__ unsigned sMsk[8][kChunk];
-
-    const int tile = blockIdx.x;
-    const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
-    const int tid = threadIdx.x, w = tid >> 5;
-    const unsigned lane = lane_id();
-    const int sx = tx * kTile + (w & 1) * 8, sy = ty * kTile + (w >> 1) * 4;
-    const int px = sx + (lane & 7), py = sy + (lane >> 3);
-    const bool inside = px < p.W && py < p.H;
-    const float pxf = (float)px, pyf = (float)py;
-    const int n = (int)p.tile_count[tile];
-    const uint32_t start = p.tile_start[tile];
-
-    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f, S = 0.f;
-    uint32_t lastc = 0, ne = 0, nc = 0;
-    bool done = !inside;
-    unsigned active = __ballot_sync(kFull, !done);
-
-    for (int cb = 0; cb < n; cb += kChunk) {
-        const int m = min(kChunk, n - cb);
-        if (tid < m) {
-            const uint32_t g = p.sorted[start + cb + tid];
-            const float4 pr = p.proj[g];
-            const float s = fabsf(pr.w);
-            const float s2 = __fmul_rn(s, s);
-            sA[tid] = make_float4(pr.x, pr.y, __fmul_rn(9.0f, s2), __fdividef(-0.5f * kLog2e, s2));
-            sB[tid] = p.col_opa[g];
-            sZ[tid] = pr.z;
-            sR[tid] = p.rect[g];
-        }
-        __syncthreads();
-        if (active) {
-            int cnt = 0;
-            for (int j = 0; j < m; j += 32) {
-                const int e = j + (int)lane;
-                const unsigned msk = e < m ? subtile_mask(sR[e], sx, sy) & active : 0u;
-                const unsigned b = __ballot_sync(kFull, msk != 0u);
-                if (msk) {
-                    const int pos = cnt + __popc(b & lanemask_lt());
-                    sIdx[w][pos] = (uint16_t)e;
-                    sMsk[w][pos] = msk;
-                }
-                cnt += __popc(b);
-            }
-            __syncwarp();
-            for (int k = 0; k < cnt; ++k) {
-                const int e = sIdx[w][k];
-                const unsigned msk = sMsk[w][k];
-                if (((msk >> lane) & 1u) && !done) {
-                    const float4 A = sA[e];
-                    const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
-                    const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-                    if (d2 <= A.z) {
-                        ++ne;
-                        const float4 B = sB[e];
-                        const float a = fminf(__fmul_rn(B.w, fast_exp2(d2 * A.w)), kAlphaMax);
-                        if (a >= 1.0f / 255.0f) {
-                            const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
-                            if (Tn < kTMin) {
-                                done = true;
-                            } else {
-                                const float om = a * T;
-                                C0 = fmaf(B.x, om, C0);
-                                C1 = fmaf(B.y, om, C1);
-                                C2 = fmaf(B.z, om, C2);
-                                D = fmaf(sZ[e], om, D);
-                                S += om;
-                                T = Tn;
-                                lastc = (uint32_t)(cb + e + 1);
-                                ++nc;
-                            }
-                        }
-                    }
-                }
-                if ((k & 7) == 7) {
-                    active = __ballot_sync(kFull, !done);
-                    if (!active) break;
-                }
-            }
-            active = __ballot_sync(kFull, !done);
-        }
-        if (!__syncthreads_or(active != 0u)) break;
-    }
-    if (inside) {
-        const int pix = py * p.W + px;
-        p.color[3 * pix + 0] = C0;
-        p.color[3 * pix + 1] = C1;
-        p.color[3 * pix + 2] = C2;
-        p.depth[pix] = D;
-        p.sil[pix] = S;
-        p.T_final[pix] = T;
-        p.last[pix] = lastc;
-    }
-    unsigned long long a = ne, b = nc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(kFull, a, o);
-        b += __shfl_xor_sync(kFull, b, o);
-    }
-    if (lane == 0) {
-        atomicAdd(&p.dev->e_eval, a);
-        atomicAdd(&p.dev->e_comp, b);
-    }
-}
 
 cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     const int W = c.intr.width, H = c.intr.height;
@@ -506,16 +416,11 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     {
         LaunchScope ls(&c, kSort, s);
         k_tile_sort<<<T, kBlock, kSortSmem, s>>>(c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2,
-                                                 c.offs);
+                                                 c.offs, c.rect, ntx, c.sub_lists, c.sub_count);
     }
     if ((err = cudaGetLastError())) return err;
-    FwdArgs a{c.proj, c.rect, c.col_opa, c.tile_count, c.tile_start, c.vals, W, H, ntx,
-              c.color, c.depth, c.sil, c.T_final, c.last, c.dev};
-    {
-        LaunchScope ls(&c, kCompFwd, s);
-        k_composite_fwd<<<T, kBlock, 0, s>>>(a);
-    }
-    return cudaGetLastError();
+    LaunchScope ls(&c, kCompFwd, s);
+    return launch_composite_fwd(c, s);
 }
 
 cudaError_t forward_set_attributes() {

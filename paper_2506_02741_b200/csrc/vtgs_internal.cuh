@@ -65,9 +65,11 @@ struct Ctx {
     uint32_t *keys2 = nullptr;       // fallback sort scratch [max_pairs]
     uint32_t *vals2 = nullptr;
     uint32_t *offs = nullptr;        // fallback sort ranks [max_pairs]
+    uint32_t *sub_lists = nullptr;   // per tile 8 sub-lists (8×4 sub-tiles), capacity 8·n_tile [8·max_pairs]
+    uint32_t *sub_count = nullptr;   // [8·max_tiles]
     float *T_final = nullptr;        // per pixel
-    uint32_t *last = nullptr;        // per pixel: 1 + list index of the last composited entry
-    double *partials = nullptr;      // per tile: 12 pose accumulators + loss + pad (16)
+    uint32_t *last = nullptr;        // per pixel: 1 + sub-list position of the last composited entry
+    double *partials = nullptr;      // per sub-tile warp: 12 pose accumulators + loss + pad (16)
     DevScalars *dev = nullptr;
     float *host_io = nullptr;        // step_host device staging (targets + pose)
     vtgs_pose *view_copy = nullptr;  // the forward's view pose, copied on the device for the backward
@@ -193,6 +195,8 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
                             int64_t learn_end, float4 *d_col_opa, float *d_radius, float *d_pose,
                             float *loss_out, cudaStream_t s);
 cudaError_t forward_set_attributes();
+cudaError_t backward_set_attributes();
+cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s);
 cudaError_t launch_pose_adam(Ctx &c, vtgs_pose *pose, const float *d_pose, float *state, float lr_rot,
                              float lr_trans, cudaStream_t s);
 
