@@ -258,18 +258,23 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
         __syncwarp();
     }
 
-    if (POSE || LOSS) {
+    if (POSE || LOSS) {   // fixed-order reduction: lanes → warp → CTA (one partial per CTA)
+        __shared__ double sRed[kBwdWarps][13];
         double v[13] = {h0, h1, h2, K00, K01, K02, K10, K11, K12, K20, K21, K22, lossv};
 #pragma unroll
         for (int q = 0; q < 13; ++q) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(kFullMask, v[q], o);
         }
-        if (lane < 13) {
-            double out = 0.0;
+        if (lane == 0)
 #pragma unroll
-            for (int q = 0; q < 13; ++q) out = (int)lane == q ? v[q] : out;
-            p.partials[((size_t)tile * 8 + sub) * 16 + lane] = out;
+            for (int q = 0; q < 13; ++q) sRed[wl_][q] = v[q];
+        __syncthreads();
+        if (threadIdx.x < 13) {
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < kBwdWarps; ++i) s += sRed[i][threadIdx.x];
+            p.partials[(size_t)blockIdx.x * 16 + threadIdx.x] = s;
         }
     }
 }
@@ -296,22 +301,38 @@ __global__ void __launch_bounds__(256) k_l1_count(const float *__restrict__ sil,
 // Fixed-order sum of the per-tile partials, then the rotation chain (DESIGN.md §3 step 11):
 //   dL/dt = −R Σg,  dL/dR = R Σ X_c gᵀ,  dL/dq̂ = Σ_ab (dL/dR)_ab ∂R_ab/∂q̂,
 //   dL/dq = (dL/dq̂ − q̂ (q̂·dL/dq̂)) / |q|.
-__global__ void __launch_bounds__(256) k_pose_finalize(const double *__restrict__ partials, int T,
-                                                       const vtgs_pose *__restrict__ view,
-                                                       float *__restrict__ d_pose,
-                                                       float *__restrict__ loss_out) {
-    __shared__ double red[256][13];
+constexpr int kFinThreads = 512;
+
+__global__ void __launch_bounds__(kFinThreads) k_pose_finalize(const double *__restrict__ partials, int T,
+                                                               const vtgs_pose *__restrict__ view,
+                                                               float *__restrict__ d_pose,
+                                                               float *__restrict__ loss_out) {
+    __shared__ double red[kFinThreads / 2][13];
     const int tid = threadIdx.x;
     double acc[13];
 #pragma unroll
     for (int q = 0; q < 13; ++q) acc[q] = 0.0;
-    for (int t = tid; t < T; t += 256)
+    for (int t = tid; t < T; t += kFinThreads) {
+        const double2 *r = reinterpret_cast<const double2 *>(partials + (size_t)t * 16);
+        double x[14];
 #pragma unroll
-        for (int q = 0; q < 13; ++q) acc[q] += partials[(size_t)t * 16 + q];
+        for (int h = 0; h < 7; ++h) {
+            const double2 d = __ldg(r + h);
+            x[2 * h] = d.x;
+            x[2 * h + 1] = d.y;
+        }
 #pragma unroll
-    for (int q = 0; q < 13; ++q) red[tid][q] = acc[q];
+        for (int q = 0; q < 13; ++q) acc[q] += x[q];
+    }
+    if (tid >= kFinThreads / 2)
+#pragma unroll
+        for (int q = 0; q < 13; ++q) red[tid - kFinThreads / 2][q] = acc[q];
     __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
+    if (tid < kFinThreads / 2)
+#pragma unroll
+        for (int q = 0; q < 13; ++q) red[tid][q] += acc[q];
+    __syncthreads();
+    for (int s = kFinThreads / 4; s > 0; s >>= 1) {
         if (tid < s)
 #pragma unroll
             for (int q = 0; q < 13; ++q) red[tid][q] += red[tid + s][q];
@@ -426,7 +447,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     if ((err = cudaGetLastError())) return err;
     if (P || (L && loss_out)) {
         LaunchScope ls(&c, kFinalize, s);
-        k_pose_finalize<<<1, 256, 0, s>>>(c.partials, T * 8, c.view_copy, P ? d_pose : nullptr, L ? loss_out : nullptr);
+        k_pose_finalize<<<1, kFinThreads, 0, s>>>(c.partials, T * (8 / kBwdWarps), c.view_copy, P ? d_pose : nullptr, L ? loss_out : nullptr);
         if ((err = cudaGetLastError())) return err;
     }
     return cudaSuccess;
