@@ -44,7 +44,7 @@ FLOPS_PER_COMP_BWD = 60.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="vtgs", choices=["vtgs", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[2, 4, 5])
@@ -79,7 +79,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -182,13 +182,14 @@ def run_reference(args):
     return 0
 
 
-def workload_config(cfg, args):
+def workload_config(cfg, args, n_views=1, views_per_rank=1):
     return {"workload": f"config{args.config}_{cfg.name}_{cfg.intr.width}x{cfg.intr.height}_K{cfg.K}",
-            "n_gaussians": cfg.n_slots, "image": [cfg.intr.width, cfg.intr.height], "views_per_rank": 1,
+            "n_gaussians": cfg.n_slots, "image": [cfg.intr.width, cfg.intr.height], "views_per_step": n_views,
+            "views_per_rank": views_per_rank,
             "loss": f"{cfg.loss_weights[0]}*L1(C) + {cfg.loss_weights[1]}*U*L1(D), sum form",
             "grads": "colour, opacity, radius", "seed": args.seed,
             "l2": "flushed between timed steps (256 MiB write outside the step events)",
-            "parallelism": f"dp{args.gpus} (view-sharded mapping, NCCL all-reduce of 5N fp32 grads)"}
+            "parallelism": f"dp{args.gpus} (view-sharded mapping, one NCCL all-reduce of the 5N fp32 gradient buffer per step)"}
 
 
 # ----------------------------------------------------------------------------------------
@@ -217,37 +218,38 @@ def main():
     # the section's Gaussians: every rank instantiates the same keyframes (no broadcast needed)
     pr, co = R.instantiate(torch.from_numpy(cfg.depth_stack()).to(dev), torch.from_numpy(cfg.rgb_stack()).to(dev),
                            vtgs.pose_tensor(cfg.pose_stack(), dev), cfg.intr, torch.from_numpy(cfg.opacity).to(dev))
-    # this rank's view: configs 4/5 list their batch of views; config 2 renders its keyframe 2 view at N=1
-    # and, with more ranks, keyframe (2 + rank) mod K (one view per rank, weak scaling)
+    # this rank's views.  Config 2 (the N = 1 headline): one view per rank — keyframe 2's at N = 1,
+    # keyframe (2 + rank) mod K with more ranks (weak scaling).  Configs 4 / 5: the config's batch of
+    # views sharded over the ranks (strong scaling; BASELINE.json configs[3], configs[4]).
+    from paper_2506_02741_b200.mapping import BatchedMapper, shard_views
     if args.config == 2:
-        k = (2 + rank) % cfg.K
-        view_np = np.asarray(cfg.keyframes[k].pose, dtype=np.float32)
-        tgt = cfg.keyframes[k]
+        kf = [(2 + rank) % cfg.K]
+        views_np = [np.asarray(cfg.keyframes[k].pose, dtype=np.float32) for k in kf]
+        tgts = [cfg.keyframes[k] for k in kf]
+        n_views_total = ws
+        scaling = "weak"
     else:
-        k = rank % len(cfg.views)
-        view_np = np.asarray(cfg.views[k], dtype=np.float32)
-        tgt = cfg.targets[k]
-    view = vtgs.pose_tensor(view_np, dev)
-    t_rgb = torch.from_numpy(tgt.rgb).to(dev)
-    t_depth = torch.from_numpy(tgt.depth).to(dev)
+        mine = shard_views(len(cfg.views), ws, rank)
+        views_np = [np.asarray(cfg.views[k], dtype=np.float32) for k in mine]
+        tgts = [cfg.targets[k] for k in mine]
+        n_views_total = len(cfg.views)
+        scaling = "strong"
+    view_np = views_np[0]
+    tgt = tgts[0]
     wc, wd = cfg.loss_weights
-    loss_spec = dict(target_rgb=t_rgb, target_depth=t_depth, w_color=wc, w_depth=wd, color_mask_mode=0,
-                     depth_mask_mode=0, normalize=0)
-    grads = torch.zeros(5 * N, device=dev)                  # d_col_opa (4N) | d_radius (N): one all-reduce
-    d_co = grads[:4 * N].view(N, 4)
-    d_r = grads[4 * N:]
-    out = (torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev), torch.empty((H, W), device=dev))
-    loss_out = torch.zeros(1, device=dev)
+    mapper = BatchedMapper(R, pr, co, cfg.intr, [vtgs.pose_tensor(v, dev) for v in views_np],
+                           [dict(rgb=torch.from_numpy(t.rgb).to(dev), depth=torch.from_numpy(t.depth).to(dev))
+                            for t in tgts], wc, wd)
+    grads = mapper.grads.flat
+    d_co, d_r = mapper.grads.d_col_opa, mapper.grads.d_radius
+    out = mapper.out
+    loss_out = mapper.loss
     want = vtgs.VTGS_GRAD_ATTR
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
     def step():
-        grads.zero_()
-        R.render_fwd(pr, co, view, cfg.intr, out=out)
-        R.render_bwd(want, d_col_opa=d_co, d_radius=d_r, loss=loss_spec, loss_out=loss_out)
-        if ws > 1:
-            dist.all_reduce(grads)
+        mapper.step(allreduce=ws > 1)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -285,9 +287,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
 
-    px_per_step = ws * W * H
+    px_per_step = n_views_total * W * H
     value = px_per_step / (ms_max * 1e-3) / 1e6
-    gps = ws * N / (ms_max * 1e-3)
+    gps = n_views_total * N / (ms_max * 1e-3)
 
     # ---------------- roofline of the dominant kernel (event-timed inside the timed region)
     stats = R.stats()
@@ -332,19 +334,20 @@ def main():
     # ---------------- e2e: the same step through the C-ABI with HOST buffers
     e2e = None
     if not args.profile_run:
-        h_rgb = torch.from_numpy(tgt.rgb).pin_memory()
-        h_depth = torch.from_numpy(tgt.depth).pin_memory()
-        h_view = torch.from_numpy(view_np.reshape(7).copy()).pin_memory()
+        h_tg = [(torch.from_numpy(t.rgb).pin_memory(), torch.from_numpy(t.depth).pin_memory()) for t in tgts]
+        h_views = [torch.from_numpy(v.reshape(7).copy()).pin_memory() for v in views_np]
         for _ in range(2):
             grads.zero_()
-            R.step_host(pr, co, h_view, cfg.intr, h_rgb, h_depth, wc, wd, 0, 0, 0, want, (0, N), out, d_co, d_r)
+            for hv, (hr, hd) in zip(h_views, h_tg):
+                R.step_host(pr, co, hv, cfg.intr, hr, hd, wc, wd, 0, 0, 0, want, (0, N), out, d_co, d_r)
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             grads.zero_()
-            R.step_host(pr, co, h_view, cfg.intr, h_rgb, h_depth, wc, wd, 0, 0, 0, want, (0, N), out, d_co, d_r)
+            for hv, (hr, hd) in zip(h_views, h_tg):
+                R.step_host(pr, co, hv, cfg.intr, hr, hd, wc, wd, 0, 0, 0, want, (0, N), out, d_co, d_r)
             if ws > 1:
                 dist.all_reduce(grads)
                 torch.cuda.synchronize()
@@ -355,8 +358,8 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_ms = float(te.item())
         e2e = {"value": px_per_step / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": int(h_rgb.numel() * 4 + h_depth.numel() * 4 + 28),
-               "d2h_bytes_per_step": 4,
+               "h2d_bytes_per_step": int(sum(hr.numel() * 4 + hd.numel() * 4 + 28 for hr, hd in h_tg)),
+               "d2h_bytes_per_step": 4 * len(h_tg),
                "api": "vtgs_step_host (host target RGB-D + pose in, host loss out)"}
 
     # ---------------- cpu baseline (oracle as it stands, bounded sample, rank 0, N=1 only)
@@ -372,10 +375,10 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded procedural rooms, ray-cast RGB-D; stands in for Replica/TUM/ScanNet)",
-            "config": workload_config(cfg, args),
+            "config": workload_config(cfg, args, n_views_total, len(views_np)),
             "gaussians_per_s": gps,
             "roofline": roofline,
             "stages": stage_json,

@@ -120,7 +120,7 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = dalloc(&c.sub_count, (size_t)8 * c.max_tiles);
     if (!e) e = dalloc(&c.T_final, px);
     if (!e) e = dalloc(&c.last, px);
-    if (!e) e = dalloc(&c.partials, (size_t)c.max_tiles * 8 * 16);
+    if (!e) e = dalloc(&c.partials, (size_t)c.max_tiles * 8 * 16 + 64 * 16);  // + k_pose_finalize level 2
     if (!e) e = dalloc(&c.dev, 1);
     if (!e) e = dalloc(&c.host_io, 4 * px + 64);
     if (!e) e = dalloc(&c.view_copy, 1);

@@ -301,18 +301,40 @@ __global__ void __launch_bounds__(256) k_l1_count(const float *__restrict__ sil,
 // Fixed-order sum of the per-tile partials, then the rotation chain (DESIGN.md §3 step 11):
 //   dL/dt = −R Σg,  dL/dR = R Σ X_c gᵀ,  dL/dq̂ = Σ_ab (dL/dR)_ab ∂R_ab/∂q̂,
 //   dL/dq = (dL/dq̂ − q̂ (q̂·dL/dq̂)) / |q|.
-constexpr int kFinThreads = 512;
+constexpr int kFinThreads = 256;
+constexpr int kFinBlocks = 64;
+
+// Two-level fixed-order reduction: block b sums rows [b·R, (b+1)·R) of the per-CTA partials
+// into partials2[b]; the last block to finish (ticket) sums partials2[0 .. kFinBlocks) in index
+// order — deterministic, and the row loads of the 64 blocks run in parallel.
+__device__ __forceinline__ void block_sum13(double acc[13], double (*red)[13]) {
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int q = 0; q < 13; ++q) red[tid][q] = acc[q];
+    __syncthreads();
+    for (int s = kFinThreads / 2; s > 0; s >>= 1) {
+        if (tid < s)
+#pragma unroll
+            for (int q = 0; q < 13; ++q) red[tid][q] += red[tid + s][q];
+        __syncthreads();
+    }
+}
 
 __global__ void __launch_bounds__(kFinThreads) k_pose_finalize(const double *__restrict__ partials, int T,
                                                                const vtgs_pose *__restrict__ view,
                                                                float *__restrict__ d_pose,
-                                                               float *__restrict__ loss_out) {
-    __shared__ double red[kFinThreads / 2][13];
+                                                               float *__restrict__ loss_out,
+                                                               double *__restrict__ partials2,
+                                                               unsigned int *__restrict__ ticket) {
+    __shared__ double red[kFinThreads][13];
+    __shared__ bool last;
     const int tid = threadIdx.x;
+    const int R = (T + kFinBlocks - 1) / kFinBlocks;
+    const int r0 = blockIdx.x * R, r1 = min(T, r0 + R);
     double acc[13];
 #pragma unroll
     for (int q = 0; q < 13; ++q) acc[q] = 0.0;
-    for (int t = tid; t < T; t += kFinThreads) {
+    for (int t = r0 + tid; t < r1; t += kFinThreads) {
         const double2 *r = reinterpret_cast<const double2 *>(partials + (size_t)t * 16);
         double x[14];
 #pragma unroll
@@ -324,20 +346,21 @@ __global__ void __launch_bounds__(kFinThreads) k_pose_finalize(const double *__r
 #pragma unroll
         for (int q = 0; q < 13; ++q) acc[q] += x[q];
     }
-    if (tid >= kFinThreads / 2)
-#pragma unroll
-        for (int q = 0; q < 13; ++q) red[tid - kFinThreads / 2][q] = acc[q];
+    block_sum13(acc, red);
+    if (tid < 13) partials2[blockIdx.x * 16 + tid] = red[0][tid];
+    __threadfence();
     __syncthreads();
-    if (tid < kFinThreads / 2)
-#pragma unroll
-        for (int q = 0; q < 13; ++q) red[tid][q] += acc[q];
+    if (tid == 0) last = atomicAdd(ticket, 1u) == kFinBlocks - 1;
     __syncthreads();
-    for (int s = kFinThreads / 4; s > 0; s >>= 1) {
-        if (tid < s)
+    if (!last) return;
+    __threadfence();
 #pragma unroll
-            for (int q = 0; q < 13; ++q) red[tid][q] += red[tid + s][q];
-        __syncthreads();
-    }
+    for (int q = 0; q < 13; ++q) acc[q] = 0.0;
+    if (tid < kFinBlocks)
+#pragma unroll
+        for (int q = 0; q < 13; ++q) acc[q] = __ldcg(partials2 + tid * 16 + q);
+    block_sum13(acc, red);
+    if (tid == 0) *ticket = 0u;
     if (tid == 0) {
         if (loss_out) *loss_out = (float)red[0][12];
         if (d_pose) {
@@ -447,7 +470,10 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     if ((err = cudaGetLastError())) return err;
     if (P || (L && loss_out)) {
         LaunchScope ls(&c, kFinalize, s);
-        k_pose_finalize<<<1, kFinThreads, 0, s>>>(c.partials, T * (8 / kBwdWarps), c.view_copy, P ? d_pose : nullptr, L ? loss_out : nullptr);
+        const int rows = T * (8 / kBwdWarps);
+        k_pose_finalize<<<kFinBlocks, kFinThreads, 0, s>>>(c.partials, rows, c.view_copy, P ? d_pose : nullptr,
+                                                           L ? loss_out : nullptr, c.partials + (size_t)c.max_tiles * 8 * 16,
+                                                           &c.dev->fin_ticket);
         if ((err = cudaGetLastError())) return err;
     }
     return cudaSuccess;

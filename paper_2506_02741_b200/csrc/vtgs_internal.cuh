@@ -36,6 +36,7 @@ struct DevScalars {
     unsigned int overflow;
     unsigned int count_c;     // fused-L1 mask counts (normalize = 1)
     unsigned int count_d;
+    unsigned int fin_ticket;  // k_pose_finalize last-block ticket (self-resetting)
 };
 
 enum Stage { kProject = 0, kScan, kEmit, kSort, kCompFwd, kL1Count, kCompBwd, kFinalize, kInstantiate,
