@@ -387,7 +387,7 @@ def main():
             "e2e": e2e,
             "clocks": clk,
             "gpu_launches": int(launches),
-            "loss": float(loss_out.item()),
+            "loss": float(loss_out.sum().item()),
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
