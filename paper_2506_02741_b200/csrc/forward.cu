@@ -313,19 +313,19 @@ __device__ __forceinline__ int block_sort_zgid(uint32_t *K0, uint32_t *V0, uint3
 // counts at sub_count[0..7].  Stable block-wide compaction, 256 entries per round.
 __device__ __forceinline__ void build_sublists(const uint32_t *V, int n, const uint2 *__restrict__ rect, int tx0,
                                                int ty0, uint32_t *__restrict__ out,
-                                               uint32_t *__restrict__ sub_count, uint32_t *sh) {
+                                               uint32_t *__restrict__ sub_count, uint32_t *sh, uint8_t *bits8) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     uint32_t *wcnt = sh;        // [8 warps][8 sub-tiles]
     uint32_t *run = sh + 64;    // [8] running totals
     if (tid < 8) run[tid] = 0;
+    // all rect gathers of the tile in flight together, then the ordered compaction rounds
+#pragma unroll 4
+    for (int i = tid; i < n; i += kBlock) bits8[i] = (uint8_t)subtile_bits(__ldg(rect + V[i]), tx0, ty0);
     __syncthreads();
     for (int r0 = 0; r0 < n; r0 += kBlock) {
         const int i = r0 + tid;
-        uint32_t g = 0, bits = 0;
-        if (i < n) {
-            g = V[i];
-            bits = subtile_bits(__ldg(rect + g), tx0, ty0);
-        }
+        const uint32_t bits = i < n ? bits8[i] : 0u;
+        const uint32_t g = i < n ? V[i] : 0u;
         unsigned b[8];
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
@@ -352,6 +352,9 @@ __device__ __forceinline__ void build_sublists(const uint32_t *V, int n, const u
     if (tid < 8) sub_count[tid] = run[tid];
 }
 
+// CAP: longest list sorted in shared memory by this instantiation.  Lists in (LO, CAP] are
+// sorted on chip; with GLOBAL = true, lists > CAP use the same code on global scratch.
+template <int LO, int CAP, bool GLOBAL>
 __global__ void __launch_bounds__(kBlock) k_tile_sort(const uint32_t *__restrict__ tile_count,
                                                       const uint32_t *__restrict__ tile_start,
                                                       uint32_t *keys, uint32_t *vals, uint32_t *keys2,
@@ -364,29 +367,35 @@ __global__ void __launch_bounds__(kBlock) k_tile_sort(const uint32_t *__restrict
     __shared__ uint32_t red[32];
     const int tile = blockIdx.x;
     const int n = (int)tile_count[tile];
+    if (n <= LO || (!GLOBAL && n > CAP)) return;
     const uint32_t base = tile_start[tile];
     const int ty = tile / ntx, tx = tile - ty * ntx;
     uint32_t *out = sub_lists + (size_t)8 * base;
-    if (n <= kSortCap) {
-        uint32_t *K0 = sm, *V0 = sm + kSortCap, *K1 = sm + 2 * kSortCap, *V1 = sm + 3 * kSortCap;
-        uint16_t *OFF = reinterpret_cast<uint16_t *>(sm + 4 * kSortCap);
+    if (n <= CAP) {
+        uint32_t *K0 = sm, *V0 = sm + CAP, *K1 = sm + 2 * CAP, *V1 = sm + 3 * CAP;
+        uint16_t *OFF = reinterpret_cast<uint16_t *>(sm + 4 * CAP);
         for (int i = threadIdx.x; i < n; i += kBlock) { K0[i] = keys[base + i]; V0[i] = vals[base + i]; }
         __syncthreads();
-        const uint32_t *Vr = V0;
-        if (n > 1) Vr = block_sort_zgid<uint16_t>(K0, V0, K1, V1, OFF, hist, red, n) ? V1 : V0;
+        bool odd = false;
+        if (n > 1) odd = block_sort_zgid<uint16_t>(K0, V0, K1, V1, OFF, hist, red, n);
+        const uint32_t *Vr = odd ? V1 : V0;
+        uint8_t *bits8 = reinterpret_cast<uint8_t *>(odd ? K0 : K1);  // the idle key buffer
         for (int i = threadIdx.x; i < n; i += kBlock) vals[base + i] = Vr[i];
-        build_sublists(Vr, n, rect, tx * kTile, ty * kTile, out, sub_count + 8 * tile, hist);
-    } else {
+        build_sublists(Vr, n, rect, tx * kTile, ty * kTile, out, sub_count + 8 * tile, hist, bits8);
+    } else if (GLOBAL) {
         const int odd = block_sort_zgid<uint32_t>(keys + base, vals + base, keys2 + base, vals2 + base,
                                                   offs + base, hist, red, n);
         if (odd)
             for (int i = threadIdx.x; i < n; i += kBlock) vals[base + i] = vals2[base + i];
         __syncthreads();
-        build_sublists(vals + base, n, rect, tx * kTile, ty * kTile, out, sub_count + 8 * tile, hist);
+        uint8_t *bits8 = reinterpret_cast<uint8_t *>(odd ? keys + base : keys2 + base);
+        build_sublists(vals + base, n, rect, tx * kTile, ty * kTile, out, sub_count + 8 * tile, hist, bits8);
     }
 }
 
+constexpr int kSortCapBig = 8192;
 constexpr size_t kSortSmem = 4 * kSortCap * sizeof(uint32_t) + kSortCap * sizeof(uint16_t);
+constexpr size_t kSortSmemBig = 4 * kSortCapBig * sizeof(uint32_t) + kSortCapBig * sizeof(uint16_t);
 
 cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     const int W = c.intr.width, H = c.intr.height;
@@ -415,8 +424,13 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     }
     {
         LaunchScope ls(&c, kSort, s);
-        k_tile_sort<<<T, kBlock, kSortSmem, s>>>(c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2,
-                                                 c.offs, c.rect, ntx, c.sub_lists, c.sub_count);
+        // lists ≤ 4096 on chip with 3 CTAs / SM; (4096, 8192] on chip with 1 CTA / SM; longer on
+        // global scratch (the second launch exits at once for every tile it does not own)
+        k_tile_sort<-1, kSortCap, false><<<T, kBlock, kSortSmem, s>>>(
+            c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists, c.sub_count);
+        k_tile_sort<kSortCap, kSortCapBig, true><<<T, kBlock, kSortSmemBig, s>>>(
+            c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists, c.sub_count);
+        ++c.launches;  // two kernels inside this scope
     }
     if ((err = cudaGetLastError())) return err;
     LaunchScope ls(&c, kCompFwd, s);
@@ -424,7 +438,12 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
 }
 
 cudaError_t forward_set_attributes() {
-    return cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_tile_sort<-1, kSortCap, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSortSmem);
+    if (!e)
+        e = cudaFuncSetAttribute(k_tile_sort<kSortCap, kSortCapBig, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBig);
+    return e;
 }
 
 }  // namespace vtgs
