@@ -60,7 +60,8 @@ __device__ __forceinline__ unsigned lane_mask(const float4 A, const uint2 r, int
         const float dy = __fsub_rn((float)y, A.y);
         const float dy2 = __fmul_rn(dy, dy);
         if (!(dy2 <= A.z)) continue;
-        const float hw = sqrtf(A.z - dy2) + 0.01f;
+        const float r2 = A.z - dy2;                                  // ≥ 0
+        const float hw = r2 * rsqrt_approx(fmaxf(r2, 1e-30f)) + 0.01f; // √r2 (+ ≤ 2⁻²² rel.) + margin
         const int xa = max(x0, (int)ceilf(A.x - hw)), xb = min(x1, (int)floorf(A.x + hw));
         if (xa > xb) continue;
         const unsigned row = (0xffu >> (7 - (xb - sx))) & (0xffu << (xa - sx));

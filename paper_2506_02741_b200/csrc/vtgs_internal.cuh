@@ -172,6 +172,12 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ unsigned lane_id() {
     unsigned l;
     asm("mov.u32 %0, %%laneid;" : "=r"(l));
