@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="vtgs", choices=["vtgs", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[2, 4, 5])
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no clocks / cpu baseline)")
@@ -195,10 +195,112 @@ def workload_config(cfg, args, n_views=1, views_per_rank=1):
 # ----------------------------------------------------------------------------------------
 # the product arm
 # ----------------------------------------------------------------------------------------
+def run_tracking(args):
+    """Config 3 (BASELINE.json configs[2]): one STEP = tracking one frame = 40 iterations of
+    forward + fused masked-L1 (Eq. 1, W mask, mean form) + pose backward + device Adam, captured in
+    one CUDA graph.  Tracking a single view does not shard: with N ranks every rank tracks its own
+    replica (no collective) and `value` counts all ranks' pixels ("replicas only")."""
+    import torch
+    import torch.distributed as dist
+    from paper_2506_02741_b200 import vtgs
+    from synth.scenes import make_config
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = make_config(3, args.seed)
+    W, H = cfg.intr.width, cfg.intr.height
+    N = cfg.n_slots
+    iters = cfg.extra["iterations"]
+    R = vtgs.Renderer(local, N, W, H)
+    pr, co = R.instantiate(torch.from_numpy(cfg.depth_stack()).to(dev), torch.from_numpy(cfg.rgb_stack()).to(dev),
+                           vtgs.pose_tensor(cfg.pose_stack(), dev), cfg.intr, torch.from_numpy(cfg.opacity).to(dev))
+    tg = cfg.targets[0]
+    L = dict(target_rgb=torch.from_numpy(tg.rgb).to(dev), target_depth=torch.from_numpy(tg.depth).to(dev),
+             w_color=cfg.loss_weights[0], w_depth=cfg.loss_weights[1], color_mask_mode=1, depth_mask_mode=1,
+             normalize=1)
+    init = vtgs.pose_tensor(np.asarray(cfg.views[0], dtype=np.float32), dev)
+    pose = init.clone()
+    state = torch.zeros(16, device=dev)
+    dp = torch.zeros(7, device=dev)
+    loss = torch.zeros(1, device=dev)
+    out = (torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev), torch.empty((H, W), device=dev))
+    s = torch.cuda.Stream()
+
+    def body(stream):
+        for _ in range(iters):
+            R.render_fwd(pr, co, pose, cfg.intr, out=out, stream=stream)
+            R.render_bwd(vtgs.VTGS_GRAD_POSE, d_pose=dp, loss=L, loss_out=loss, stream=stream)
+            R.pose_adam_step(pose, dp, state, cfg.extra["lr_rot"], cfg.extra["lr_trans"], stream=stream)
+
+    with torch.cuda.stream(s):           # warm-up (eager) before capture
+        body(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        body(s)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(max(args.warmup, 1)):
+        pose.copy_(init); state.zero_(); g.replay()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    cur = torch.cuda.current_stream()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        pose.copy_(init)
+        state.zero_()
+        ev[i][0].record(cur)
+        g.replay()
+        ev[i][1].record(cur)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    px = ws * iters * W * H
+    gt = cfg.extra["gt_pose"]
+    pf = pose.cpu().numpy()[0].astype(np.float64)
+    # per-kernel shares from an eager profiled frame (events cannot be recorded inside the graph)
+    R.set_profiling(True)
+    R.profile()
+    pose.copy_(init); state.zero_()
+    body(torch.cuda.current_stream())
+    prof = R.profile()
+    R.set_profiling(False)
+    if rank == 0:
+        line = {"metric": METRIC, "value": px / (ms * 1e-3) / 1e6, "unit": "Mpix/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"config3_tracking_{W}x{H}_K{cfg.K}", "n_gaussians": N,
+                           "iterations_per_step": iters, "graph": True, "loss": "0.5*W*L1(C) + 1.0*W*L1(D), mean",
+                           "l2": "flushed between timed steps", "parallelism": f"replicas x{ws}"},
+                "gaussians_per_s": ws * iters * N / (ms * 1e-3),
+                "tracking": {"t_err_init_m": float(np.linalg.norm(np.asarray(cfg.views[0])[4:] - gt[4:])),
+                             "t_err_final_m": float(np.linalg.norm(pf[4:] - gt[4:]))},
+                "stages_eager_frame_ms": {k: v[0] for k, v in prof.items() if v[1]},
+                "clocks": clk, "gpu_launches": int(args.steps * sum(v[1] for v in prof.values()))}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 3:
+        return run_tracking(args)
     import torch
     import torch.distributed as dist
     from paper_2506_02741_b200 import vtgs
