@@ -236,21 +236,38 @@ def ray_cast(scene: Scene, pose: np.ndarray, intr: Intrinsics, rng: np.random.Ge
     hit_hi = np.take_along_axis(t2 >= t1, exit_axis[:, None], 1)[:, 0]
     best_t = t_exit
     best_face = exit_axis * 2 + hit_hi.astype(np.int64)
+    all_idx = np.arange(n)
     for k, b in enumerate(scene.solids):
-        t1 = (b.lo - t) * inv
-        t2 = (b.hi - t) * inv
+        # rays that can hit the box: its 8 corners' image bbox (+2 px) when all are in front of
+        # the camera, else every ray (a speed-up only; the per-ray arithmetic is unchanged)
+        corners = np.array([[x, y, z] for x in (b.lo[0], b.hi[0]) for y in (b.lo[1], b.hi[1])
+                            for z in (b.lo[2], b.hi[2])])
+        cc = (corners - t) @ R
+        if np.all(cc[:, 2] > 0.05):
+            uu = intr.fx * cc[:, 0] / cc[:, 2] + intr.cx
+            vv = intr.fy * cc[:, 1] / cc[:, 2] + intr.cy
+            x0, x1 = int(max(0, np.floor(uu.min()) - 2)), int(min(W - 1, np.ceil(uu.max()) + 2))
+            y0, y1 = int(max(0, np.floor(vv.min()) - 2)), int(min(H - 1, np.ceil(vv.max()) + 2))
+            if x0 > x1 or y0 > y1:
+                continue
+            idx = (np.arange(y0, y1 + 1)[:, None] * W + np.arange(x0, x1 + 1)[None, :]).reshape(-1)
+        else:
+            idx = all_idx
+        t1 = (b.lo - t) * inv[idx]
+        t2 = (b.hi - t) * inv[idx]
         tmin_axis = np.minimum(t1, t2)
         tmax_axis = np.maximum(t1, t2)
         ent_axis = np.argmax(tmin_axis, axis=1)
-        t_ent = tmin_axis[np.arange(n), ent_axis]
+        t_ent = tmin_axis[np.arange(len(idx)), ent_axis]
         t_ex = np.min(tmax_axis, axis=1)
-        hit = (t_ent <= t_ex) & (t_ent > 1e-6) & (t_ent < best_t)
+        hit = (t_ent <= t_ex) & (t_ent > 1e-6) & (t_ent < best_t[idx])
         if np.any(hit):
-            best_t = np.where(hit, t_ent, best_t)
-            best_obj = np.where(hit, k, best_obj)
+            hi_ = idx[hit]
+            best_t[hi_] = t_ent[hit]
+            best_obj[hi_] = k
             # entering through the low face of an axis when the ray moves +axis
             lo_face = np.take_along_axis(t1 <= t2, ent_axis[:, None], 1)[:, 0]
-            best_face = np.where(hit, ent_axis * 2 + (~lo_face).astype(np.int64), best_face)
+            best_face[hi_] = (ent_axis * 2 + (~lo_face).astype(np.int64))[hit]
     pts = t[None, :] + best_t[:, None] * dw
     rgb = np.empty((n, 3))
     objs = [scene.shell] + scene.solids
