@@ -56,7 +56,7 @@ __device__ __forceinline__ float sgnf(float r) { return (float)((r > 0.0f) - (r 
 //             float4 + one float global atomic per (Gaussian, sub-tile), the pose chain is
 //             applied per (Gaussian, sub-tile) into the lane's 12 accumulators.
 // One warp per 8×4 sub-tile, kBwdWarps warps per CTA, no block barriers.
-constexpr int kBwdWarps = 4;
+constexpr int kBwdWarps = 2;
 
 template <bool ATTR, bool POSE, bool LOSS>
 __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
@@ -67,9 +67,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
     __shared__ float4 sG[kBwdWarps][32];             // per pixel (g_C, g_D)
     extern __shared__ float2 sMdyn[];                 // [kBwdWarps][32 entries][33 (pad)]
 
-    const int tile = blockIdx.x >> 1;
+    const int gsub = blockIdx.x * kBwdWarps + (int)(threadIdx.x >> 5);
+    const int tile = gsub >> 3;
     const int wl_ = threadIdx.x >> 5;
-    const int sub = (blockIdx.x & 1) * kBwdWarps + wl_;  // sub-tile 0..7 of the tile
+    const int sub = gsub & 7;  // sub-tile 0..7 of the tile
     float2 (*M)[33] = reinterpret_cast<float2 (*)[33]>(sMdyn + (size_t)wl_ * 32 * 33);
     const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
     const unsigned lane = lane_id();

@@ -20,14 +20,18 @@ struct FwdArgs {
     DevScalars *dev;
 };
 
-__global__ void __launch_bounds__(kBlock, 4) k_composite_fwd(FwdArgs p) {
-    __shared__ float4 sA[8][32];  // u, v, 9σ², −log2(e)/(2σ²) of the warp's current batch
-    __shared__ float4 sB[8][32];  // colour, opacity
-    __shared__ float sZ[8][32];
+constexpr int kFwdWarps = 2;  // warps (8×4 sub-tiles) per CTA: small CTAs retire independently
 
-    const int tile = blockIdx.x;
+__global__ void __launch_bounds__(kFwdWarps * 32, 16) k_composite_fwd(FwdArgs p) {
+    __shared__ float4 sA[kFwdWarps][32];  // u, v, 9σ², −log2(e)/(2σ²) of the warp's current batch
+    __shared__ float4 sB[kFwdWarps][32];  // colour, opacity
+    __shared__ float sZ[kFwdWarps][32];
+
+    const int wl = threadIdx.x >> 5;
+    const int gsub = blockIdx.x * kFwdWarps + wl;
+    const int tile = gsub >> 3;
     const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
-    const int w = threadIdx.x >> 5;
+    const int w = gsub & 7;
     const unsigned lane = lane_id();
     const int sx = tx * kTile + (w & 1) * 8, sy = ty * kTile + (w >> 1) * 4;
     const int px = sx + (lane & 7), py = sy + (lane >> 3);
@@ -50,9 +54,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_composite_fwd(FwdArgs p) {
         unsigned mj = 0u;
         if (bb + (int)lane < cnt) {
             const float4 A = entry_geom(cur.pr);
-            sA[w][lane] = A;
-            sB[w][lane] = cur.co;
-            sZ[w][lane] = cur.pr.z;
+            sA[wl][lane] = A;
+            sB[wl][lane] = cur.co;
+            sZ[wl][lane] = cur.pr.z;
             mj = lane_mask(A, cur.r, sx, sy) & active;
         }
         __syncwarp();
@@ -60,12 +64,12 @@ __global__ void __launch_bounds__(kBlock, 4) k_composite_fwd(FwdArgs p) {
         while (bits) {
             const int k = __ffs(bits) - 1;
             bits &= bits - 1u;
-            const float4 A = sA[w][k];
+            const float4 A = sA[wl][k];
             const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
             const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
             if (d2 <= A.z) {
                 ++ne;
-                const float4 B = sB[w][k];
+                const float4 B = sB[wl][k];
                 const float a = fminf(__fmul_rn(B.w, fast_exp2(d2 * A.w)), kAlphaMax);
                 if (a >= 1.0f / 255.0f) {
                     const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_composite_fwd(FwdArgs p) {
                         C0 = fmaf(B.x, om, C0);
                         C1 = fmaf(B.y, om, C1);
                         C2 = fmaf(B.z, om, C2);
-                        D = fmaf(sZ[w][k], om, D);
+                        D = fmaf(sZ[wl][k], om, D);
                         Sl += om;
                         T = Tn;
                         lastc = (uint32_t)(bb + k + 1);
@@ -116,7 +120,7 @@ cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
     const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile;
     FwdArgs a{c.proj, c.rect, c.col_opa, c.tile_count, c.tile_start, c.sub_lists, c.sub_count, W, H, ntx,
               c.color, c.depth, c.sil, c.T_final, c.last, c.dev};
-    k_composite_fwd<<<ntx * nty, kBlock, 0, s>>>(a);
+    k_composite_fwd<<<ntx * nty * 8 / kFwdWarps, kFwdWarps * 32, 0, s>>>(a);
     return cudaGetLastError();
 }
 
