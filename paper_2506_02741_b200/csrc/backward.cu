@@ -65,13 +65,16 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
     __shared__ float sZ[kBwdWarps][32];
     __shared__ float4 sX[kBwdWarps][POSE ? 32 : 1];  // X_c and ±σ (−: σ clamped)
     __shared__ float4 sG[kBwdWarps][32];             // per pixel (g_C, g_D)
-    extern __shared__ float2 sMdyn[];                 // [kBwdWarps][32 entries][33 (pad)]
+    // [kBwdWarps][32 entries][32 pixels]: phase 1 writes column = own lane (conflict-free per
+    // half-warp phase of the 64-bit stores), phase 2 reads row = own lane, walking its pixel bits
+    // from a lane-rotated start so the half-warp's reads spread over the banks
+    extern __shared__ float2 sMdyn[];
 
     const int gsub = blockIdx.x * kBwdWarps + (int)(threadIdx.x >> 5);
     const int tile = gsub >> 3;
     const int wl_ = threadIdx.x >> 5;
     const int sub = gsub & 7;  // sub-tile 0..7 of the tile
-    float2 (*M)[33] = reinterpret_cast<float2 (*)[33]>(sMdyn + (size_t)wl_ * 32 * 33);
+    float2 (*M)[32] = reinterpret_cast<float2 (*)[32]>(sMdyn + (size_t)wl_ * 32 * 32);
     const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
     const unsigned lane = lane_id();
     const int sx = tx * kTile + (sub & 1) * 8, sy = ty * kTile + (sub >> 1) * 4;
@@ -210,10 +213,11 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             const float4 B = cur.co;
             const float z = cur.pr.z;
             float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, sw2 = 0.f, swx = 0.f, swy = 0.f, dzd = 0.f;
-            unsigned mm = mj;
+            unsigned mm = __funnelshift_r(mj, mj, lane);  // rotate right by lane
             while (mm) {
-                const int i = __ffs(mm) - 1;
+                const int r = __ffs(mm) - 1;
                 mm &= mm - 1u;
+                const int i = (r + (int)lane) & 31;
                 const float2 md = M[lane][i];
                 if (md.x == 0.f) continue;  // not composited (ω > 0 for every composited pair)
                 const float4 gp = sG[wl_][i];
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(kFinThreads) k_pose_finalize(const double *__r
     }
 }
 
-constexpr size_t kBwdDynSmem = sizeof(float2) * kBwdWarps * 32 * 33;
+constexpr size_t kBwdDynSmem = sizeof(float2) * kBwdWarps * 32 * 32;
 
 template <bool A, bool P, bool L>
 static void launch_bwd_t(const BwdArgs &a, int T, cudaStream_t s) {
