@@ -48,7 +48,7 @@ __device__ __forceinline__ float sgnf(float r) { return (float)((r > 0.0f) - (r 
 
 // Per batch of 32 sub-list entries the backward runs in two phases (composite_common.cuh):
 //   phase 1 — lane i = pixel walks ITS candidate entries back to front, recovering T_i and the
-//             behind-accumulators, and writes (ω = α_i T_i, dL/dα_i·[α unclamped]) into the
+//             behind-accumulator, and writes (ω = α_i T_i, dL/dα_i·w_i·[α unclamped]) into the
 //             warp's 32×32 matrix M[entry][pixel] (0 for pairs that were not composited);
 //   phase 2 — lane j = entry walks the pixels its footprint covers and sums that entry's
 //             colour / opacity / σ / (u, v, z) gradient from M and the per-pixel upstream — a
@@ -143,10 +143,14 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
     const unsigned onmask = __ballot_sync(kFullMask, on);
     const int wmax = (int)__reduce_max_sync(kFullMask, L);  // sub-list positions < wmax matter
 
-    // behind-accumulators relative to the references: Xb = Σ_{j behind} w_j (x_j − x_ref) with
-    // w_j = α_j T_j / T_{i+1}, and Tb = 1 − Σ w_j = Π (1 − α_j) (so x_i − x̄ = (x_i − x_ref) − Xb +
-    // x_ref·Tb and 1 − S̄ = Tb, all without cancellation against x_ref)
-    float Cb0 = 0.f, Cb1 = 0.f, Cb2 = 0.f, Db = 0.f, Tb = 1.0f;
+    // Behind-accumulator, relative to the pixel's references and already dotted with the
+    // (constant) upstream gradient: Fb = Σ_{j behind} w_j f_j with f_j = g_C·(c_j − c_ref) +
+    // g_D (z_j − z_ref), w_j = α_j T_j / T_{i+1}; Tb = 1 − Σ w_j = Π (1 − α_j).  Then
+    //   g·(x_i − x̄) + g_S (1 − S̄) = f_i − Fb + Kr·Tb,   Kr = g_C·c_ref + g_D z_ref + g_S,
+    // one scalar recursion instead of one per channel, and no difference of nearly equal
+    // colours / depths is ever formed in fp32 (R23).
+    float Fb = 0.f, Tb = 1.0f;
+    const float Kr = g0 * r0 + g1 * r1 + g2 * r2 + gD * rz + gS;
     float h0 = 0.f, h1 = 0.f, h2 = 0.f;
     float K00 = 0.f, K01 = 0.f, K02 = 0.f, K10 = 0.f, K11 = 0.f, K12 = 0.f, K20 = 0.f, K21 = 0.f, K22 = 0.f;
     const float fmean = 0.5f * (p.in.fx + p.in.fy);
@@ -185,21 +189,18 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
                 const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
                 if (d2 <= A.z) {
                     const float4 B = sB[wl_][k];
-                    const float raw = __fmul_rn(B.w, fast_exp2(d2 * A.w));
+                    const float wgt = fast_exp2(d2 * A.w);
+                    const float raw = __fmul_rn(B.w, wgt);
                     const bool aclamp = raw > kAlphaMax;
                     const float a = aclamp ? kAlphaMax : raw;
                     if (a >= 1.0f / 255.0f) {
                         const float oma = 1.0f - a;
                         const float Ti = __fdividef(T, oma);
                         om = a * Ti;
-                        const float e0 = B.x - r0, e1 = B.y - r1, e2 = B.z - r2, ez = sZ[wl_][k] - rz;
-                        const float fpart = g0 * (e0 - Cb0 + r0 * Tb) + g1 * (e1 - Cb1 + r1 * Tb) +
-                                            g2 * (e2 - Cb2 + r2 * Tb) + gD * (ez - Db + rz * Tb) + gS * Tb;
-                        dAe = aclamp ? 0.f : Ti * fpart;
-                        Cb0 = a * e0 + oma * Cb0;
-                        Cb1 = a * e1 + oma * Cb1;
-                        Cb2 = a * e2 + oma * Cb2;
-                        Db = a * ez + oma * Db;
+                        const float fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (sZ[wl_][k] - rz);
+                        // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
+                        dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
+                        Fb = a * fi + oma * Fb;
                         Tb = oma * Tb;
                         T = Ti;
                     }
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
                 if (md.y != 0.f) {
                     const float dx = (float)(sx + (i & 7)) - Aj.x, dy = (float)(sy + (i >> 3)) - Aj.y;
                     const float d2 = dx * dx + dy * dy;
-                    const float dw = md.y * fast_exp2(d2 * Aj.w);  // dL/dα · w  (= ∂L/∂o contribution)
+                    const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution)
                     dop += dw;
                     sw2 = fmaf(dw, d2, sw2);
                     swx = fmaf(dw, dx, swx);
