@@ -182,6 +182,15 @@ def run_reference(args):
     return 0
 
 
+def measured_traffic(workload, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            return json.load(f)[workload][kernel]["bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def workload_config(cfg, args, n_views=1, views_per_rank=1):
     return {"workload": f"config{args.config}_{cfg.name}_{cfg.intr.width}x{cfg.intr.height}_K{cfg.K}",
             "n_gaussians": cfg.n_slots, "image": [cfg.intr.width, cfg.intr.height], "views_per_step": n_views,
@@ -428,7 +437,7 @@ def main():
     d = stage_json[dom]
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"],
                 "peak": hbm_peak if d["bound"] == "hbm" else fp32_peak, "unit": d["unit"], "frac": d["frac"],
-                "traffic": None,
+                "traffic": measured_traffic(workload_config(cfg, args)["workload"], dom),
                 "peak_source": (f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
                                 f"FP32 {SM_COUNT} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz "
                                 f"(B200_PROFILING.md unit counts, max clock)")}
