@@ -50,7 +50,7 @@ cudaError_t dalloc(T **p, size_t n) {
 }
 
 void free_all(Ctx &c) {
-    void *ptrs[] = {c.proj, c.rect, c.tile_count, c.tile_start, c.tile_cursor, c.keys, c.vals, c.keys2,
+    void *ptrs[] = {c.proj, c.rect, c.tile_count, c.tile_start, c.tile_cursor, c.tile_flag, c.keys, c.vals, c.pbits, c.keys2,
                     c.vals2, c.offs, c.sub_lists, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -111,8 +111,11 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = dalloc(&c.tile_count, (size_t)c.max_tiles);
     if (!e) e = dalloc(&c.tile_start, (size_t)c.max_tiles + 1);
     if (!e) e = dalloc(&c.tile_cursor, (size_t)c.max_tiles);
+    if (!e) e = dalloc(&c.tile_flag, (size_t)c.max_tiles);
+    if (!e) e = cudaMemset(c.tile_flag, 0, sizeof(uint32_t) * c.max_tiles);
     if (!e) e = dalloc(&c.keys, (size_t)max_pairs);
     if (!e) e = dalloc(&c.vals, (size_t)max_pairs);
+    if (!e) e = dalloc(&c.pbits, (size_t)max_pairs);
     if (!e) e = dalloc(&c.keys2, (size_t)max_pairs);
     if (!e) e = dalloc(&c.vals2, (size_t)max_pairs);
     if (!e) e = dalloc(&c.offs, (size_t)max_pairs);

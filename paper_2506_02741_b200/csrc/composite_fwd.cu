@@ -2,6 +2,8 @@
 // (Eq. 1 `splat`), α floor 1/255 from north_star (4).
 // Decision arithmetic exactly as DESIGN.md §3 step 7.  Work decomposition: composite_common.cuh
 // (one warp per 8×4 sub-tile, lane = pixel, per-lane candidate lists by bit transpose).
+#include <stdlib.h>
+
 #include "composite_common.cuh"
 
 namespace vtgs {
@@ -115,13 +117,185 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 16) k_composite_fwd(FwdArgs p)
     }
 }
 
+// Ring walk.  The warp builds 32-entry batches of its sub-list into a ring of R slots (entry
+// data A = (u, v, 9σ², o), B = (c_r, c_g, c_b, z), and per lane the bit column of the entries
+// whose footprint can touch its pixel).  Each lane then walks ITS candidates front to back at
+// its own pace: a lane only waits when it reaches the batch not yet built and the ring is full
+// (R batches ahead of the slowest live lane).  Compared with walking batch by batch in lock
+// step (the warp runs max-over-lanes candidates per batch), the warp runs ≈ max-over-lanes of
+// the whole-list candidate count — tools/sim_batches.py: lane efficiency 0.27 → 0.87 at R = 16.
+constexpr int kInner = 4;                      // lane-independent steps between warp checks
+constexpr float kExpScale9 = -4.5f * kLog2e;  // −log2(e)/(2σ²) = kExpScale9 / (9σ²)
+
+template <int R>
+struct FwdRing {
+    float4 A[R * 32];
+    float4 B[R * 32];
+    uint32_t bits[R * 32];
+};
+
+template <int R>
+__global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p) {
+    extern __shared__ float4 fwd_smem[];
+    static_assert((R & (R - 1)) == 0, "ring depth must be a power of two");
+    const int wl = threadIdx.x >> 5;
+    FwdRing<R> &ring = reinterpret_cast<FwdRing<R> *>(fwd_smem)[wl];
+    const int gsub = blockIdx.x * kFwdWarps + wl;
+    const int tile = gsub >> 3;
+    const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
+    const int w = gsub & 7;
+    const unsigned lane = lane_id();
+    const int sx = tx * kTile + (w & 1) * 8, sy = ty * kTile + (w >> 1) * 4;
+    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const bool inside = px < p.W && py < p.H;
+    const float pxf = (float)px, pyf = (float)py;
+    const int n = (int)p.tile_count[tile];
+    const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)w * n;
+    const int cnt = (int)p.sub_count[tile * 8 + w];
+    const int nb = (cnt + 31) >> 5;
+    const unsigned inmask = __ballot_sync(kFullMask, inside);
+
+    EntryRegs nxt;
+    fetch_entry(nxt, list, (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    int built = 0;
+    // build batch `built` from the prefetched registers, prefetch the one after it
+    auto build = [&]() {
+        const int slot = (built & (R - 1)) * 32;
+        const int idx = built * 32 + (int)lane;
+        unsigned mj = 0u;
+        if (idx < cnt) {
+            const float s = fabsf(nxt.pr.w);
+            const float s9 = __fmul_rn(9.0f, __fmul_rn(s, s));
+            const float4 A = make_float4(nxt.pr.x, nxt.pr.y, s9, nxt.co.w);
+            ring.A[slot + lane] = A;
+            ring.B[slot + lane] = make_float4(nxt.co.x, nxt.co.y, nxt.co.z, nxt.pr.z);
+            mj = lane_mask(A, nxt.r, sx, sy) & inmask;
+        }
+        ring.bits[slot + lane] = __brev(transpose32(mj, lane));  // bit 31 − j = entry j
+        ++built;
+        fetch_entry(nxt, list, built * 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    };
+    while (built < nb && built < R) build();
+    __syncwarp();
+
+    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f, Sl = 0.f;
+    uint32_t lastc = 0, ne = 0, nc = 0;
+    // lane state: batch b, its remaining candidate bits cur.  Finished (terminated, walked the
+    // whole list, or outside the image) ⇔ cur == 0 && b + 1 ≥ nb.
+    int b = inside ? -1 : nb;
+    unsigned cur = 0u;
+    for (;;) {
+        // a few lane-independent steps between warp-level checks (a blocked lane idles ≤ kInner);
+        // branch-free body: every lane runs the same predicated instructions
+#pragma unroll
+        for (int it = 0; it < kInner; ++it) {
+            if (cur == 0u && b + 1 < built) {
+                ++b;
+                cur = ring.bits[(b & (R - 1)) * 32 + lane];
+            }
+            const bool has = cur != 0u;
+            const int k = __clz(cur);                      // lowest remaining entry (bit-reversed)
+            cur &= ~(0x80000000u >> (k & 31));
+            const int e = ((b & (R - 1)) << 5) | (k & 31);
+            float4 A = make_float4(0.f, 0.f, -1.f, 0.f), Bc = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (has) {
+                A = ring.A[e];
+                Bc = ring.B[e];
+            }
+            const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
+            const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+            const bool elig = d2 <= A.z;                   // false when !has (A.z = −1)
+            const float a = fminf(__fmul_rn(A.w, fast_exp2(d2 * (kExpScale9 * rcp_approx(A.z)))), kAlphaMax);
+            const bool comp = elig && a >= 1.0f / 255.0f;
+            const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
+            const bool term = comp && Tn < kTMin;
+            const bool acc = comp && !term;
+            const float om = acc ? a * T : 0.0f;
+            C0 = fmaf(Bc.x, om, C0);
+            C1 = fmaf(Bc.y, om, C1);
+            C2 = fmaf(Bc.z, om, C2);
+            D = fmaf(Bc.w, om, D);
+            Sl += om;
+            T = acc ? Tn : T;
+            lastc = acc ? (uint32_t)(b * 32 + k + 1) : lastc;
+            ne += elig ? 1u : 0u;
+            nc += acc ? 1u : 0u;
+            if (term) {
+                cur = 0u;
+                b = nb;
+            }
+        }
+        // lanes whose next word was empty: catch up before the warp-level check
+        while (cur == 0u && b + 1 < built) {
+            ++b;
+            cur = ring.bits[(b & (R - 1)) * 32 + lane];
+        }
+        const bool live = cur != 0u || b + 1 < nb;
+        if (!__any_sync(kFullMask, live)) break;
+        const bool blocked = cur == 0u && b + 1 < nb && b + 1 >= built;
+        if (__any_sync(kFullMask, blocked)) {
+            const int need = !live ? 0x7fffffff : (cur ? b : b + 1);  // earliest batch still needed
+            const int lo = __reduce_min_sync(kFullMask, need);
+            if (built < nb && built < lo + R) {
+                while (built < nb && built < lo + R) build();
+                __syncwarp();
+            }
+        }
+    }
+    if (inside) {
+        const int pix = py * p.W + px;
+        p.color[3 * pix + 0] = C0;
+        p.color[3 * pix + 1] = C1;
+        p.color[3 * pix + 2] = C2;
+        p.depth[pix] = D;
+        p.sil[pix] = Sl;
+        p.T_final[pix] = T;
+        p.last[pix] = lastc;
+    }
+    unsigned long long a = ne, bsum = nc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(kFullMask, a, o);
+        bsum += __shfl_xor_sync(kFullMask, bsum, o);
+    }
+    if (lane == 0 && (a | bsum)) {
+        atomicAdd(&p.dev->e_eval, a);
+        atomicAdd(&p.dev->e_comp, bsum);
+    }
+}
+
+static int fwd_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("VTGS_FWD");
+        v = e ? atoi(e) : 4;    // 0: batch lock-step walk; 4 / 8 / 16: ring depth
+    }
+    return v;
+}
+
+template <int R>
+static cudaError_t launch_ring(const FwdArgs &a, int T, cudaStream_t s) {
+    const size_t sm = sizeof(FwdRing<R>) * kFwdWarps;
+    cudaError_t e = cudaFuncSetAttribute(k_composite_fwd_ring<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e) return e;
+    k_composite_fwd_ring<R><<<T * 8 / kFwdWarps, kFwdWarps * 32, sm, s>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
     const int W = c.intr.width, H = c.intr.height;
     const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile;
     FwdArgs a{c.proj, c.rect, c.col_opa, c.tile_count, c.tile_start, c.sub_lists, c.sub_count, W, H, ntx,
               c.color, c.depth, c.sil, c.T_final, c.last, c.dev};
-    k_composite_fwd<<<ntx * nty * 8 / kFwdWarps, kFwdWarps * 32, 0, s>>>(a);
-    return cudaGetLastError();
+    switch (fwd_variant()) {
+        case 0:
+            k_composite_fwd<<<ntx * nty * 8 / kFwdWarps, kFwdWarps * 32, 0, s>>>(a);
+            return cudaGetLastError();
+        case 4: return launch_ring<4>(a, ntx * nty, s);
+        case 8: return launch_ring<8>(a, ntx * nty, s);
+        case 32: return launch_ring<32>(a, ntx * nty, s);
+        default: return launch_ring<16>(a, ntx * nty, s);
+    }
 }
 
 }  // namespace vtgs

@@ -9,6 +9,8 @@
 // per warp), then each tile's bucket is sorted in shared memory by (z bits, gid) — one
 // bucket-scatter pass plus an on-chip sort instead of a multi-pass global 64-bit radix sort
 // (K4/K5).
+#include <stdlib.h>
+
 #include "composite_common.cuh"
 
 namespace vtgs {
@@ -166,6 +168,7 @@ __global__ void __launch_bounds__(256) k_emit_pairs(const float4 *__restrict__ p
                                                     uint32_t *__restrict__ cursor,
                                                     uint32_t *__restrict__ keys,
                                                     uint32_t *__restrict__ vals,
+                                                    uint8_t *__restrict__ pbits,
                                                     const DevScalars *__restrict__ dev) {
     if (dev->overflow) return;
     const int64_t Nr = (N + 31) & ~(int64_t)31;
@@ -174,8 +177,9 @@ __global__ void __launch_bounds__(256) k_emit_pairs(const float4 *__restrict__ p
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < Nr; g += stride) {
         int cnt = 0, ntg = 1, tx0 = 0, ty0 = 0;
         uint32_t zb = 0;
+        uint2 r = make_uint2(0u, 0u);
         if (g < N) {
-            const uint2 r = rect[g];
+            r = rect[g];
             if (r.x != 0xffffffffu) {
                 const int x0 = r.x & 0xffff, x1 = r.x >> 16, y0 = r.y & 0xffff, y1 = r.y >> 16;
                 tx0 = x0 >> 4;
@@ -198,8 +202,10 @@ __global__ void __launch_bounds__(256) k_emit_pairs(const float4 *__restrict__ p
             base = __shfl_sync(kFull, base, leader);
             if (tile >= 0) {
                 const uint32_t slot = base + __popc(peers & lanemask_lt());
+                const int tyy = tile / ntx;
                 keys[slot] = zb;
                 vals[slot] = (uint32_t)g;
+                pbits[slot] = (uint8_t)subtile_bits(r, (tile - tyy * ntx) * kTile, tyy * kTile);
             }
         }
     }
@@ -315,8 +321,9 @@ __device__ __forceinline__ void build_sublists(const uint32_t *V, int n, const u
                                                int ty0, uint32_t *__restrict__ out,
                                                uint32_t *__restrict__ sub_count, uint32_t *sh, uint8_t *bits8) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    uint32_t *wcnt = sh;        // [8 warps][8 sub-tiles]
-    uint32_t *run = sh + 64;    // [8] running totals
+    uint32_t *wcnt = sh;        // [8 warps][8 sub-tiles] counts of this round
+    uint32_t *woff = sh + 64;   // [8 warps][8 sub-tiles] output offsets of this round
+    uint32_t *run = sh + 128;   // [8] running totals
     if (tid < 8) run[tid] = 0;
     // all rect gathers of the tile in flight together, then the ordered compaction rounds
 #pragma unroll 4
@@ -328,25 +335,25 @@ __device__ __forceinline__ void build_sublists(const uint32_t *V, int n, const u
         const uint32_t g = i < n ? V[i] : 0u;
         unsigned b[8];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-            b[s] = __ballot_sync(kFull, (bits >> s) & 1u);
-            if (lane == 0) wcnt[w * 8 + s] = __popc(b[s]);
-        }
-        __syncthreads();
+        for (int s = 0; s < 8; ++s) b[s] = __ballot_sync(kFull, (bits >> s) & 1u);
+        if (lane < 8) {
+            unsigned c = 0;
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-            if ((bits >> s) & 1u) {
-                uint32_t pos = run[s] + __popc(b[s] & lanemask_lt());
-                for (int ww = 0; ww < w; ++ww) pos += wcnt[ww * 8 + s];
-                out[(size_t)s * n + pos] = g;
-            }
+            for (int s = 0; s < 8; ++s) c = lane == s ? __popc(b[s]) : c;
+            wcnt[w * 8 + lane] = c;
         }
         __syncthreads();
-        if (tid < 8) {
-            uint32_t t = 0;
-            for (int ww = 0; ww < 8; ++ww) t += wcnt[ww * 8 + tid];
-            run[tid] += t;
+        if (tid < 64) {   // (warp ww, sub-tile ss): offset = run + counts of the warps before
+            const int ww = tid >> 3, ss = tid & 7;
+            uint32_t o = run[ss];
+            for (int x = 0; x < ww; ++x) o += wcnt[x * 8 + ss];
+            woff[tid] = o;
         }
+        __syncthreads();
+        if (tid < 8) run[tid] = woff[56 + tid] + wcnt[56 + tid];
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            if ((bits >> s) & 1u) out[(size_t)s * n + woff[w * 8 + s] + __popc(b[s] & lanemask_lt())] = g;
         __syncthreads();
     }
     if (tid < 8) sub_count[tid] = run[tid];
@@ -361,13 +368,15 @@ __global__ void __launch_bounds__(kBlock) k_tile_sort(const uint32_t *__restrict
                                                       uint32_t *vals2, uint32_t *offs,
                                                       const uint2 *__restrict__ rect, int ntx,
                                                       uint32_t *__restrict__ sub_lists,
-                                                      uint32_t *__restrict__ sub_count) {
+                                                      uint32_t *__restrict__ sub_count,
+                                                      const uint32_t *__restrict__ tile_flag) {
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t hist[8 * 256];
     __shared__ uint32_t red[32];
     const int tile = blockIdx.x;
     const int n = (int)tile_count[tile];
-    if (n <= LO || (!GLOBAL && n > CAP)) return;
+    // tiles longer than LO, or flagged by the bucket sort (degenerate depth distribution)
+    if ((n <= LO && !(tile_flag && tile_flag[tile])) || (!GLOBAL && n > CAP)) return;
     const uint32_t base = tile_start[tile];
     const int ty = tile / ntx, tx = tile - ty * ntx;
     uint32_t *out = sub_lists + (size_t)8 * base;
@@ -393,9 +402,228 @@ __global__ void __launch_bounds__(kBlock) k_tile_sort(const uint32_t *__restrict
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// K5 (main path): per-tile bucket + rank sort by (z bits, gid), lists ≤ CAP on chip.
+//   1. keys / gids → shared memory, block min / max of the z bits;
+//   2. bucket = (key − kmin) ≫ shift with shift chosen so the key range spans ≤ 4096 buckets
+//      (z bits of positive floats are monotone as unsigned integers), counted with shared-memory
+//      integer atomics, exclusive scan → contiguous bucket segments;
+//   3. scatter into the segments (arbitrary order inside a segment);
+//   4. every element's final position = segment start + its rank among the segment's elements
+//      by (key, gid) — a direct O(c) count per element, no further passes.
+// One global read of the pairs, one write of the sorted gids.  A tile whose largest bucket
+// exceeds kMaxBucket (many equal or nearly equal depths) falls back to the radix sort above.
+// ------------------------------------------------------------------------------------------
+constexpr int kMaxBucket = 256;
+
+// Sub-lists from the sorted gids V and their sub-tile bits B: thread-local runs of E entries,
+// one block scan of the 8 per-sub-tile counts packed 4 × 16 bits into two 64-bit words.
+template <int NT>
+__device__ __forceinline__ void sublists_from_bits(const uint32_t *V, const uint8_t *B, int n,
+                                                   uint32_t *__restrict__ out, uint32_t *__restrict__ sub_count,
+                                                   unsigned long long (*red64)[33]) {
+    constexpr int NW = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int E = (n + NT - 1) / NT;
+    const int i0 = min(tid * E, n), i1 = min(i0 + E, n);
+    unsigned long long c0 = 0, c1 = 0;  // counts of sub-tiles 0-3 / 4-7, 16 bits each
+    for (int i = i0; i < i1; ++i) {
+        const uint32_t b = B[i];
+        c0 += (unsigned long long)(b & 1u) | ((unsigned long long)((b >> 1) & 1u) << 16) |
+              ((unsigned long long)((b >> 2) & 1u) << 32) | ((unsigned long long)((b >> 3) & 1u) << 48);
+        c1 += (unsigned long long)((b >> 4) & 1u) | ((unsigned long long)((b >> 5) & 1u) << 16) |
+              ((unsigned long long)((b >> 6) & 1u) << 32) | ((unsigned long long)((b >> 7) & 1u) << 48);
+    }
+    unsigned long long s0 = c0, s1 = c1;  // inclusive warp scan (no carries: every total ≤ n < 2^16)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y0 = __shfl_up_sync(kFull, s0, o), y1 = __shfl_up_sync(kFull, s1, o);
+        if (lane >= o) { s0 += y0; s1 += y1; }
+    }
+    if (lane == 31) { red64[0][w] = s0; red64[1][w] = s1; }
+    __syncthreads();
+    if (w == 0) {   // exclusive scan of the warps' totals (entry NW = the block total)
+        unsigned long long a0 = lane < NW ? red64[0][lane] : 0ull, a1 = lane < NW ? red64[1][lane] : 0ull;
+        unsigned long long i0s = a0, i1s = a1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y0 = __shfl_up_sync(kFull, i0s, o), y1 = __shfl_up_sync(kFull, i1s, o);
+            if (lane >= o) { i0s += y0; i1s += y1; }
+        }
+        __syncwarp();
+        red64[0][lane] = i0s - a0;
+        red64[1][lane] = i1s - a1;
+        if (lane == 31) { red64[0][NW] = i0s; red64[1][NW] = i1s; }   // NW < 32 (i0s at lane 31 = total)
+    }
+    __syncthreads();
+    const unsigned long long p0 = s0 - c0 + red64[0][w], p1 = s1 - c1 + red64[1][w];
+    const unsigned long long t0 = red64[0][NW], t1 = red64[1][NW];
+    if (tid < 8) sub_count[tid] = (uint32_t)(((tid < 4 ? t0 : t1) >> (16 * (tid & 3))) & 0xffffu);
+    uint32_t off[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        off[q] = (uint32_t)((p0 >> (16 * q)) & 0xffffu);
+        off[4 + q] = (uint32_t)((p1 >> (16 * q)) & 0xffffu);
+    }
+    for (int i = i0; i < i1; ++i) {
+        const uint32_t b = B[i], g = V[i];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if ((b >> q) & 1u) out[(size_t)q * n + off[q]++] = g;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K5 (main path): per-tile bucket + rank sort by (z bits, gid) of lists of ≤ CAP entries on
+// chip with NT threads, carrying each pair's sub-tile bits (written by k_emit_pairs).
+//   1. keys / gids / bits → shared memory, block min / max of the z bits;
+//   2. bucket = (key − kmin) ≫ shift with shift chosen so the key range spans ≤ NB buckets
+//      (z bits of positive floats are monotone as unsigned integers), counted with shared-memory
+//      integer atomics, exclusive scan → contiguous bucket segments;
+//   3. scatter into the segments (arbitrary order inside a segment);
+//   4. every element's final position = segment start + its rank among its segment by
+//      (key, gid) — a direct O(bucket size) count per element;
+//   5. the sorted gids and the 8 sub-lists are written.
+// A tile whose largest bucket exceeds kMaxBucket (many equal or nearly equal depths) is flagged
+// and left to the radix sort kernel.  Lists in (LO, CAP] are handled; others return at once.
+// ------------------------------------------------------------------------------------------
+template <int LO, int CAP, int NB, int NT>
+__global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restrict__ tile_count,
+                                                         const uint32_t *__restrict__ tile_start,
+                                                         const uint32_t *__restrict__ keys,
+                                                         uint32_t *__restrict__ vals,
+                                                         const uint8_t *__restrict__ pbits,
+                                                         uint32_t *__restrict__ sub_lists,
+                                                         uint32_t *__restrict__ sub_count,
+                                                         uint32_t *__restrict__ tile_flag) {
+    constexpr int NW = NT / 32;
+    constexpr int PT = NB / NT;
+    static_assert(PT >= 1 && PT * NT == NB, "NB must be a multiple of NT");
+    extern __shared__ uint32_t sm[];
+    __shared__ uint32_t red[4][32];
+    __shared__ unsigned long long red64[2][33];
+    const int tile = blockIdx.x;
+    const int n = (int)tile_count[tile];
+    if (n <= LO || n > CAP) return;
+    constexpr int kLogNB = NB == 4096 ? 12 : (NB == 2048 ? 11 : 10);
+    static_assert((1 << kLogNB) == NB, "NB must be 1024, 2048 or 4096");
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t base = tile_start[tile];
+    uint32_t *K = sm, *V = sm + CAP, *K2 = sm + 2 * CAP, *V2 = sm + 3 * CAP, *H = sm + 4 * CAP;
+    uint8_t *B = reinterpret_cast<uint8_t *>(sm + 4 * CAP + NB), *B2 = B + CAP;
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (int i = tid; i < n; i += NT) {
+        const uint32_t k = __ldg(keys + base + i);
+        K[i] = k;
+        V[i] = __ldg(vals + base + i);
+        B[i] = __ldg(pbits + base + i);
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
+    }
+    for (int i = tid; i < NB; i += NT) H[i] = 0u;
+    kmin = __reduce_min_sync(kFull, kmin);
+    kmax = __reduce_max_sync(kFull, kmax);
+    if (lane == 0) { red[0][w] = kmin; red[1][w] = kmax; }
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t a = __reduce_min_sync(kFull, lane < NW ? red[0][lane] : 0xffffffffu);
+        const uint32_t b = __reduce_max_sync(kFull, lane < NW ? red[1][lane] : 0u);
+        __syncwarp();
+        if (lane == 0) { red[0][0] = a; red[1][0] = b; }
+    }
+    __syncthreads();
+    kmin = red[0][0];
+    kmax = red[1][0];
+    const uint32_t range = kmax - kmin;
+    const int nbits = range ? 32 - __clz(range) : 0;
+    const int shift = nbits > kLogNB ? nbits - kLogNB : 0;
+    for (int i = tid; i < n; i += NT) atomicAdd(&H[(K[i] - kmin) >> shift], 1u);
+    __syncthreads();
+    uint32_t cmax = 0;
+    {   // exclusive scan of the NB counts: PT per thread, then a block scan of the sums
+        uint32_t c[PT], tot = 0;
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+            c[j] = H[tid * PT + j];
+            tot += c[j];
+            cmax = max(cmax, c[j]);
+        }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        cmax = __reduce_max_sync(kFull, cmax);
+        if (lane == 31) red[2][w] = incl;
+        if (lane == 0) red[3][w] = cmax;
+        __syncthreads();
+        if (w == 0) {   // exclusive scan of the warps' sums, max of their largest buckets
+            const uint32_t a = lane < NW ? red[2][lane] : 0u;
+            uint32_t ia = a;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, ia, o);
+                if (lane >= o) ia += y;
+            }
+            const uint32_t m = __reduce_max_sync(kFull, lane < NW ? red[3][lane] : 0u);
+            __syncwarp();
+            red[2][lane] = ia - a;
+            red[3][lane] = m;
+        }
+        __syncthreads();
+        uint32_t run = incl - tot + red[2][w];
+        cmax = red[3][0];
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+            H[tid * PT + j] = run;
+            run += c[j];
+        }
+    }
+    if (cmax > (uint32_t)kMaxBucket) {   // degenerate depth distribution → the radix kernel
+        if (tid == 0) tile_flag[tile] = 1u;
+        return;
+    }
+    if (tid == 0) tile_flag[tile] = 0u;
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) {
+        const uint32_t k = K[i];
+        const uint32_t pos = atomicAdd(&H[(k - kmin) >> shift], 1u);  // H[b] becomes the segment end
+        K2[pos] = k;
+        V2[pos] = V[i];
+        B2[pos] = B[i];
+    }
+    __syncthreads();
+    for (int p = tid; p < n; p += NT) {
+        const uint32_t k = K2[p], v = V2[p];
+        const uint32_t b = (k - kmin) >> shift;
+        const int s0 = b ? (int)H[b - 1] : 0, s1 = (int)H[b];
+        int rank = 0;
+        for (int j = s0; j < s1; ++j) {
+            const uint32_t kj = K2[j];
+            rank += (kj < k || (kj == k && V2[j] < v)) ? 1 : 0;
+        }
+        V[s0 + rank] = v;
+        B[s0 + rank] = B2[p];
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) vals[base + i] = V[i];
+    sublists_from_bits<NT>(V, B, n, sub_lists + (size_t)8 * base, sub_count + 8 * tile, red64);
+}
+
 constexpr int kSortCapBig = 8192;
 constexpr size_t kSortSmem = 4 * kSortCap * sizeof(uint32_t) + kSortCap * sizeof(uint16_t);
 constexpr size_t kSortSmemBig = 4 * kSortCapBig * sizeof(uint32_t) + kSortCapBig * sizeof(uint16_t);
+constexpr size_t bucket_smem(int cap, int nb) { return (4 * (size_t)cap + nb) * sizeof(uint32_t) + 2 * (size_t)cap; }
+
+static int sort_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("VTGS_SORT");
+        v = e ? atoi(e) : 1;   // 1: bucket + rank sort; 0: radix sort
+    }
+    return v;
+}
 
 cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     const int W = c.intr.width, H = c.intr.height;
@@ -419,18 +647,32 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     if ((err = cudaGetLastError())) return err;
     if (N > 0) {
         LaunchScope ls(&c, kEmit, s);
-        k_emit_pairs<<<gN, 256, 0, s>>>(c.proj, c.rect, N, ntx, c.tile_cursor, c.keys, c.vals, c.dev);
+        k_emit_pairs<<<gN, 256, 0, s>>>(c.proj, c.rect, N, ntx, c.tile_cursor, c.keys, c.vals, c.pbits, c.dev);
         if ((err = cudaGetLastError())) return err;
     }
     {
         LaunchScope ls(&c, kSort, s);
-        // lists ≤ 4096 on chip with 3 CTAs / SM; (4096, 8192] on chip with 1 CTA / SM; longer on
-        // global scratch (the second launch exits at once for every tile it does not own)
-        k_tile_sort<-1, kSortCap, false><<<T, kBlock, kSortSmem, s>>>(
-            c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists, c.sub_count);
-        k_tile_sort<kSortCap, kSortCapBig, true><<<T, kBlock, kSortSmemBig, s>>>(
-            c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists, c.sub_count);
-        ++c.launches;  // two kernels inside this scope
+        // every launch exits at once for the tiles it does not own
+        if (sort_variant()) {
+            // lists ≤ 2048: 512 threads, 4 CTAs / SM; (2048, 4096]: 1024 threads, 2 CTAs / SM;
+            // longer lists and flagged tiles: the radix kernel on global scratch / 8192 on chip
+            k_tile_sort_bucket<-1, 2048, 4096, 512><<<T, 512, bucket_smem(2048, 4096), s>>>(
+                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag);
+            k_tile_sort_bucket<2048, kSortCap, 4096, 1024><<<T, 1024, bucket_smem(kSortCap, 4096), s>>>(
+                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag);
+            k_tile_sort<kSortCap, kSortCapBig, true><<<T, kBlock, kSortSmemBig, s>>>(
+                c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists,
+                c.sub_count, c.tile_flag);
+            c.launches += 2;
+        } else {
+            k_tile_sort<-1, kSortCap, false><<<T, kBlock, kSortSmem, s>>>(
+                c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists,
+                c.sub_count, nullptr);
+            k_tile_sort<kSortCap, kSortCapBig, true><<<T, kBlock, kSortSmemBig, s>>>(
+                c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists,
+                c.sub_count, nullptr);
+            ++c.launches;
+        }
     }
     if ((err = cudaGetLastError())) return err;
     LaunchScope ls(&c, kCompFwd, s);
@@ -440,6 +682,12 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
 cudaError_t forward_set_attributes() {
     cudaError_t e = cudaFuncSetAttribute(k_tile_sort<-1, kSortCap, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kSortSmem);
+    if (!e)
+        e = cudaFuncSetAttribute(k_tile_sort_bucket<-1, 2048, 4096, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)bucket_smem(2048, 4096));
+    if (!e)
+        e = cudaFuncSetAttribute(k_tile_sort_bucket<2048, kSortCap, 4096, 1024>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, 4096));
     if (!e)
         e = cudaFuncSetAttribute(k_tile_sort<kSortCap, kSortCapBig, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBig);

@@ -61,8 +61,10 @@ struct Ctx {
     uint32_t *tile_count = nullptr;  // [max_tiles]
     uint32_t *tile_start = nullptr;  // [max_tiles + 1]
     uint32_t *tile_cursor = nullptr; // [max_tiles]
+    uint32_t *tile_flag = nullptr;   // [max_tiles] bucket sort → radix sort hand-off
     uint32_t *keys = nullptr;        // bucket: z bits   [max_pairs]
     uint32_t *vals = nullptr;        // bucket: gid      [max_pairs] — sorted in place
+    uint8_t *pbits = nullptr;        // bucket: the 8×4 sub-tiles of its tile the pair's rect touches [max_pairs]
     uint32_t *keys2 = nullptr;       // fallback sort scratch [max_pairs]
     uint32_t *vals2 = nullptr;
     uint32_t *offs = nullptr;        // fallback sort ranks [max_pairs]
@@ -169,6 +171,12 @@ __device__ __forceinline__ void view_transform(const float *R, const float *t, f
 __device__ __forceinline__ float fast_exp2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 

@@ -95,6 +95,41 @@ def test_tile_lists_micro_scenes(vt):
         assert np.array_equal(start, ostart) and np.array_equal(gid.astype(np.int64), ogid)
 
 
+@pytest.mark.parametrize("case", ["equal_depth", "two_depths", "long_lists"])
+def test_tile_lists_sort_paths(vt, case):
+    """The per-tile sort's three paths, bit-exact against the oracle: equal or nearly equal
+    depths (a bucket larger than the bucket sort takes → radix hand-off, ties broken by gid),
+    and lists longer than the on-chip bucket sort (> 4096 entries per tile)."""
+    rng = np.random.Generator(np.random.PCG64([7, {"equal_depth": 0, "two_depths": 1, "long_lists": 2}[case]]))
+    W, H = 40, 36
+    intr = Intrinsics(30.0, 30.0, (W - 1) / 2, (H - 1) / 2, W, H)
+    n = 6000 if case != "long_lists" else 20000
+    if case == "equal_depth":
+        z = np.full(n, 2.0)
+    elif case == "two_depths":
+        z = np.where(rng.random(n) < 0.5, 2.0, np.nextafter(np.float32(2.0), np.float32(3.0)))
+    else:
+        z = rng.uniform(1.0, 4.0, size=n)
+    u = rng.uniform(0.0, W - 1.0, size=n)
+    v = rng.uniform(0.0, H - 1.0, size=n)
+    x = (u - intr.cx) * z / intr.fx
+    y = (v - intr.cy) * z / intr.fy
+    r = rng.uniform(0.8, 2.5, size=n) * z / intr.fx
+    pos_rad = np.stack([x, y, z, r], 1).astype(np.float32)
+    col_opa = np.concatenate([rng.random((n, 3)), rng.uniform(0.01, 0.2, (n, 1))], 1).astype(np.float32)
+    view = np.array([1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0])
+    R = vt.Renderer(0, n, W, H)
+    pr = torch.from_numpy(pos_rad).cuda()
+    co = torch.from_numpy(col_opa).cuda()
+    pv = vt.pose_tensor(view32(view), "cuda")
+    R.render_fwd(pr, co, pv, intr)
+    start, gid = R.export_tiles(intr)
+    ostart, ogid = oracle.tile_lists(pos_rad, view32(view), intr)
+    assert np.array_equal(start, ostart) and np.array_equal(gid.astype(np.int64), ogid)
+    if case == "long_lists":
+        assert np.diff(ostart).max() > 4096
+
+
 # ------------------------------------------------------------------------------ (a4)
 def _check_images(out, ref, flags, atol=1e-4, max_flagged=5e-3):
     color, depth, sil = (t.cpu().numpy().astype(np.float64) for t in out)
