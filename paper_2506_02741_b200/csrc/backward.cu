@@ -46,6 +46,63 @@ struct BwdArgs {
 
 __device__ __forceinline__ float sgnf(float r) { return (float)((r > 0.0f) - (r < 0.0f)); }
 
+// Per-pixel upstream gradient (explicit, or the fused masked-L1 prologue of Eq. 1 / Eq. 2),
+// the saved forward state, and the pixel's reference colour / depth (its normalised render):
+// the behind-accumulators are kept relative to it, so c − c̄ and z − z̄ — differences of nearly
+// equal values when view-tied layers sit on one surface — keep fp32 relative precision.
+struct PixelUp {
+    float g0, g1, g2, gD, gS, T, r0, r1, r2, rz;
+    uint32_t L;
+    double lossv;
+};
+
+template <bool LOSS>
+__device__ __forceinline__ PixelUp pixel_upstream(const BwdArgs &p, int px, int py, bool inside) {
+    PixelUp u{0.f, 0.f, 0.f, 0.f, 0.f, 1.0f, 0.f, 0.f, 0.f, 0.f, 0u, 0.0};
+    if (!inside) return u;
+    const int pix = py * p.W + px;
+    if (LOSS) {
+        const float tDv = p.tD[pix];
+        const float Sv = p.sil[pix];
+        const bool U = tDv > 0.0f;
+        const bool Wm = U && Sv > 0.99f && (p.vis ? p.vis[pix] != 0 : true);
+        const bool mc = p.cmode ? Wm : true;
+        const bool md = p.dmode ? Wm : U;
+        float sc = 1.0f, sd = 1.0f;
+        if (p.normalize) {
+            sc = p.dev->count_c ? 1.0f / (float)p.dev->count_c : 0.0f;
+            sd = p.dev->count_d ? 1.0f / (float)p.dev->count_d : 0.0f;
+        }
+        if (mc) {
+            const float e0 = p.color[3 * pix] - p.tC[3 * pix];
+            const float e1 = p.color[3 * pix + 1] - p.tC[3 * pix + 1];
+            const float e2 = p.color[3 * pix + 2] - p.tC[3 * pix + 2];
+            const float k = p.wc * sc;
+            u.g0 = k * sgnf(e0); u.g1 = k * sgnf(e1); u.g2 = k * sgnf(e2);
+            u.lossv += (double)k * ((double)fabsf(e0) + (double)fabsf(e1) + (double)fabsf(e2));
+        }
+        if (md) {
+            const float e = p.depth[pix] - tDv;
+            const float k = p.wd * sd;
+            u.gD = k * sgnf(e);
+            u.lossv += (double)k * (double)fabsf(e);
+        }
+    } else {
+        if (p.dC) { u.g0 = p.dC[3 * pix]; u.g1 = p.dC[3 * pix + 1]; u.g2 = p.dC[3 * pix + 2]; }
+        if (p.dD) u.gD = p.dD[pix];
+        if (p.dS) u.gS = p.dS[pix];
+    }
+    u.T = p.T_final[pix];
+    u.L = p.last[pix];
+    const float Sv = p.sil[pix];
+    if (Sv > 0.0f) {
+        const float inv = 1.0f / Sv;
+        u.r0 = p.color[3 * pix] * inv; u.r1 = p.color[3 * pix + 1] * inv; u.r2 = p.color[3 * pix + 2] * inv;
+        u.rz = p.depth[pix] * inv;
+    }
+    return u;
+}
+
 // Per batch of 32 sub-list entries the backward runs in two phases (composite_common.cuh):
 //   phase 1 — lane i = pixel walks ITS candidate entries back to front, recovering T_i and the
 //             behind-accumulator, and writes (ω = α_i T_i, dL/dα_i·w_i·[α unclamped]) into the
@@ -87,56 +144,11 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
     PoseR P;
     if (POSE) pose_rotation(*p.view, P);
 
-    // ---- per-pixel upstream gradient (explicit, or the fused masked-L1 prologue) ----
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f, gD = 0.f, gS = 0.f, T = 1.0f;
-    float r0 = 0.f, r1 = 0.f, r2 = 0.f, rz = 0.f;
-    uint32_t L = 0;
-    double lossv = 0.0;
-    if (inside) {
-        const int pix = py * p.W + px;
-        if (LOSS) {
-            const float tDv = p.tD[pix];
-            const float Sv = p.sil[pix];
-            const bool U = tDv > 0.0f;
-            const bool Wm = U && Sv > 0.99f && (p.vis ? p.vis[pix] != 0 : true);
-            const bool mc = p.cmode ? Wm : true;
-            const bool md = p.dmode ? Wm : U;
-            float sc = 1.0f, sd = 1.0f;
-            if (p.normalize) {
-                sc = p.dev->count_c ? 1.0f / (float)p.dev->count_c : 0.0f;
-                sd = p.dev->count_d ? 1.0f / (float)p.dev->count_d : 0.0f;
-            }
-            if (mc) {
-                const float e0 = p.color[3 * pix] - p.tC[3 * pix];
-                const float e1 = p.color[3 * pix + 1] - p.tC[3 * pix + 1];
-                const float e2 = p.color[3 * pix + 2] - p.tC[3 * pix + 2];
-                const float k = p.wc * sc;
-                g0 = k * sgnf(e0); g1 = k * sgnf(e1); g2 = k * sgnf(e2);
-                lossv += (double)k * ((double)fabsf(e0) + (double)fabsf(e1) + (double)fabsf(e2));
-            }
-            if (md) {
-                const float e = p.depth[pix] - tDv;
-                const float k = p.wd * sd;
-                gD = k * sgnf(e);
-                lossv += (double)k * (double)fabsf(e);
-            }
-        } else {
-            if (p.dC) { g0 = p.dC[3 * pix]; g1 = p.dC[3 * pix + 1]; g2 = p.dC[3 * pix + 2]; }
-            if (p.dD) gD = p.dD[pix];
-            if (p.dS) gS = p.dS[pix];
-        }
-        T = p.T_final[pix];
-        L = p.last[pix];
-        // reference colour / depth of the pixel (its normalised render): the behind-
-        // accumulators are kept relative to it, so c − c̄ and z − z̄ — differences of nearly
-        // equal values when view-tied layers sit on one surface — keep fp32 relative precision
-        const float Sv = p.sil[pix];
-        if (Sv > 0.0f) {
-            const float inv = 1.0f / Sv;
-            r0 = p.color[3 * pix] * inv; r1 = p.color[3 * pix + 1] * inv; r2 = p.color[3 * pix + 2] * inv;
-            rz = p.depth[pix] * inv;
-        }
-    }
+    const PixelUp up = pixel_upstream<LOSS>(p, px, py, inside);
+    float g0 = up.g0, g1 = up.g1, g2 = up.g2, gD = up.gD, gS = up.gS, T = up.T;
+    const float r0 = up.r0, r1 = up.r1, r2 = up.r2, rz = up.rz;
+    uint32_t L = up.L;
+    const double lossv = up.lossv;
     const bool on = inside && L > 0 && (g0 != 0.f || g1 != 0.f || g2 != 0.f || gD != 0.f || gS != 0.f);
     if (!on) L = 0;
     sG[wl_][lane] = make_float4(g0, g1, g2, gD);
@@ -195,7 +207,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
                     const float a = aclamp ? kAlphaMax : raw;
                     if (a >= 1.0f / 255.0f) {
                         const float oma = 1.0f - a;
-                        const float Ti = __fdividef(T, oma);
+                        const float Ti = T * rcp_approx(oma);
                         om = a * Ti;
                         const float fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (sZ[wl_][k] - rz);
                         // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
