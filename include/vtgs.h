@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define VTGS_ABI_VERSION 1
+#define VTGS_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define VTGS_API __attribute__((visibility("default")))
@@ -134,7 +134,8 @@ typedef struct vtgs_l1_loss {
     int32_t color_mask_mode, depth_mask_mode, normalize;
 } vtgs_l1_loss;
 
-enum { VTGS_GRAD_COLOR = 1, VTGS_GRAD_OPACITY = 2, VTGS_GRAD_RADIUS = 4, VTGS_GRAD_POSE = 8 };
+enum { VTGS_GRAD_COLOR = 1, VTGS_GRAD_OPACITY = 2, VTGS_GRAD_RADIUS = 4, VTGS_GRAD_POSE = 8,
+       VTGS_GRAD_POSITION = 16 };
 
 /* (5) Backward of the LAST vtgs_render_fwd on this context — SPEC.md:197-205 (chain through
  * the α/T recurrence, the footprint σ = f·r/z, the projection), SPEC.md:223 (pose gradient on
@@ -145,6 +146,10 @@ enum { VTGS_GRAD_COLOR = 1, VTGS_GRAD_OPACITY = 2, VTGS_GRAD_RADIUS = 4, VTGS_GR
  *   d_col_opa float4[N] (dc_r, dc_g, dc_b, do) and d_radius [N] are ACCUMULATED (+=, the
  *   caller zeroes them), so multi-view mapping is a loop of fwd/bwd pairs.  Either may be NULL
  *   when the corresponding want bits are clear.
+ *   d_position float4[N]: with VTGS_GRAD_POSITION, dL/dX_w (x, y, z; w untouched) of every
+ *   Gaussian centre is ACCUMULATED (+=) — the input of the head-frame bundle adjustment
+ *   (vtgs_keyframe_pose_grad); NULL when not wanted.  Not restricted to
+ *   [learn_begin, learn_end).
  *   d_pose [7] (dq_w, dq_x, dq_y, dq_z, dt_x, dt_y, dt_z) is OVERWRITTEN (NULL if not wanted).
  *   loss_out: device float, OVERWRITTEN with the loss value (NULL = not needed; requires loss).
  * Attribute gradients are summed with float atomics across tiles: run-to-run results can
@@ -152,7 +157,23 @@ enum { VTGS_GRAD_COLOR = 1, VTGS_GRAD_OPACITY = 2, VTGS_GRAD_RADIUS = 4, VTGS_GR
 VTGS_API vtgs_status vtgs_render_bwd(vtgs_ctx *ctx, const float *dL_dcolor, const float *dL_ddepth,
                             const float *dL_dsil, const vtgs_l1_loss *loss, uint32_t want,
                             int64_t learn_begin, int64_t learn_end, float *d_col_opa,
-                            float *d_radius, float *d_pose, float *loss_out, void *stream);
+                            float *d_radius, float *d_position, float *d_pose, float *loss_out,
+                            void *stream);
+
+/* Head-frame bundle adjustment — PAPER.md:248-250 (§3.5: "back-propagate gradients to update
+ * the camera pose of the head frame").  A view-tied centre is its keyframe's back-projected
+ * depth pixel, X_w = R_k X_k + t_k, so
+ *   dL/dt_k = Σ_{g ∈ k} dL/dX_w,g,   dL/dR_k = Σ_{g ∈ k} dL/dX_w,g X_kᵀ,  X_k = R_kᵀ(X_w − t_k),
+ * then through R(q̂), q̂ = q/|q|.  Keyframe k owns slots [k·slots_per_kf,
+ * (k+1)·slots_per_kf) (vtgs_instantiate's layout); invalid slots (r = 0) are skipped.
+ *   pos_rad float4[K·slots_per_kf] (device), d_position float4[...] (device, from
+ *   vtgs_render_bwd with VTGS_GRAD_POSITION), kf_poses vtgs_pose[K] (device);
+ *   d_kf_pose float[K×7] (device) is OVERWRITTEN (dq 4, dt 3 per keyframe).
+ * The total gradient of a head frame that is also the rendered view is d_pose + d_kf_pose[k].
+ * Sums are fp64 in a fixed order (deterministic).  Asynchronous on `stream`. */
+VTGS_API vtgs_status vtgs_keyframe_pose_grad(vtgs_ctx *ctx, const float *pos_rad, const float *d_position,
+                                    const vtgs_pose *kf_poses, int32_t K, int64_t slots_per_kf,
+                                    float *d_kf_pose, void *stream);
 
 /* One Adam step on a device pose (β1 = 0.9, β2 = 0.999, ε = 1e-8; learning
  * rates lr_rot for q and lr_trans for t), then q ← q/|q|.
@@ -175,8 +196,8 @@ VTGS_API vtgs_status vtgs_get_stats(vtgs_ctx *ctx, vtgs_stats *out /* host */, v
 /* Per-kernel device timing (CUDA events recorded on the launching stream around every kernel
  * while enabled; not for use inside CUDA-graph capture).  Stages, in order:
  *   0 project_count, 1 scan_tiles, 2 emit_pairs, 3 tile_sort, 4 composite_fwd, 5 l1_count,
- *   6 composite_bwd, 7 pose_finalize, 8 instantiate, 9 pose_adam. */
-#define VTGS_NUM_STAGES 10
+ *   6 composite_bwd, 7 pose_finalize, 8 instantiate, 9 pose_adam, 10 keyframe_pose_grad. */
+#define VTGS_NUM_STAGES 11
 VTGS_API vtgs_status vtgs_set_profiling(vtgs_ctx *ctx, int32_t enable);
 /* Synchronous: sum of event-timed milliseconds (ms[VTGS_NUM_STAGES], host) and launch counts
  * (counts[VTGS_NUM_STAGES], host, may be NULL) per stage since the previous call; resets. */

@@ -62,7 +62,10 @@ def _load():
                           _D, _D, _D, _D, _I32, _I32, _I64, _U8, ctypes.POINTER(ctypes.c_uint64), _I32]
             f = getattr(lib, f"or_render_bwd_{m}")
             f.restype = ctypes.c_int
-            f.argtypes = [_D, _D, ctypes.c_int64, _D, _D, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D, _D, _D, _D, _D]
+            f.argtypes = [_D, _D, ctypes.c_int64, _D, _D, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D, _D, _D, _D, _D, _D, _D]
+            f = getattr(lib, f"or_keyframe_pose_grad_{m}")
+            f.restype = None
+            f.argtypes = [_D, _D, ctypes.c_int, _D, ctypes.c_int, ctypes.c_int, _D, _D]
         f = lib.or_l1_upstream
         f.restype = ctypes.c_double
         f.argtypes = [_D, _D, _D, _D, _D, _U8, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
@@ -164,7 +167,7 @@ def render(pos_rad, col_opa, view, intr, rows=None, mode="f32", want_tainted=Fal
 
 def render_bwd(pos_rad, col_opa, view, intr, gC=None, gD=None, gS=None, mode="f32"):
     """(a5) → dict(d_col_opa [N,4], d_radius [N], d_pose [7], d_geom [N,4] (du,dv,dσ,dz),
-    d_abs [N,5] (Σ of |per-pixel contributions| to dc0..2, do, dr))."""
+    d_abs [N,5] (Σ of |per-pixel contributions| to dc0..2, do, dr), d_pos [N,3] (dL/dX_w), d_pos_abs [N,3] (its Σ|terms|))."""
     lib = _load()
     pos_rad = _d(pos_rad).reshape(-1, 4)
     col_opa = _d(col_opa).reshape(-1, 4)
@@ -178,13 +181,30 @@ def render_bwd(pos_rad, col_opa, view, intr, gC=None, gD=None, gS=None, mode="f3
     d_pose = np.zeros(7)
     d_geom = np.zeros((max(N, 1), 4))
     d_abs = np.zeros((max(N, 1), 5))
+    d_pos = np.zeros((max(N, 1), 3))
+    d_pos_abs = np.zeros((max(N, 1), 3))
     rc = getattr(lib, f"or_render_bwd_{mode}")(_p(pos_rad), _p(col_opa), N, _p(_d(view)), _p(_intr(intr)), W, H,
                                                _p(gC), _p(gD), _p(gS), _p(d_col_opa), _p(d_rad), _p(d_pose),
-                                               _p(d_geom), _p(d_abs))
+                                               _p(d_geom), _p(d_abs), _p(d_pos), _p(d_pos_abs))
     if rc:
         raise MemoryError("oracle render_bwd")
     return {"d_col_opa": d_col_opa[:N], "d_radius": d_rad[:N], "d_pose": d_pose, "d_geom": d_geom[:N],
-            "d_abs": d_abs[:N]}
+            "d_abs": d_abs[:N], "d_pos": d_pos[:N], "d_pos_abs": d_pos_abs[:N]}
+
+
+def keyframe_pose_grad(depth, poses, intr, d_pos, mode="f64"):
+    """Head-frame bundle adjustment: dL/d(keyframe pose) [K,7] (dq 4, dt 3) from the
+    keyframes' depth [K,H,W], poses [K,7] and dL/dX_w per slot [K*H*W,3]."""
+    lib = _load()
+    depth = _d(depth)
+    K, H, W = depth.shape
+    poses = _d(poses).reshape(K, 7)
+    d_pos = _d(d_pos).reshape(K * H * W, 3)
+    out = np.zeros((K, 7))
+    getattr(lib, f"or_keyframe_pose_grad_{mode}")(_p(depth), _p(poses), K, _p(_intr(intr)), W, H, _p(d_pos),
+                                                  _p(out))
+    return out
+
 
 
 def l1_upstream(color, depth, sil, target_rgb, target_depth, vis=None, w_color=1.0, w_depth=0.5,

@@ -12,6 +12,7 @@
  *   or_tile_lists_*   (a3)  16×16 tile lists in (z, gid) order
  *   or_render_*       (a4)  per-pixel front-to-back compositing
  *   or_render_bwd_*   (a5)  derivative of the compositing closed form
+ *   or_keyframe_pose_grad_*  head-frame bundle adjustment: keyframe poses
  *   or_l1_upstream          masked L1 terms of Eq. 1 / Eq. 2
  * Two builds of the same source (oracle_impl.inc): *_f32 takes every decision in fp32 (the
  * kernel's precision) with fp64 values; *_f64 is fp64 throughout.

@@ -216,12 +216,13 @@ vtgs_status vtgs_render_fwd(vtgs_ctx *ctx, const float *pos_rad, const float *co
 vtgs_status vtgs_render_bwd(vtgs_ctx *ctx, const float *dL_dcolor, const float *dL_ddepth,
                             const float *dL_dsil, const vtgs_l1_loss *loss, uint32_t want,
                             int64_t learn_begin, int64_t learn_end, float *d_col_opa,
-                            float *d_radius, float *d_pose, float *loss_out, void *stream) {
+                            float *d_radius, float *d_position, float *d_pose, float *loss_out,
+                            void *stream) {
     if (!ctx) return VTGS_ERR_INVALID_ARG;
     Ctx &c = ctx->c;
     c.last_error[0] = 0;
     if (!c.have_fwd) return fail(ctx, VTGS_ERR_STATE, "vtgs_render_bwd before any vtgs_render_fwd");
-    if (want & ~0xfu) return fail(ctx, VTGS_ERR_INVALID_ARG, "unknown bits in want = 0x%x", want);
+    if (want & ~0x1fu) return fail(ctx, VTGS_ERR_INVALID_ARG, "unknown bits in want = 0x%x", want);
     if (loss && (dL_dcolor || dL_ddepth || dL_dsil))
         return fail(ctx, VTGS_ERR_INVALID_ARG, "pass either upstream gradients or a fused loss, not both");
     if (loss && (!loss->target_rgb || !loss->target_depth))
@@ -233,14 +234,38 @@ vtgs_status vtgs_render_bwd(vtgs_ctx *ctx, const float *dL_dcolor, const float *
         return fail(ctx, VTGS_ERR_INVALID_ARG, "radius gradient wanted but d_radius is NULL");
     if ((want & VTGS_GRAD_POSE) && !d_pose)
         return fail(ctx, VTGS_ERR_INVALID_ARG, "pose gradient wanted but d_pose is NULL");
+    if ((want & VTGS_GRAD_POSITION) && !d_position)
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "position gradient wanted but d_position is NULL");
+    if (d_position && !aligned16(d_position))
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "d_position must be a 16-byte aligned float4 array");
     if (d_col_opa && !aligned16(d_col_opa))
         return fail(ctx, VTGS_ERR_INVALID_ARG, "d_col_opa must be a 16-byte aligned float4 array");
     if (learn_begin < 0) learn_begin = 0;
     if (learn_end > c.N) learn_end = c.N;
     cudaSetDevice(c.device);
     cudaError_t e = vtgs::launch_backward(c, dL_dcolor, dL_ddepth, dL_dsil, loss, want, learn_begin, learn_end,
-                                          (float4 *)d_col_opa, d_radius, d_pose, loss_out, (cudaStream_t)stream);
+                                          (float4 *)d_col_opa, d_radius, (float4 *)d_position, d_pose, loss_out,
+                                          (cudaStream_t)stream);
     return e ? cuda_fail(ctx, e, "vtgs_render_bwd") : VTGS_OK;
+}
+
+vtgs_status vtgs_keyframe_pose_grad(vtgs_ctx *ctx, const float *pos_rad, const float *d_position,
+                                    const vtgs_pose *kf_poses, int32_t K, int64_t slots_per_kf, float *d_kf_pose,
+                                    void *stream) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    c.last_error[0] = 0;
+    if (!pos_rad || !d_position || !kf_poses || !d_kf_pose)
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "NULL pos_rad / d_position / kf_poses / d_kf_pose");
+    if (K < 0 || slots_per_kf < 0) return fail(ctx, VTGS_ERR_SHAPE, "K = %d, slots_per_kf = %lld", K,
+                                                (long long)slots_per_kf);
+    if (!aligned16(pos_rad) || !aligned16(d_position))
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "pos_rad / d_position must be 16-byte aligned float4 arrays");
+    if (K == 0) return VTGS_OK;
+    cudaSetDevice(c.device);
+    cudaError_t e = vtgs::launch_keyframe_pose_grad(c, (const float4 *)pos_rad, (const float4 *)d_position, kf_poses,
+                                                    K, slots_per_kf, d_kf_pose, (cudaStream_t)stream);
+    return e ? cuda_fail(ctx, e, "vtgs_keyframe_pose_grad") : VTGS_OK;
 }
 
 vtgs_status vtgs_pose_adam_step(vtgs_ctx *ctx, vtgs_pose *pose, const float *d_pose, float *adam_state,
@@ -361,8 +386,9 @@ vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col
     st = vtgs_render_fwd(ctx, pos_rad, col_opa, N, d_view, intr, color, depth, silhouette, stream);
     if (st) return st;
     vtgs_l1_loss L{d_rgb, d_dep, nullptr, w_color, w_depth, color_mask_mode, depth_mask_mode, normalize};
-    st = vtgs_render_bwd(ctx, nullptr, nullptr, nullptr, &L, want, learn_begin, learn_end, d_col_opa, d_radius,
-                         (want & VTGS_GRAD_POSE) ? d_dpose : nullptr, d_loss, stream);
+    st = vtgs_render_bwd(ctx, nullptr, nullptr, nullptr, &L, want & ~(uint32_t)VTGS_GRAD_POSITION, learn_begin,
+                         learn_end, d_col_opa, d_radius, nullptr, (want & VTGS_GRAD_POSE) ? d_dpose : nullptr, d_loss,
+                         stream);
     if (st) return st;
     e = cudaMemcpyAsync(loss_host, d_loss, sizeof(float), cudaMemcpyDeviceToHost, s);
     if (!e && d_pose_host && (want & VTGS_GRAD_POSE))

@@ -41,6 +41,7 @@ struct BwdArgs {
     uint32_t want;
     float4 *d_col_opa;
     float *d_radius;
+    float4 *d_position;
     double *partials;
 };
 
@@ -267,6 +268,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
                 float dzt = dzd - (du * (Aj.x - p.in.cx) + dv * (Aj.y - p.in.cy)) * iz;
                 if (X.w > 0.f) dzt -= dsg * s * iz;  // ∂σ/∂z = −σ/z (unclamped)
                 const float gx = du * p.in.fx * iz, gy = dv * p.in.fy * iz, gz = dzt;
+                if ((p.want & VTGS_GRAD_POSITION) && (gx != 0.f || gy != 0.f || gz != 0.f))   // dL/dX_w = R g
+                    atomicAdd(&p.d_position[cur.g],
+                              make_float4(P.R[0] * gx + P.R[1] * gy + P.R[2] * gz, P.R[3] * gx + P.R[4] * gy + P.R[5] * gz,
+                                          P.R[6] * gx + P.R[7] * gy + P.R[8] * gz, 0.f));
                 h0 += gx; h1 += gy; h2 += gz;
                 K00 = fmaf(X.x, gx, K00); K01 = fmaf(X.x, gy, K01); K02 = fmaf(X.x, gz, K02);
                 K10 = fmaf(X.y, gx, K10); K11 = fmaf(X.y, gy, K11); K12 = fmaf(X.y, gz, K12);
@@ -441,8 +446,8 @@ cudaError_t backward_set_attributes() {
 
 cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const float *dS,
                             const vtgs_l1_loss *loss, uint32_t want, int64_t learn_begin,
-                            int64_t learn_end, float4 *d_col_opa, float *d_radius, float *d_pose,
-                            float *loss_out, cudaStream_t s) {
+                            int64_t learn_end, float4 *d_col_opa, float *d_radius, float4 *d_position,
+                            float *d_pose, float *loss_out, cudaStream_t s) {
     const int W = c.intr.width, H = c.intr.height;
     const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile, T = ntx * nty;
     cudaError_t err;
@@ -454,7 +459,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     a.dC = dC; a.dD = dD; a.dS = dS;
     a.dev = c.dev; a.view = c.view_copy; a.in = c.intr;
     a.learn_begin = learn_begin; a.learn_end = learn_end; a.want = want;
-    a.d_col_opa = d_col_opa; a.d_radius = d_radius; a.partials = c.partials;
+    a.d_col_opa = d_col_opa; a.d_radius = d_radius; a.d_position = d_position; a.partials = c.partials;
     const bool L = loss != nullptr;
     if (L) {
         a.tC = loss->target_rgb; a.tD = loss->target_depth; a.vis = loss->vis_mask;
@@ -471,7 +476,9 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     }
     const bool A = (want & (VTGS_GRAD_COLOR | VTGS_GRAD_OPACITY | VTGS_GRAD_RADIUS)) != 0;
     const bool P = (want & VTGS_GRAD_POSE) != 0 && d_pose != nullptr;
-    const int sel = (A ? 4 : 0) | (P ? 2 : 0) | (L ? 1 : 0);
+    const bool X = (want & VTGS_GRAD_POSITION) != 0 && d_position != nullptr;   // same chain as the pose
+    if (!X) a.want &= ~(uint32_t)VTGS_GRAD_POSITION;
+    const int sel = (A ? 4 : 0) | ((P || X) ? 2 : 0) | (L ? 1 : 0);
     {
     LaunchScope ls(&c, kCompBwd, s);
     switch (sel) {
@@ -495,6 +502,80 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
         if ((err = cudaGetLastError())) return err;
     }
     return cudaSuccess;
+}
+
+
+// Head-frame bundle adjustment: per keyframe k, the 12 sums Σ dL/dX_w and
+// Σ dL/dX_w X_kᵀ over its slots (X_k = R_kᵀ(X_w − t_k), fp64), then the rotation chain.  One
+// CTA per keyframe, fixed-order block reduction (deterministic).
+__global__ void __launch_bounds__(256) k_keyframe_pose_grad(const float4 *__restrict__ pos_rad,
+                                                            const float4 *__restrict__ d_position,
+                                                            const vtgs_pose *__restrict__ kf_poses,
+                                                            int64_t spk, float *__restrict__ d_kf) {
+    __shared__ double red[256][12];
+    __shared__ PoseR P;
+    const int k = blockIdx.x, tid = threadIdx.x;
+    if (tid == 0) pose_rotation(kf_poses[k], P);
+    __syncthreads();
+    const double w = P.qhat[0], x = P.qhat[1], y = P.qhat[2], z = P.qhat[3];
+    // fp64 rotation from the normalised quaternion (X_k recovered without fp32 rounding of R)
+    const double Rd[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                          2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+                          2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
+    const double t0 = kf_poses[k].t[0], t1 = kf_poses[k].t[1], t2 = kf_poses[k].t[2];
+    double acc[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) acc[i] = 0.0;
+    const int64_t b = (int64_t)k * spk;
+    for (int64_t i = tid; i < spk; i += 256) {
+        const float4 pr = __ldg(pos_rad + b + i);
+        if (!(pr.w > 0.f)) continue;
+        const float4 g = __ldg(d_position + b + i);
+        const double d0 = (double)pr.x - t0, d1 = (double)pr.y - t1, d2 = (double)pr.z - t2;
+        const double X[3] = {Rd[0] * d0 + Rd[3] * d1 + Rd[6] * d2, Rd[1] * d0 + Rd[4] * d1 + Rd[7] * d2,
+                             Rd[2] * d0 + Rd[5] * d1 + Rd[8] * d2};
+        const double G[3] = {g.x, g.y, g.z};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            acc[a] += G[a];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc[3 + 3 * a + c] += G[a] * X[c];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 12; ++i) red[tid][i] = acc[i];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (tid < s)
+#pragma unroll
+            for (int i = 0; i < 12; ++i) red[tid][i] += red[tid + s][i];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        const double *M = &red[0][3];   // dL/dR_k (row-major), dL/dt_k = red[0][0..2]
+        const double Dw[9] = {0, -2 * z, 2 * y, 2 * z, 0, -2 * x, -2 * y, 2 * x, 0};
+        const double Dx[9] = {0, 2 * y, 2 * z, 2 * y, -4 * x, -2 * w, 2 * z, 2 * w, -4 * x};
+        const double Dy[9] = {-4 * y, 2 * x, 2 * w, 2 * x, 0, 2 * z, -2 * w, 2 * z, -4 * y};
+        const double Dz[9] = {-4 * z, -2 * w, 2 * x, 2 * w, -4 * z, 2 * y, 2 * x, 2 * y, 0};
+        double gq[4] = {0, 0, 0, 0};
+        for (int i = 0; i < 9; ++i) {
+            gq[0] += M[i] * Dw[i];
+            gq[1] += M[i] * Dx[i];
+            gq[2] += M[i] * Dy[i];
+            gq[3] += M[i] * Dz[i];
+        }
+        const double dot = gq[0] * w + gq[1] * x + gq[2] * y + gq[3] * z;
+        const double qh[4] = {w, x, y, z};
+        for (int i = 0; i < 4; ++i) d_kf[7 * k + i] = (float)((gq[i] - qh[i] * dot) / P.qnorm);
+        for (int a = 0; a < 3; ++a) d_kf[7 * k + 4 + a] = (float)red[0][a];
+    }
+}
+
+cudaError_t launch_keyframe_pose_grad(Ctx &c, const float4 *pos_rad, const float4 *d_position,
+                                      const vtgs_pose *kf_poses, int K, int64_t spk, float *d_kf, cudaStream_t s) {
+    LaunchScope ls(&c, kKfPose, s);
+    k_keyframe_pose_grad<<<K, 256, 0, s>>>(pos_rad, d_position, kf_poses, spk, d_kf);
+    return cudaGetLastError();
 }
 
 // One Adam step on the device pose, then q ← q / |q|.

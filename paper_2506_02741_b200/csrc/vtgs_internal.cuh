@@ -40,7 +40,7 @@ struct DevScalars {
 };
 
 enum Stage { kProject = 0, kScan, kEmit, kSort, kCompFwd, kL1Count, kCompBwd, kFinalize, kInstantiate,
-             kPoseAdam, kNumStages };
+             kPoseAdam, kKfPose, kNumStages };
 
 struct ProfEvent {
     int stage;
@@ -207,8 +207,10 @@ cudaError_t launch_instantiate(Ctx &c, const float *depth, const float *rgb, con
 cudaError_t launch_forward(Ctx &c, cudaStream_t s);
 cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const float *dS,
                             const vtgs_l1_loss *loss, uint32_t want, int64_t learn_begin,
-                            int64_t learn_end, float4 *d_col_opa, float *d_radius, float *d_pose,
-                            float *loss_out, cudaStream_t s);
+                            int64_t learn_end, float4 *d_col_opa, float *d_radius, float4 *d_position,
+                            float *d_pose, float *loss_out, cudaStream_t s);
+cudaError_t launch_keyframe_pose_grad(Ctx &c, const float4 *pos_rad, const float4 *d_position,
+                                      const vtgs_pose *kf_poses, int K, int64_t spk, float *d_kf, cudaStream_t s);
 cudaError_t forward_set_attributes();
 cudaError_t backward_set_attributes();
 cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s);

@@ -29,7 +29,7 @@ VTGS_ERR_CAPACITY = -3
 VTGS_ERR_CUDA = -4
 VTGS_ERR_STATE = -5
 VTGS_ERR_NO_DEVICE = -6
-VTGS_GRAD_COLOR, VTGS_GRAD_OPACITY, VTGS_GRAD_RADIUS, VTGS_GRAD_POSE = 1, 2, 4, 8
+VTGS_GRAD_COLOR, VTGS_GRAD_OPACITY, VTGS_GRAD_RADIUS, VTGS_GRAD_POSE, VTGS_GRAD_POSITION = 1, 2, 4, 8, 16
 VTGS_GRAD_ATTR = VTGS_GRAD_COLOR | VTGS_GRAD_OPACITY | VTGS_GRAD_RADIUS
 VTGS_GRAD_ALL = VTGS_GRAD_ATTR | VTGS_GRAD_POSE
 
@@ -66,7 +66,8 @@ _SIGS = {
     "vtgs_instantiate": (_c.c_int32, [_P, _P, _P, _P, _c.c_int32, vtgs_intrinsics, _P, _c.c_float, _P, _P, _P]),
     "vtgs_render_fwd": (_c.c_int32, [_P, _P, _P, _c.c_int64, _P, vtgs_intrinsics, _P, _P, _P, _P]),
     "vtgs_render_bwd": (_c.c_int32, [_P, _P, _P, _P, _c.POINTER(vtgs_l1_loss), _c.c_uint32, _c.c_int64, _c.c_int64,
-                                     _P, _P, _P, _P, _P]),
+                                     _P, _P, _P, _P, _P, _P]),
+    "vtgs_keyframe_pose_grad": (_c.c_int32, [_P, _P, _P, _P, _c.c_int32, _c.c_int64, _P, _P]),
     "vtgs_pose_adam_step": (_c.c_int32, [_P, _P, _P, _P, _c.c_float, _c.c_float, _P]),
     "vtgs_get_stats": (_c.c_int32, [_P, _c.POINTER(vtgs_stats), _P]),
     "vtgs_check": (_c.c_int32, [_P, _P]),
@@ -173,7 +174,7 @@ class Renderer:
     # --- (5)
     def render_bwd(self, want: int, d_col_opa=None, d_radius=None, d_pose=None, dL_dcolor=None, dL_ddepth=None,
                    dL_dsil=None, loss: Optional[dict] = None, learn: Sequence[int] = (0, 1 << 62),
-                   loss_out=None, stream=None):
+                   loss_out=None, stream=None, d_position=None):
         lp = None
         if loss is not None:
             L = vtgs_l1_loss(_ptr(loss["target_rgb"]), _ptr(loss["target_depth"]), _ptr(loss.get("vis_mask")),
@@ -182,8 +183,18 @@ class Renderer:
                              int(loss.get("normalize", 0)))
             lp = ctypes.byref(L)
         _ok(vtgs_render_bwd(self.ctx, _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(dL_dsil), lp, int(want), int(learn[0]),
-                            int(learn[1]), _ptr(d_col_opa), _ptr(d_radius), _ptr(d_pose), _ptr(loss_out),
-                            _stream(stream)), self.ctx)
+                            int(learn[1]), _ptr(d_col_opa), _ptr(d_radius), _ptr(d_position), _ptr(d_pose),
+                            _ptr(loss_out), _stream(stream)), self.ctx)
+
+    def keyframe_pose_grad(self, pos_rad: torch.Tensor, d_position: torch.Tensor, kf_poses: torch.Tensor,
+                           slots_per_kf: int, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """Head-frame bundle adjustment: dL/d(keyframe pose) [K, 7]."""
+        K = kf_poses.reshape(-1, 7).shape[0]
+        if out is None:
+            out = torch.empty((K, 7), dtype=torch.float32, device=self.device)
+        _ok(vtgs_keyframe_pose_grad(self.ctx, _ptr(pos_rad), _ptr(d_position), _ptr(kf_poses), K, int(slots_per_kf),
+                                    _ptr(out), _stream(stream)), self.ctx)
+        return out
 
     def pose_adam_step(self, pose: torch.Tensor, d_pose: torch.Tensor, state: torch.Tensor, lr_rot: float,
                        lr_trans: float, stream=None):
@@ -199,7 +210,7 @@ class Renderer:
         return d
 
     STAGES = ("project_count", "scan_tiles", "emit_pairs", "tile_sort", "composite_fwd", "l1_count",
-              "composite_bwd", "pose_finalize", "instantiate", "pose_adam")
+              "composite_bwd", "pose_finalize", "instantiate", "pose_adam", "keyframe_pose_grad")
 
     def set_profiling(self, enable: bool):
         _ok(vtgs_set_profiling(self.ctx, int(bool(enable))), self.ctx)

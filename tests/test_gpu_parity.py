@@ -509,3 +509,86 @@ def test_step_host_matches_device_path(vt):
     torch.cuda.synchronize()
     assert loss_h == pytest.approx(lo.item(), rel=1e-6)
     assert torch.allclose(d1, d2, rtol=1e-5, atol=1e-6)
+
+
+# ------------------------------------------------------------------------------ f1 (head-frame BA)
+def _ba_scene(seed=0, W=64, H=48, K=3):
+    """K keyframes of a noisy slanted surface 1.5–3 m away, a view between keyframes 0 and 1."""
+    from synth.scenes import perturb_pose
+    rng = np.random.default_rng(seed)
+    intr = Intrinsics(60.0, 60.0, (W - 1) / 2, (H - 1) / 2, W, H)
+    base = np.array([1.0, 0, 0, 0, 0, 0, 0])
+    poses = np.stack([perturb_pose(base, 2.0 * k, 0.03 * k, rng) for k in range(K)]).astype(np.float32)
+    xs, ys = np.meshgrid(np.arange(W), np.arange(H))
+    depth = np.stack([1.5 + 1.5 * xs / W + 0.3 * ys / H + rng.normal(0, 0.01, (H, W)) for _ in range(K)])
+    depth[:, rng.random((H, W)) < 0.01] = 0.0
+    rgb = rng.uniform(0, 1, (K, H, W, 3))
+    opa = 1 / (1 + np.exp(-rng.normal(size=(K, H, W))))
+    view = perturb_pose(poses[0].astype(np.float64), 1.0, 0.015, rng)
+    return intr, poses, depth.astype(np.float32), rgb.astype(np.float32), opa.astype(np.float32), view
+
+
+def test_position_and_keyframe_pose_gradient_parity(vt):
+    """Head-frame bundle adjustment: dL/dX_w per Gaussian (VTGS_GRAD_POSITION)
+    within the gradient bar (1e-3 rel / 1e-5 abs, or the fp32 summation floor, R23) on
+    untainted Gaussians, and the per-keyframe pose gradients (vtgs_keyframe_pose_grad) within 1e-3
+    of their norm, against the oracle's or_render_bwd d_pos + or_keyframe_pose_grad."""
+    intr, poses, depth, rgb, opa, view = _ba_scene()
+    K, H, W = depth.shape
+    N = K * H * W
+    R = vt.Renderer(0, N, W, H)
+    dev = "cuda"
+    pr, co = R.instantiate(torch.from_numpy(depth).to(dev), torch.from_numpy(rgb).to(dev),
+                           vt.pose_tensor(poses, dev), intr, torch.from_numpy(opa).to(dev))
+    v = vt.pose_tensor(view32(view), dev)
+    out = R.render_fwd(pr, co, v, intr)
+    rng = np.random.default_rng(3)
+    gC = rng.normal(size=(H, W, 3)).astype(np.float32)
+    gD = rng.normal(size=(H, W)).astype(np.float32)
+    gS = rng.normal(size=(H, W)).astype(np.float32)
+    dpos = torch.zeros((N, 4), device=dev)
+    dpose = torch.zeros(7, device=dev)
+    R.render_bwd(vt.VTGS_GRAD_POSITION | vt.VTGS_GRAD_POSE, d_position=dpos, d_pose=dpose,
+                 dL_dcolor=torch.from_numpy(gC).to(dev), dL_ddepth=torch.from_numpy(gD).to(dev),
+                 dL_dsil=torch.from_numpy(gS).to(dev))
+    kf_gpu = R.keyframe_pose_grad(pr, dpos, vt.pose_tensor(poses, dev), H * W).cpu().numpy().astype(np.float64)
+    torch.cuda.synchronize()
+    del out
+    opr, oco, _ = oracle.instantiate(depth, rgb, poses.astype(np.float64), intr, opa)
+    ref = oracle.render(opr, oco, view32(view), intr, want_tainted=True)
+    g = oracle.render_bwd(opr, oco, view32(view), intr, gC, gD, gS)
+    keep = ~ref["tainted"]
+    d = dpos.cpu().numpy()[:, :3].astype(np.float64)
+    st = {}
+    ok = close(d[keep], g["d_pos"][keep], absum=g["d_pos_abs"][keep], stats=st)
+    assert ok.all(), report("d_position", ok, d[keep], g["d_pos"][keep])
+    assert st["floor_only"] <= 5 + 1e-5 * st["n"], st
+    assert np.linalg.norm(dpose.cpu().numpy() - g["d_pose"]) <= 1e-3 * np.linalg.norm(g["d_pose"])
+    kf_ref = oracle.keyframe_pose_grad(depth, poses.astype(np.float64), intr, g["d_pos"])
+    for k in range(K):
+        assert np.linalg.norm(kf_gpu[k] - kf_ref[k]) <= 1e-3 * np.linalg.norm(kf_ref[k]), (k, kf_gpu[k], kf_ref[k])
+
+
+def test_view_tied_pose_invariance_gpu(vt):
+    """A keyframe rendered from its own pose: view-pose and owner-pose gradients cancel
+    (d_pose + d_kf_pose = 0 up to fp32 summation, PAPER.md:119 view-tied centres)."""
+    intr, poses, depth, rgb, opa, _ = _ba_scene(seed=1, K=1)
+    K, H, W = depth.shape
+    N = K * H * W
+    R = vt.Renderer(0, N, W, H)
+    dev = "cuda"
+    pt = vt.pose_tensor(poses, dev)
+    pr, co = R.instantiate(torch.from_numpy(depth).to(dev), torch.from_numpy(rgb).to(dev), pt, intr,
+                           torch.from_numpy(opa).to(dev))
+    out = R.render_fwd(pr, co, pt[0:1].clone(), intr)
+    rng = np.random.default_rng(5)
+    dpos = torch.zeros((N, 4), device=dev)
+    dpose = torch.zeros(7, device=dev)
+    R.render_bwd(vt.VTGS_GRAD_POSITION | vt.VTGS_GRAD_POSE, d_position=dpos, d_pose=dpose,
+                 dL_dcolor=torch.from_numpy(rng.normal(size=(H, W, 3)).astype(np.float32)).to(dev))
+    kf = R.keyframe_pose_grad(pr, dpos, pt, H * W)[0]
+    torch.cuda.synchronize()
+    del out
+    s = dpose.abs().max().item()
+    assert s > 1e-2
+    assert (dpose + kf).abs().max().item() <= 2e-3 * s, (dpose.cpu().numpy(), kf.cpu().numpy())

@@ -511,3 +511,71 @@ def test_tracking_mask_semantics():
     Wm = np.array([[1, 0, 0], [1, 0, 1]], dtype=bool)
     assert loss == pytest.approx(Wm.sum() * (3 * 1.0 + 0.5))
     assert np.all((gC != 0).any(-1) == Wm) and np.all((gD != 0) == Wm)
+
+
+# ------------------------------------------------------------------------------ f1 (head-frame BA)
+def _two_keyframe_scene(seed, W=14, H=12, K=2):
+    """K keyframes of a noisy tilted plane (depth 1.5–2.5 m), a view near keyframe 0."""
+    rng = np.random.default_rng(seed)
+    intr = Intrinsics(12.0, 12.5, (W - 1) / 2, (H - 1) / 2, W, H)
+    poses, depth = [], []
+    for k in range(K):
+        poses.append(perturb_pose(np.array([1.0, 0, 0, 0, 0, 0, 0]), 3.0 * k, 0.05 * k, rng))
+        xs = np.arange(W)[None, :]
+        depth.append(1.5 + 0.05 * xs + 0.03 * np.arange(H)[:, None] + rng.normal(0, 0.01, (H, W)))
+    depth = np.stack(depth)
+    rgb = rng.uniform(0, 1, (K, H, W, 3))
+    opa = 1 / (1 + np.exp(-rng.normal(size=(K, H, W))))
+    view = perturb_pose(poses[0], 1.0, 0.02, rng)
+    return intr, np.stack(poses), depth, rgb, opa, view
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_keyframe_pose_gradient_central_differences(seed):
+    """P:248-250 (head-frame bundle adjustment): dL/d(keyframe pose) through the view-tied centres
+    X_w = R_k X_k + t_k, from the per-Gaussian dL/dX_w, against central finite differences of a
+    random linear functional of (C, D, S) re-instantiating the keyframes (fp64, ε = 1e-6)."""
+    intr, poses, depth, rgb, opa, view = _two_keyframe_scene(seed)
+    H, W = intr.height, intr.width
+    rng = np.random.default_rng(100 + seed)
+    lC, lD, lS = rng.normal(size=(H, W, 3)), rng.normal(size=(H, W)), rng.normal(size=(H, W))
+
+    def L(ps):
+        pr, co, _ = oracle.instantiate(depth, rgb, ps, intr, opa, mode="f64")
+        r = oracle.render(pr, co, view, intr, mode="f64")
+        return (r["color"] * lC).sum() + (r["depth"] * lD).sum() + (r["sil"] * lS).sum(), r["trace"]
+
+    pr, co, _ = oracle.instantiate(depth, rgb, poses, intr, opa, mode="f64")
+    g = oracle.render_bwd(pr, co, view, intr, lC, lD, lS, mode="f64")
+    ana = oracle.keyframe_pose_grad(depth, poses, intr, g["d_pos"])
+    _, t0 = L(poses)
+    eps, checked, worst = 1e-6, 0, 0.0
+    for k in range(len(poses)):
+        for j in range(7):
+            pp, pm = poses.copy(), poses.copy()
+            pp[k, j] += eps
+            pm[k, j] -= eps
+            (lp, tp), (lm, tm) = L(pp), L(pm)
+            if not (np.array_equal(tp, t0) and np.array_equal(tm, t0)):
+                continue
+            fd = (lp - lm) / (2 * eps)
+            worst = max(worst, abs(fd - ana[k, j]) / max(abs(ana[k, j]), 1e-3))
+            checked += 1
+    assert checked >= 12 and worst < 1e-5, (checked, worst)
+
+
+def test_view_tied_pose_invariance():
+    """Rendering keyframe k's own Gaussians from keyframe k's own pose does not depend on that
+    pose (the centres move with the camera): the view-pose gradient and the owner-pose
+    gradient cancel exactly, d_view + d_kf = 0, and a rigid motion of both leaves the image."""
+    intr, poses, depth, rgb, opa, _ = _two_keyframe_scene(3, K=1)
+    H, W = intr.height, intr.width
+    rng = np.random.default_rng(7)
+    lC, lD, lS = rng.normal(size=(H, W, 3)), rng.normal(size=(H, W)), rng.normal(size=(H, W))
+    view = poses[0]
+    pr, co, _ = oracle.instantiate(depth, rgb, poses, intr, opa, mode="f64")
+    g = oracle.render_bwd(pr, co, view, intr, lC, lD, lS, mode="f64")
+    kf = oracle.keyframe_pose_grad(depth, poses, intr, g["d_pos"])[0]
+    scale = np.abs(g["d_pose"]).max()
+    assert scale > 1e-3
+    np.testing.assert_allclose(g["d_pose"] + kf, 0.0, atol=1e-8 * max(scale, 1.0))
