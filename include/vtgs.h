@@ -125,14 +125,32 @@ VTGS_API vtgs_status vtgs_render_fwd(vtgs_ctx *ctx, const float *pos_rad, const 
  *   color_mask_mode 0: m_c = 1 (Eq. 2), 1: m_c = W (Eq. 1)
  *   depth_mask_mode 0: m_d = U (Eq. 2), 1: m_d = W (Eq. 1)
  *   normalize 0: s = 1 (sum form), 1: s = 1 / Σ m (mean over masked pixels; 0 if
- *   the mask is empty).  Upstream gradients use sgn(0) = 0. */
+ *   the mask is empty).  Upstream gradients use sgn(0) = 0.
+ *   extra_dcolor [H×W×3] (device, may be NULL) is added to the colour upstream gradient — the
+ *   SSIM term of Eq. 2 from vtgs_ssim_loss, so the full mapping objective
+ *   ρ‖V − V'‖₁ + τ L_S + σ U‖D − D'‖₁ runs through one backward. */
 typedef struct vtgs_l1_loss {
     const float *target_rgb;   /* [H×W×3] */
     const float *target_depth; /* [H×W], 0 = invalid */
     const uint8_t *vis_mask;   /* [H×W] or NULL (= all visible) */
     float w_color, w_depth;
     int32_t color_mask_mode, depth_mask_mode, normalize;
+    const float *extra_dcolor;  /* [H×W×3] or NULL */
 } vtgs_l1_loss;
+
+/* SSIM term of the mapping objective Eq. 2 — PAPER.md:195-201 ("τ L_S(V_i, V_i') ... L_S is the
+ * SSIM loss"), τ = 0.2 in the paper's experiments.  DESIGN.md reading R24: 11×11
+ * Gaussian window σ = 1.5, C1 = 0.01², C2 = 0.03², per colour channel, zero padding outside the
+ * image, L_S = 1 − mean of the SSIM map over all pixels and channels.
+ *   color (the render V') and target_rgb (V) [height×width×3], device.
+ *   d_color [height×width×3] (device, may be NULL): dL/dV' of τ·L_S is ACCUMULATED (+=) — pass
+ *   it as vtgs_l1_loss.extra_dcolor (or add it to dL_dcolor) for vtgs_render_bwd.
+ *   loss_out (device float, may be NULL) is OVERWRITTEN with τ·L_S.
+ * Errors: image smaller than the 11×11 window → VTGS_ERR_SHAPE; larger than the context's
+ * max_width × max_height → VTGS_ERR_CAPACITY.  Asynchronous on `stream`; the loss is summed
+ * in a fixed order (deterministic). */
+VTGS_API vtgs_status vtgs_ssim_loss(vtgs_ctx *ctx, const float *color, const float *target_rgb, int32_t width,
+                           int32_t height, float tau, float *d_color, float *loss_out, void *stream);
 
 enum { VTGS_GRAD_COLOR = 1, VTGS_GRAD_OPACITY = 2, VTGS_GRAD_RADIUS = 4, VTGS_GRAD_POSE = 8,
        VTGS_GRAD_POSITION = 16 };
@@ -196,8 +214,8 @@ VTGS_API vtgs_status vtgs_get_stats(vtgs_ctx *ctx, vtgs_stats *out /* host */, v
 /* Per-kernel device timing (CUDA events recorded on the launching stream around every kernel
  * while enabled; not for use inside CUDA-graph capture).  Stages, in order:
  *   0 project_count, 1 scan_tiles, 2 emit_pairs, 3 tile_sort, 4 composite_fwd, 5 l1_count,
- *   6 composite_bwd, 7 pose_finalize, 8 instantiate, 9 pose_adam, 10 keyframe_pose_grad. */
-#define VTGS_NUM_STAGES 11
+ *   6 composite_bwd, 7 pose_finalize, 8 instantiate, 9 pose_adam, 10 keyframe_pose_grad, 11 ssim. */
+#define VTGS_NUM_STAGES 12
 VTGS_API vtgs_status vtgs_set_profiling(vtgs_ctx *ctx, int32_t enable);
 /* Synchronous: sum of event-timed milliseconds (ms[VTGS_NUM_STAGES], host) and launch counts
  * (counts[VTGS_NUM_STAGES], host, may be NULL) per stage since the previous call; resets. */

@@ -66,6 +66,9 @@ def _load():
             f = getattr(lib, f"or_keyframe_pose_grad_{m}")
             f.restype = None
             f.argtypes = [_D, _D, ctypes.c_int, _D, ctypes.c_int, ctypes.c_int, _D, _D]
+        f = lib.or_ssim_loss
+        f.restype = ctypes.c_double
+        f.argtypes = [_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_double, _D, _D]
         f = lib.or_l1_upstream
         f.restype = ctypes.c_double
         f.argtypes = [_D, _D, _D, _D, _D, _U8, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
@@ -223,3 +226,14 @@ def l1_upstream(color, depth, sil, target_rgb, target_depth, vis=None, w_color=1
                               float(w_depth), int(color_mask_mode), int(depth_mask_mode), int(normalize),
                               _p(gC), _p(gD), _p(gS), _p(fl, _I32))
     return float(loss), gC, gD, gS, fl.astype(bool)
+
+
+def ssim_loss(render_rgb, target_rgb, tau=0.2, want_map=False):
+    """SSIM term of Eq. 2: (τ·(1 − mean SSIM), dL/d render [H,W,3][, SSIM map])."""
+    lib = _load()
+    x, y = _d(render_rgb), _d(target_rgb)
+    H, W, _ = x.shape
+    grad = np.zeros((H, W, 3))
+    smap = np.zeros((H, W, 3)) if want_map else None
+    loss = lib.or_ssim_loss(_p(x), _p(y), W, H, float(tau), _p(grad), _p(smap))
+    return (loss, grad, smap) if want_map else (loss, grad)

@@ -14,6 +14,7 @@
  *   or_render_bwd_*   (a5)  derivative of the compositing closed form
  *   or_keyframe_pose_grad_*  head-frame bundle adjustment: keyframe poses
  *   or_l1_upstream          masked L1 terms of Eq. 1 / Eq. 2
+ *   or_ssim_loss            SSIM term τ·L_S of Eq. 2 and its gradient
  * Two builds of the same source (oracle_impl.inc): *_f32 takes every decision in fp32 (the
  * kernel's precision) with fp64 values; *_f64 is fp64 throughout.
  *
@@ -100,4 +101,82 @@ double or_l1_upstream(const double *C, const double *D, const double *S, const d
         if (flag) flag[p] = fl;
     }
     return loss;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * SSIM term of the mapping objective Eq. 2 ("τ L_S(V_i, V_i') ... L_S is the SSIM
+ * loss"; τ = 0.2).  The paper fixes no variant; reading R24 takes the standard
+ * one: 11×11 Gaussian window with σ = 1.5 normalised to sum 1, C1 = 0.01²,
+ * C2 = 0.03², applied to each colour channel with zero padding outside the image ("same"
+ * output size), L_S = 1 − mean of the SSIM map over all pixels and the 3 channels.
+ * Plain definition: for every pixel p and channel c the five window moments are summed
+ * directly over the 121 window taps,
+ *     μx = Σ w x, μy = Σ w y, σx² = Σ w x² − μx², σy² = Σ w y² − μy², σxy = Σ w x y − μx μy,
+ *     SSIM_p = (2 μx μy + C1)(2 σxy + C2) / ((μx² + μy² + C1)(σx² + σy² + C2)),
+ * and the gradient of τ·L_S w.r.t. x (the render) is the chain rule through those moments
+ * written out per (window centre p, tap q):
+ *     ∂SSIM_p/∂x_q = w_{q−p} [∂S/∂μx + 2 x_q ∂S/∂Exx + y_q ∂S/∂Exy]
+ * with ∂S/∂μx = S(2μy/A1 − 2μy/A2 − 2μx/B1 + 2μx/B2), ∂S/∂Exx = −S/B2, ∂S/∂Exy = 2S/A2
+ * (A1 = 2μxμy + C1, A2 = 2σxy + C2, B1 = μx² + μy² + C1, B2 = σx² + σy² + C2).
+ * fp64 throughout.  x, y: H×W×3 (x = render, y = target).  Returns τ·L_S; writes grad (H×W×3,
+ * overwritten, may be NULL) and the SSIM map (H×W×3, may be NULL).
+ * ------------------------------------------------------------------------------------- */
+double or_ssim_loss(const double *x, const double *y, int W, int H, double tau, double *grad, double *smap)
+{
+    const double C1 = 0.01 * 0.01, C2 = 0.03 * 0.03;
+    double w[11][11], g1[11], gs = 0.0;
+    for (int i = 0; i < 11; ++i) {
+        g1[i] = exp(-((double)(i - 5) * (i - 5)) / (2.0 * 1.5 * 1.5));
+        gs += g1[i];
+    }
+    for (int i = 0; i < 11; ++i)
+        for (int j = 0; j < 11; ++j) w[i][j] = (g1[i] / gs) * (g1[j] / gs);
+    const int64_t npx = (int64_t)W * H;
+    double *dS = (double *)malloc(sizeof(double) * 3 * (size_t)npx * 3);   /* ∂S/∂μx, ∂S/∂Exx, ∂S/∂Exy */
+    if (!dS) return NAN;
+    double sum = 0.0;
+    for (int py = 0; py < H; ++py)
+        for (int px = 0; px < W; ++px)
+            for (int c = 0; c < 3; ++c) {
+                double mx = 0, my = 0, exx = 0, eyy = 0, exy = 0;
+                for (int i = 0; i < 11; ++i)
+                    for (int j = 0; j < 11; ++j) {
+                        const int qy = py + i - 5, qx = px + j - 5;
+                        if (qx < 0 || qy < 0 || qx >= W || qy >= H) continue;   /* zero padding */
+                        const double a = x[3 * ((int64_t)qy * W + qx) + c], b = y[3 * ((int64_t)qy * W + qx) + c];
+                        mx += w[i][j] * a;
+                        my += w[i][j] * b;
+                        exx += w[i][j] * a * a;
+                        eyy += w[i][j] * b * b;
+                        exy += w[i][j] * a * b;
+                    }
+                const double A1 = 2 * mx * my + C1, A2 = 2 * (exy - mx * my) + C2;
+                const double B1 = mx * mx + my * my + C1, B2 = (exx - mx * mx) + (eyy - my * my) + C2;
+                const double S = A1 * A2 / (B1 * B2);
+                const int64_t k = 3 * ((int64_t)py * W + px) + c;
+                if (smap) smap[k] = S;
+                sum += S;
+                dS[3 * k + 0] = S * (2 * my / A1 - 2 * my / A2 - 2 * mx / B1 + 2 * mx / B2);
+                dS[3 * k + 1] = -S / B2;
+                dS[3 * k + 2] = 2 * S / A2;
+            }
+    const double n = 3.0 * (double)npx;
+    if (grad) {
+        const double dLdS = -tau / n;   /* L = τ (1 − Σ S / n) */
+        for (int64_t i = 0; i < 3 * npx; ++i) grad[i] = 0.0;
+        for (int py = 0; py < H; ++py)
+            for (int px = 0; px < W; ++px)
+                for (int c = 0; c < 3; ++c) {
+                    const int64_t k = 3 * ((int64_t)py * W + px) + c;
+                    for (int i = 0; i < 11; ++i)
+                        for (int j = 0; j < 11; ++j) {
+                            const int qy = py + i - 5, qx = px + j - 5;
+                            if (qx < 0 || qy < 0 || qx >= W || qy >= H) continue;
+                            const int64_t q = 3 * ((int64_t)qy * W + qx) + c;
+                            grad[q] += dLdS * w[i][j] * (dS[3 * k] + 2 * x[q] * dS[3 * k + 1] + y[q] * dS[3 * k + 2]);
+                        }
+                }
+    }
+    free(dS);
+    return tau * (1.0 - sum / n);
 }

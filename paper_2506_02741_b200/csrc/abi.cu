@@ -51,7 +51,7 @@ cudaError_t dalloc(T **p, size_t n) {
 
 void free_all(Ctx &c) {
     void *ptrs[] = {c.proj, c.rect, c.tile_count, c.tile_start, c.tile_cursor, c.tile_flag, c.keys, c.vals, c.pbits, c.keys2,
-                    c.vals2, c.offs, c.sub_lists, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy};
+                    c.vals2, c.offs, c.sub_lists, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy, c.ssim_abc, c.ssim_partials};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -125,6 +125,8 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = dalloc(&c.last, px);
     if (!e) e = dalloc(&c.partials, (size_t)c.max_tiles * 8 * 16 + 64 * 16);  // + k_pose_finalize level 2
     if (!e) e = dalloc(&c.dev, 1);
+    if (!e) e = dalloc(&c.ssim_abc, 9 * px);
+    if (!e) e = dalloc(&c.ssim_partials, ((size_t)(max_width + 31) / 32) * ((max_height + 7) / 8));
     if (!e) e = dalloc(&c.host_io, 4 * px + 64);
     if (!e) e = dalloc(&c.view_copy, 1);
     if (!e) e = cudaMemset(c.dev, 0, sizeof(vtgs::DevScalars));
@@ -132,6 +134,7 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = cudaMemset(c.tile_start, 0, sizeof(uint32_t) * (c.max_tiles + 1));
     if (!e) e = vtgs::forward_set_attributes();
     if (!e) e = vtgs::backward_set_attributes();
+    if (!e) e = vtgs::ssim_set_constants();
     if (!e) e = cudaDeviceSynchronize();
     cudaSetDevice(prev);
     if (e) {
@@ -268,6 +271,23 @@ vtgs_status vtgs_keyframe_pose_grad(vtgs_ctx *ctx, const float *pos_rad, const f
     return e ? cuda_fail(ctx, e, "vtgs_keyframe_pose_grad") : VTGS_OK;
 }
 
+vtgs_status vtgs_ssim_loss(vtgs_ctx *ctx, const float *color, const float *target_rgb, int32_t width,
+                           int32_t height, float tau, float *d_color, float *loss_out, void *stream) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    c.last_error[0] = 0;
+    if (!color || !target_rgb) return fail(ctx, VTGS_ERR_INVALID_ARG, "NULL color / target_rgb");
+    if (width < 11 || height < 11)
+        return fail(ctx, VTGS_ERR_SHAPE, "SSIM needs an image of at least 11×11 (the window), got %d×%d", width,
+                    height);
+    if (width > c.max_w || height > c.max_h)
+        return fail(ctx, VTGS_ERR_CAPACITY, "image %d×%d exceeds the context's %d×%d", width, height, c.max_w,
+                    c.max_h);
+    cudaSetDevice(c.device);
+    cudaError_t e = vtgs::launch_ssim(c, color, target_rgb, width, height, tau, d_color, loss_out, (cudaStream_t)stream);
+    return e ? cuda_fail(ctx, e, "vtgs_ssim_loss") : VTGS_OK;
+}
+
 vtgs_status vtgs_pose_adam_step(vtgs_ctx *ctx, vtgs_pose *pose, const float *d_pose, float *adam_state,
                                 float lr_rot, float lr_trans, void *stream) {
     if (!ctx) return VTGS_ERR_INVALID_ARG;
@@ -385,7 +405,7 @@ vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col
     if (e) return cuda_fail(ctx, e, "vtgs_step_host (H2D)");
     st = vtgs_render_fwd(ctx, pos_rad, col_opa, N, d_view, intr, color, depth, silhouette, stream);
     if (st) return st;
-    vtgs_l1_loss L{d_rgb, d_dep, nullptr, w_color, w_depth, color_mask_mode, depth_mask_mode, normalize};
+    vtgs_l1_loss L{d_rgb, d_dep, nullptr, w_color, w_depth, color_mask_mode, depth_mask_mode, normalize, nullptr};
     st = vtgs_render_bwd(ctx, nullptr, nullptr, nullptr, &L, want & ~(uint32_t)VTGS_GRAD_POSITION, learn_begin,
                          learn_end, d_col_opa, d_radius, nullptr, (want & VTGS_GRAD_POSE) ? d_dpose : nullptr, d_loss,
                          stream);

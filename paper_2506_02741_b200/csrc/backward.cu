@@ -32,6 +32,7 @@ struct BwdArgs {
     const float *dC, *dD, *dS;
     const float *tC, *tD;
     const uint8_t *vis;
+    const float *extra_dc;
     float wc, wd;
     int cmode, dmode, normalize;
     const DevScalars *dev;
@@ -81,6 +82,9 @@ __device__ __forceinline__ PixelUp pixel_upstream(const BwdArgs &p, int px, int 
             const float k = p.wc * sc;
             u.g0 = k * sgnf(e0); u.g1 = k * sgnf(e1); u.g2 = k * sgnf(e2);
             u.lossv += (double)k * ((double)fabsf(e0) + (double)fabsf(e1) + (double)fabsf(e2));
+        }
+        if (p.extra_dc) {   // e.g. the SSIM term of Eq. 2 (vtgs_ssim_loss)
+            u.g0 += p.extra_dc[3 * pix]; u.g1 += p.extra_dc[3 * pix + 1]; u.g2 += p.extra_dc[3 * pix + 2];
         }
         if (md) {
             const float e = p.depth[pix] - tDv;
@@ -462,7 +466,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     a.d_col_opa = d_col_opa; a.d_radius = d_radius; a.d_position = d_position; a.partials = c.partials;
     const bool L = loss != nullptr;
     if (L) {
-        a.tC = loss->target_rgb; a.tD = loss->target_depth; a.vis = loss->vis_mask;
+        a.tC = loss->target_rgb; a.tD = loss->target_depth; a.vis = loss->vis_mask; a.extra_dc = loss->extra_dcolor;
         a.wc = loss->w_color; a.wd = loss->w_depth;
         a.cmode = loss->color_mask_mode; a.dmode = loss->depth_mask_mode; a.normalize = loss->normalize;
         if (a.normalize) {

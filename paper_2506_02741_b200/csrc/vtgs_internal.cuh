@@ -40,7 +40,7 @@ struct DevScalars {
 };
 
 enum Stage { kProject = 0, kScan, kEmit, kSort, kCompFwd, kL1Count, kCompBwd, kFinalize, kInstantiate,
-             kPoseAdam, kKfPose, kNumStages };
+             kPoseAdam, kKfPose, kSsim, kNumStages };
 
 struct ProfEvent {
     int stage;
@@ -73,6 +73,8 @@ struct Ctx {
     float *T_final = nullptr;        // per pixel
     uint32_t *last = nullptr;        // per pixel: 1 + sub-list position of the last composited entry
     double *partials = nullptr;      // per sub-tile warp: 12 pose accumulators + loss + pad (16)
+    float *ssim_abc = nullptr;       // SSIM chain factors a, b, c × 3 channels per pixel [9 · px]
+    double *ssim_partials = nullptr; // per-CTA Σ SSIM
     DevScalars *dev = nullptr;
     float *host_io = nullptr;        // step_host device staging (targets + pose)
     vtgs_pose *view_copy = nullptr;  // the forward's view pose, copied on the device for the backward
@@ -214,6 +216,9 @@ cudaError_t launch_keyframe_pose_grad(Ctx &c, const float4 *pos_rad, const float
 cudaError_t forward_set_attributes();
 cudaError_t backward_set_attributes();
 cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s);
+cudaError_t ssim_set_constants();
+cudaError_t launch_ssim(Ctx &c, const float *color, const float *target, int W, int H, float tau, float *d_color,
+                        float *loss_out, cudaStream_t s);
 cudaError_t launch_pose_adam(Ctx &c, vtgs_pose *pose, const float *d_pose, float *state, float lr_rot,
                              float lr_trans, cudaStream_t s);
 

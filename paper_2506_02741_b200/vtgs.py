@@ -46,7 +46,7 @@ class vtgs_pose(ctypes.Structure):
 class vtgs_l1_loss(ctypes.Structure):
     _fields_ = [("target_rgb", ctypes.c_void_p), ("target_depth", ctypes.c_void_p), ("vis_mask", ctypes.c_void_p),
                 ("w_color", ctypes.c_float), ("w_depth", ctypes.c_float), ("color_mask_mode", ctypes.c_int32),
-                ("depth_mask_mode", ctypes.c_int32), ("normalize", ctypes.c_int32)]
+                ("depth_mask_mode", ctypes.c_int32), ("normalize", ctypes.c_int32), ("extra_dcolor", ctypes.c_void_p)]
 
 
 class vtgs_stats(ctypes.Structure):
@@ -67,6 +67,7 @@ _SIGS = {
     "vtgs_render_fwd": (_c.c_int32, [_P, _P, _P, _c.c_int64, _P, vtgs_intrinsics, _P, _P, _P, _P]),
     "vtgs_render_bwd": (_c.c_int32, [_P, _P, _P, _P, _c.POINTER(vtgs_l1_loss), _c.c_uint32, _c.c_int64, _c.c_int64,
                                      _P, _P, _P, _P, _P, _P]),
+    "vtgs_ssim_loss": (_c.c_int32, [_P, _P, _P, _c.c_int32, _c.c_int32, _c.c_float, _P, _P, _P]),
     "vtgs_keyframe_pose_grad": (_c.c_int32, [_P, _P, _P, _P, _c.c_int32, _c.c_int64, _P, _P]),
     "vtgs_pose_adam_step": (_c.c_int32, [_P, _P, _P, _P, _c.c_float, _c.c_float, _P]),
     "vtgs_get_stats": (_c.c_int32, [_P, _c.POINTER(vtgs_stats), _P]),
@@ -180,11 +181,18 @@ class Renderer:
             L = vtgs_l1_loss(_ptr(loss["target_rgb"]), _ptr(loss["target_depth"]), _ptr(loss.get("vis_mask")),
                              float(loss.get("w_color", 1.0)), float(loss.get("w_depth", 1.0)),
                              int(loss.get("color_mask_mode", 0)), int(loss.get("depth_mask_mode", 0)),
-                             int(loss.get("normalize", 0)))
+                             int(loss.get("normalize", 0)), _ptr(loss.get("extra_dcolor")))
             lp = ctypes.byref(L)
         _ok(vtgs_render_bwd(self.ctx, _ptr(dL_dcolor), _ptr(dL_ddepth), _ptr(dL_dsil), lp, int(want), int(learn[0]),
                             int(learn[1]), _ptr(d_col_opa), _ptr(d_radius), _ptr(d_position), _ptr(d_pose),
                             _ptr(loss_out), _stream(stream)), self.ctx)
+
+    def ssim_loss(self, color: torch.Tensor, target_rgb: torch.Tensor, tau: float = 0.2, d_color=None,
+                  loss_out=None, stream=None):
+        """SSIM term τ·L_S of Eq. 2: d_color += dL/dcolor, loss_out = τ·L_S."""
+        H, W = color.shape[0], color.shape[1]
+        _ok(vtgs_ssim_loss(self.ctx, _ptr(color), _ptr(target_rgb), int(W), int(H), float(tau), _ptr(d_color),
+                           _ptr(loss_out), _stream(stream)), self.ctx)
 
     def keyframe_pose_grad(self, pos_rad: torch.Tensor, d_position: torch.Tensor, kf_poses: torch.Tensor,
                            slots_per_kf: int, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
@@ -210,7 +218,7 @@ class Renderer:
         return d
 
     STAGES = ("project_count", "scan_tiles", "emit_pairs", "tile_sort", "composite_fwd", "l1_count",
-              "composite_bwd", "pose_finalize", "instantiate", "pose_adam", "keyframe_pose_grad")
+              "composite_bwd", "pose_finalize", "instantiate", "pose_adam", "keyframe_pose_grad", "ssim")
 
     def set_profiling(self, enable: bool):
         _ok(vtgs_set_profiling(self.ctx, int(bool(enable))), self.ctx)

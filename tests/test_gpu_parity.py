@@ -592,3 +592,67 @@ def test_view_tied_pose_invariance_gpu(vt):
     s = dpose.abs().max().item()
     assert s > 1e-2
     assert (dpose + kf).abs().max().item() <= 2e-3 * s, (dpose.cpu().numpy(), kf.cpu().numpy())
+
+
+# ------------------------------------------------------------------------------ f2 (SSIM of Eq. 2)
+@pytest.mark.parametrize("size", [(64, 48), (37, 29), (11, 11)])
+def test_ssim_loss_parity(vt, size):
+    """τ·L_S of Eq. 2 (R24) and its gradient against the oracle's plain
+    121-tap window definition: loss within 1e-5 relative; gradient within 1e-3 relative or 1e-5
+    absolute (the north_star gradient bar) elementwise, including the ragged borders."""
+    W, H = size
+    rng = np.random.default_rng(W * H)
+    x = rng.uniform(size=(H, W, 3)).astype(np.float32)
+    y = np.clip(x + rng.normal(0, 0.1, size=x.shape), 0, 1).astype(np.float32)
+    R = vt.Renderer(0, 16, W, H)
+    d = torch.zeros((H, W, 3), device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    R.ssim_loss(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), 0.2, d_color=d, loss_out=loss)
+    torch.cuda.synchronize()
+    ref_loss, ref_g = oracle.ssim_loss(x, y, 0.2)
+    assert abs(loss.item() - ref_loss) <= 1e-5 * abs(ref_loss)
+    g = d.cpu().numpy().astype(np.float64)
+    ok = close(g, ref_g)
+    assert ok.all(), report("ssim grad", ok, g, ref_g)
+
+
+def test_ssim_errors_and_accumulate(vt):
+    R = vt.Renderer(0, 16, 64, 48)
+    x = torch.rand((10, 12, 3), device="cuda")
+    with pytest.raises(vt.VtgsError):
+        R.ssim_loss(x, x)                       # smaller than the 11×11 window
+    x = torch.rand((48, 64, 3), device="cuda")
+    y = torch.rand((48, 64, 3), device="cuda")
+    d1 = torch.zeros_like(x)
+    R.ssim_loss(x, y, 0.2, d_color=d1)
+    d2 = d1.clone()
+    R.ssim_loss(x, y, 0.2, d_color=d2)          # accumulates
+    torch.cuda.synchronize()
+    assert torch.allclose(d2, 2 * d1, rtol=1e-6, atol=0)
+
+
+def test_mapping_objective_with_ssim_parity(vt):
+    """The full mapping objective of Eq. 2, ρ‖V − V'‖₁ + τ L_S + σ U‖D − D'‖₁ (ρ, τ, σ = 0.8, 0.2,
+    1.0), on config 1: SSIM gradient from vtgs_ssim_loss passed as the fused loss's
+    extra colour upstream; colour / opacity / radius gradients against the oracle."""
+    cfg = cached_config(1)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    _, out = _render_gpu(vt, R, cfg, pr, co)
+    tg = cfg.targets[0]
+    H, W = cfg.intr.height, cfg.intr.width
+    trgb = torch.from_numpy(tg.rgb).cuda()
+    dss = torch.zeros((H, W, 3), device="cuda")
+    R.ssim_loss(out[0], trgb, 0.2, d_color=dss)
+    L = dict(target_rgb=trgb, target_depth=torch.from_numpy(tg.depth).cuda(), w_color=0.8, w_depth=1.0,
+             extra_dcolor=dss)
+    want = vt.VTGS_GRAD_ATTR
+    dco, drad, dpose = _run_bwd(vt, R, cfg, want, cfg.n_slots, loss=L)
+    opr, oco = oracle_instantiate(cfg)
+    v = _view(cfg)
+    img = oracle.render(opr, oco, v, cfg.intr)
+    _, gC, gD, gS, lflags = oracle.l1_upstream(img["color"], img["depth"], img["sil"], tg.rgb, tg.depth, None,
+                                               0.8, 1.0, 0, 0, 0)
+    _, gss = oracle.ssim_loss(img["color"], tg.rgb, 0.2)
+    ref, g = _oracle_grads(cfg, opr, oco, v, gC + gss, gD, gS, extra_flags=lflags)
+    _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt)

@@ -579,3 +579,48 @@ def test_view_tied_pose_invariance():
     scale = np.abs(g["d_pose"]).max()
     assert scale > 1e-3
     np.testing.assert_allclose(g["d_pose"] + kf, 0.0, atol=1e-8 * max(scale, 1.0))
+
+
+# ------------------------------------------------------------------------------ f2 (SSIM of Eq. 2)
+def test_ssim_identity_and_symmetry():
+    """L_S(x, x) = 0 with zero gradient (SSIM's maximum, S:265 "a = b → SSIM 1, L_S 0");
+    SSIM is symmetric in its arguments; τ scales value and gradient (linearity in weights)."""
+    rng = np.random.default_rng(0)
+    x, y = rng.uniform(size=(14, 17, 3)), rng.uniform(size=(14, 17, 3))
+    l0, g0 = oracle.ssim_loss(x, x, tau=0.2)
+    assert l0 == 0.0 and np.abs(g0).max() < 1e-15
+    a, _ = oracle.ssim_loss(x, y, tau=0.2)
+    b, _ = oracle.ssim_loss(y, x, tau=0.2)
+    assert a > 0 and abs(a - b) < 1e-14
+    c, gc = oracle.ssim_loss(x, y, tau=0.4)
+    _, ga = oracle.ssim_loss(x, y, tau=0.2)
+    assert abs(c - 2 * a) < 1e-14 and np.allclose(gc, 2 * ga, rtol=0, atol=1e-15)
+
+
+def test_ssim_constant_images_closed_form():
+    """Constant images a, b: at pixels whose 11×11 window lies inside the image the window
+    weights sum to 1 and both variances vanish, so SSIM = (2ab + C1)/(a² + b² + C1)
+    (S:266 "a constant 0, b constant 1 → C1/(1 + C1)")."""
+    H, W = 16, 18
+    for a, b in ((0.0, 1.0), (0.3, 0.7), (0.5, 0.5)):
+        _, _, smap = oracle.ssim_loss(np.full((H, W, 3), a), np.full((H, W, 3), b), want_map=True)
+        C1 = 0.01 ** 2
+        ref = (2 * a * b + C1) / (a * a + b * b + C1)
+        np.testing.assert_allclose(smap[5:H - 5, 5:W - 5], ref, rtol=1e-12)
+
+
+def test_ssim_gradient_central_differences():
+    """Gradient of τ·L_S w.r.t. the render against central differences (fp64, ε = 1e-6) at
+    every pixel of a 12×13 image."""
+    rng = np.random.default_rng(1)
+    x, y = rng.uniform(size=(12, 13, 3)), rng.uniform(size=(12, 13, 3))
+    _, g = oracle.ssim_loss(x, y, tau=0.2)
+    eps = 1e-6
+    worst = 0.0
+    for idx in np.ndindex(*x.shape):
+        xp, xm = x.copy(), x.copy()
+        xp[idx] += eps
+        xm[idx] -= eps
+        fd = (oracle.ssim_loss(xp, y)[0] - oracle.ssim_loss(xm, y)[0]) / (2 * eps)
+        worst = max(worst, abs(fd - g[idx]) / max(abs(g[idx]), 1e-6))
+    assert worst < 1e-5
