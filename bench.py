@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no clocks / cpu baseline)")
+    ap.add_argument("--ssim", type=float, default=0.0,
+                    help="add Eq. 2's SSIM term with this weight tau (0.2 in the paper) to the mapping step")
     return ap.parse_args()
 
 
@@ -195,7 +197,8 @@ def workload_config(cfg, args, n_views=1, views_per_rank=1):
     return {"workload": f"config{args.config}_{cfg.name}_{cfg.intr.width}x{cfg.intr.height}_K{cfg.K}",
             "n_gaussians": cfg.n_slots, "image": [cfg.intr.width, cfg.intr.height], "views_per_step": n_views,
             "views_per_rank": views_per_rank,
-            "loss": f"{cfg.loss_weights[0]}*L1(C) + {cfg.loss_weights[1]}*U*L1(D), sum form",
+            "loss": f"{cfg.loss_weights[0]}*L1(C) + {cfg.loss_weights[1]}*U*L1(D)"
+                    + (f" + {args.ssim}*L_S(C)" if getattr(args, "ssim", 0.0) > 0 else "") + ", sum form",
             "grads": "colour, opacity, radius", "seed": args.seed,
             "l2": "flushed between timed steps (256 MiB write outside the step events)",
             "parallelism": f"dp{args.gpus} (view-sharded mapping, one NCCL all-reduce of the 5N fp32 gradient buffer per step)"}
@@ -350,7 +353,7 @@ def main():
     wc, wd = cfg.loss_weights
     mapper = BatchedMapper(R, pr, co, cfg.intr, [vtgs.pose_tensor(v, dev) for v in views_np],
                            [dict(rgb=torch.from_numpy(t.rgb).to(dev), depth=torch.from_numpy(t.depth).to(dev))
-                            for t in tgts], wc, wd)
+                            for t in tgts], wc, wd, w_ssim=args.ssim)
     grads = mapper.grads.flat
     d_co, d_r = mapper.grads.d_col_opa, mapper.grads.d_radius
     out = mapper.out
@@ -418,6 +421,7 @@ def main():
         "tile_sort": ("hbm", 12 * P),                                # (key, gid) in, gid out
         "composite_fwd": ("alu", FLOPS_PER_EVAL_FWD * stats["e_eval"]),
         "composite_bwd": ("alu", FLOPS_PER_COMP_BWD * stats["e_comp"]),
+        "ssim": ("hbm", 36 * HW / 3),                                # per launch (3 launches / view): x, y in, dL/dx out
     }
     stage_json = {}
     for k, (ms_k, cnt) in prof.items():

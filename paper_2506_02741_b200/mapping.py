@@ -54,11 +54,13 @@ def allreduce_grads(buf: GradBuffer, group: Optional[dist.ProcessGroup] = None) 
 
 
 class BatchedMapper:
-    """Per-rank driver of one mapping step over a shard of views (fused masked-L1 of Eq. 2)."""
+    """Per-rank driver of one mapping step over a shard of views: the fused masked-L1 terms of
+    Eq. 2, plus its SSIM term τ·L_S when `w_ssim` = τ > 0 (τ = 0.2 at P:262)."""
 
     def __init__(self, renderer, pos_rad: torch.Tensor, col_opa: torch.Tensor, intr,
                  views: Sequence[torch.Tensor], targets: Sequence[dict], w_color: float, w_depth: float,
-                 learn: Sequence[int] = (0, 1 << 62), group: Optional[dist.ProcessGroup] = None):
+                 learn: Sequence[int] = (0, 1 << 62), group: Optional[dist.ProcessGroup] = None,
+                 w_ssim: float = 0.0):
         from . import vtgs
         self.vt = vtgs
         self.R = renderer
@@ -75,15 +77,23 @@ class BatchedMapper:
         self.out = (torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev),
                     torch.empty((H, W), device=dev))
         self.loss = torch.zeros(max(len(self.views), 1), device=dev)
+        self.w_ssim = float(w_ssim)
+        self.ssim_loss = torch.zeros(max(len(self.views), 1), device=dev)
+        self.d_ssim = torch.zeros((H, W, 3), device=dev) if self.w_ssim > 0 else None
 
     def step(self, allreduce: bool = True) -> GradBuffer:
         """Zero the gradients, render + backprop every local view (accumulating), all-reduce."""
         self.grads.zero_()
         for i, (v, t) in enumerate(zip(self.views, self.targets)):
             self.R.render_fwd(self.pos_rad, self.col_opa, v, self.intr, out=self.out)
+            if self.d_ssim is not None:
+                self.d_ssim.zero_()
+                self.R.ssim_loss(self.out[0], t["rgb"], self.w_ssim, d_color=self.d_ssim,
+                                 loss_out=self.ssim_loss[i:i + 1])
             self.R.render_bwd(self.vt.VTGS_GRAD_ATTR, d_col_opa=self.grads.d_col_opa, d_radius=self.grads.d_radius,
                               loss=dict(target_rgb=t["rgb"], target_depth=t["depth"], w_color=self.w_color,
-                                        w_depth=self.w_depth), learn=self.learn, loss_out=self.loss[i:i + 1])
+                                        w_depth=self.w_depth, extra_dcolor=self.d_ssim),
+                              learn=self.learn, loss_out=self.loss[i:i + 1])
         if allreduce:
             allreduce_grads(self.grads, self.group)
         return self.grads
