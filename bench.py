@@ -368,8 +368,9 @@ def main():
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
-    st = R.stats()
+    st = R.stats()                                         # work counters of the (identical) warm-up steps
     assert st["overflow"] == 0, "tile-pair capacity exceeded"
+    R.set_work_counters(False)                             # diagnostics only: off in the timed region
 
     # ---------------- timed region
     R.set_profiling(True)
@@ -406,7 +407,7 @@ def main():
     gps = n_views_total * N / (ms_max * 1e-3)
 
     # ---------------- roofline of the dominant kernel (event-timed inside the timed region)
-    stats = R.stats()
+    stats = dict(R.stats(), e_eval=st["e_eval"], e_comp=st["e_comp"])
     peaks, peak_src = load_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     fp32_peak = SM_COUNT * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12       # TFLOP/s at max clock

@@ -210,6 +210,9 @@ typedef struct vtgs_stats {
     int64_t launches;    /* kernels this context has launched since it was created */
 } vtgs_stats;
 VTGS_API vtgs_status vtgs_get_stats(vtgs_ctx *ctx, vtgs_stats *out /* host */, void *stream);
+/* The forward's e_eval / e_comp counters cost a few instructions per evaluation; they are on by
+ * default and can be switched off (then both read 0; n_pairs / max_tile are always kept). */
+VTGS_API vtgs_status vtgs_set_work_counters(vtgs_ctx *ctx, int32_t enable);
 
 /* Per-kernel device timing (CUDA events recorded on the launching stream around every kernel
  * while enabled; not for use inside CUDA-graph capture).  Stages, in order:

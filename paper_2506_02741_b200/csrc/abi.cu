@@ -318,6 +318,12 @@ vtgs_status vtgs_get_stats(vtgs_ctx *ctx, vtgs_stats *out, void *stream) {
                       : VTGS_OK;
 }
 
+vtgs_status vtgs_set_work_counters(vtgs_ctx *ctx, int32_t enable) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    ctx->c.count_work = enable != 0;
+    return VTGS_OK;
+}
+
 vtgs_status vtgs_set_profiling(vtgs_ctx *ctx, int32_t enable) {
     if (!ctx) return VTGS_ERR_INVALID_ARG;
     ctx->c.profiling = enable != 0;

@@ -134,7 +134,7 @@ struct FwdRing {
     uint32_t bits[R * 32];
 };
 
-template <int R>
+template <int R, bool STATS>
 __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p) {
     extern __shared__ float4 fwd_smem[];
     static_assert((R & (R - 1)) == 0, "ring depth must be a power of two");
@@ -180,56 +180,64 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
 
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f, Sl = 0.f;
     uint32_t lastc = 0, ne = 0, nc = 0;
-    // lane state: batch b, its remaining candidate bits cur.  Finished (terminated, walked the
-    // whole list, or outside the image) ⇔ cur == 0 && b + 1 ≥ nb.
+    // lane state: batch b, its remaining candidate bits cur (bit 31 − j = entry j, so the lowest
+    // remaining entry is the highest set bit, one FLO), the address of the batch's entry 31 and
+    // 1 + the sub-list position of its entry 31.  Finished (terminated, walked the whole list,
+    // or outside the image) ⇔ cur == 0 && b + 1 ≥ nb.
     int b = inside ? -1 : nb;
     unsigned cur = 0u;
+    const float4 *abase = ring.A;
+    int lbase = 0;
+    auto advance = [&]() {
+        ++b;
+        cur = ring.bits[(b & (R - 1)) * 32 + lane];
+        abase = ring.A + (b & (R - 1)) * 32 + 31;
+        lbase = b * 32 + 32;
+    };
     for (;;) {
         // a few lane-independent steps between warp-level checks (a blocked lane idles ≤ kInner);
         // branch-free body: every lane runs the same predicated instructions
 #pragma unroll
         for (int it = 0; it < kInner; ++it) {
-            if (cur == 0u && b + 1 < built) {
-                ++b;
-                cur = ring.bits[(b & (R - 1)) * 32 + lane];
-            }
+            if (cur == 0u && b + 1 < built) advance();
             const bool has = cur != 0u;
-            const int k = __clz(cur);                      // lowest remaining entry (bit-reversed)
-            cur &= ~(0x80000000u >> (k & 31));
-            const int e = ((b & (R - 1)) << 5) | (k & 31);
-            float4 A = make_float4(0.f, 0.f, -1.f, 0.f), Bc = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (has) {
-                A = ring.A[e];
-                Bc = ring.B[e];
+            const int hb = 31 - __clz(cur);                // highest set bit = lowest remaining entry
+            cur &= ~(1u << (hb & 31));
+            const float4 *ap = abase - hb;                 // entry 31 − hb
+            float4 A, Bc;                                  // unused unless `has` (elig includes it)
+            if (has) {   // predicated loads: idle lanes add no shared-memory traffic
+                A = ap[0];
+                Bc = ap[R * 32];
             }
             const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
             const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-            const bool elig = d2 <= A.z;                   // false when !has (A.z = −1)
+            const bool elig = has && d2 <= A.z;
             const float a = fminf(__fmul_rn(A.w, fast_exp2(d2 * (kExpScale9 * rcp_approx(A.z)))), kAlphaMax);
             const bool comp = elig && a >= 1.0f / 255.0f;
             const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
             const bool term = comp && Tn < kTMin;
             const bool acc = comp && !term;
-            const float om = acc ? a * T : 0.0f;
-            C0 = fmaf(Bc.x, om, C0);
-            C1 = fmaf(Bc.y, om, C1);
-            C2 = fmaf(Bc.z, om, C2);
-            D = fmaf(Bc.w, om, D);
-            Sl += om;
-            T = acc ? Tn : T;
-            lastc = acc ? (uint32_t)(b * 32 + k + 1) : lastc;
-            ne += elig ? 1u : 0u;
-            nc += acc ? 1u : 0u;
+            const float om = a * T;
+            if (acc) {   // predicated: Bc is garbage for lanes without a candidate
+                C0 = fmaf(Bc.x, om, C0);
+                C1 = fmaf(Bc.y, om, C1);
+                C2 = fmaf(Bc.z, om, C2);
+                D = fmaf(Bc.w, om, D);
+                Sl += om;
+                T = Tn;
+                lastc = (uint32_t)(lbase - hb);
+            }
+            if (STATS) {
+                ne += elig ? 1u : 0u;
+                nc += acc ? 1u : 0u;
+            }
             if (term) {
                 cur = 0u;
                 b = nb;
             }
         }
         // lanes whose next word was empty: catch up before the warp-level check
-        while (cur == 0u && b + 1 < built) {
-            ++b;
-            cur = ring.bits[(b & (R - 1)) * 32 + lane];
-        }
+        while (cur == 0u && b + 1 < built) advance();
         const bool live = cur != 0u || b + 1 < nb;
         if (!__any_sync(kFullMask, live)) break;
         const bool blocked = cur == 0u && b + 1 < nb && b + 1 >= built;
@@ -252,15 +260,17 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
         p.T_final[pix] = T;
         p.last[pix] = lastc;
     }
-    unsigned long long a = ne, bsum = nc;
+    if (STATS) {
+        unsigned long long a = ne, bsum = nc;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(kFullMask, a, o);
-        bsum += __shfl_xor_sync(kFullMask, bsum, o);
-    }
-    if (lane == 0 && (a | bsum)) {
-        atomicAdd(&p.dev->e_eval, a);
-        atomicAdd(&p.dev->e_comp, bsum);
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(kFullMask, a, o);
+            bsum += __shfl_xor_sync(kFullMask, bsum, o);
+        }
+        if (lane == 0 && (a | bsum)) {
+            atomicAdd(&p.dev->e_eval, a);
+            atomicAdd(&p.dev->e_comp, bsum);
+        }
     }
 }
 
@@ -273,13 +283,19 @@ static int fwd_variant() {
     return v;
 }
 
-template <int R>
-static cudaError_t launch_ring(const FwdArgs &a, int T, cudaStream_t s) {
+template <int R, bool STATS>
+static cudaError_t launch_ring_s(const FwdArgs &a, int T, cudaStream_t s) {
     const size_t sm = sizeof(FwdRing<R>) * kFwdWarps;
-    cudaError_t e = cudaFuncSetAttribute(k_composite_fwd_ring<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_composite_fwd_ring<R, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
-    k_composite_fwd_ring<R><<<T * 8 / kFwdWarps, kFwdWarps * 32, sm, s>>>(a);
+    k_composite_fwd_ring<R, STATS><<<T * 8 / kFwdWarps, kFwdWarps * 32, sm, s>>>(a);
     return cudaGetLastError();
+}
+
+template <int R>
+static cudaError_t launch_ring(const FwdArgs &a, int T, bool stats, cudaStream_t s) {
+    return stats ? launch_ring_s<R, true>(a, T, s) : launch_ring_s<R, false>(a, T, s);
 }
 
 cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
@@ -291,10 +307,9 @@ cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
         case 0:
             k_composite_fwd<<<ntx * nty * 8 / kFwdWarps, kFwdWarps * 32, 0, s>>>(a);
             return cudaGetLastError();
-        case 4: return launch_ring<4>(a, ntx * nty, s);
-        case 8: return launch_ring<8>(a, ntx * nty, s);
-        case 32: return launch_ring<32>(a, ntx * nty, s);
-        default: return launch_ring<16>(a, ntx * nty, s);
+        case 8: return launch_ring<8>(a, ntx * nty, c.count_work, s);
+        case 16: return launch_ring<16>(a, ntx * nty, c.count_work, s);
+        default: return launch_ring<4>(a, ntx * nty, c.count_work, s);
     }
 }
 

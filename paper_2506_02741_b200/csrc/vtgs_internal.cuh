@@ -90,6 +90,7 @@ struct Ctx {
     // launch accounting / optional per-stage event timing
     int64_t launches = 0;
     bool profiling = false;
+    bool count_work = true;           // forward work counters e_eval / e_comp (vtgs_set_work_counters)
     std::vector<ProfEvent> prof;      // recorded since the last vtgs_get_profile
     std::vector<ProfEvent> prof_free; // reusable event pairs
     int64_t prof_counts[kNumStages] = {0};

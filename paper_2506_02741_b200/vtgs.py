@@ -73,6 +73,7 @@ _SIGS = {
     "vtgs_get_stats": (_c.c_int32, [_P, _c.POINTER(vtgs_stats), _P]),
     "vtgs_check": (_c.c_int32, [_P, _P]),
     "vtgs_set_profiling": (_c.c_int32, [_P, _c.c_int32]),
+    "vtgs_set_work_counters": (_c.c_int32, [_P, _c.c_int32]),
     "vtgs_get_profile": (_c.c_int32, [_P, _P, _P, _P]),
     "vtgs_export_tiles": (_c.c_int32, [_P, _P, _P, _c.c_int64, _c.POINTER(_c.c_int64), _P]),
     "vtgs_step_host": (_c.c_int32, [_P, _P, _P, _c.c_int64, _P, vtgs_intrinsics, _P, _P, _c.c_float, _c.c_float,
@@ -219,6 +220,9 @@ class Renderer:
 
     STAGES = ("project_count", "scan_tiles", "emit_pairs", "tile_sort", "composite_fwd", "l1_count",
               "composite_bwd", "pose_finalize", "instantiate", "pose_adam", "keyframe_pose_grad", "ssim")
+
+    def set_work_counters(self, enable: bool):
+        _ok(vtgs_set_work_counters(self.ctx, int(bool(enable))), self.ctx)
 
     def set_profiling(self, enable: bool):
         _ok(vtgs_set_profiling(self.ctx, int(bool(enable))), self.ctx)
