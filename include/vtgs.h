@@ -103,6 +103,21 @@ VTGS_API vtgs_status vtgs_instantiate(vtgs_ctx *ctx, const float *depth, const f
                              const float *opacity_init, float opacity_default, float *pos_rad,
                              float *col_opa, void *stream);
 
+/* Densification on a regular frame — PAPER.md:192 ("complement Gaussians at pixels uncovered by
+ * the current Gaussians' renderings"), PAPER.md:261 ("0.5 as a mask threshold to determine if
+ * current Gaussians ... cover a pixel").  A new Gaussian at every pixel with
+ * valid depth (> 0, finite) and silhouette < threshold (strict), initialised exactly as
+ * vtgs_instantiate does, appended in row-major pixel order (deterministic).
+ *   depth [H×W], rgb [H×W×3], pose (device vtgs_pose of the frame), silhouette [H×W] (the
+ *   section rendered from that pose by vtgs_render_fwd), opacity [H×W] or NULL (→ default).
+ *   pos_rad_out / col_opa_out float4 (device, capacity H×W, e.g. the section's arrays + N):
+ *   the first *n_new rows are written; n_new: device int64, OVERWRITTEN.
+ * Asynchronous on `stream` (read n_new after synchronising). */
+VTGS_API vtgs_status vtgs_densify(vtgs_ctx *ctx, const float *depth, const float *rgb, const vtgs_pose *pose,
+                         vtgs_intrinsics intr, const float *silhouette, float threshold, const float *opacity,
+                         float opacity_default, float *pos_rad_out, float *col_opa_out, int64_t *n_new,
+                         void *stream);
+
 /* (2)–(4) Forward render of N Gaussians from `view` — PAPER.md:146 (Eq. 1 `splat`),
  * PAPER.md:192 (Eq. 2 multi-set render: concatenate the sets, pass the union).
  *   projection: X_c = Rᵀ(X_w − t), culled if r ≤ 0 or z ≤ 0.01 m; σ = max(f_mean·r/z, 0.3) px;
@@ -217,8 +232,9 @@ VTGS_API vtgs_status vtgs_set_work_counters(vtgs_ctx *ctx, int32_t enable);
 /* Per-kernel device timing (CUDA events recorded on the launching stream around every kernel
  * while enabled; not for use inside CUDA-graph capture).  Stages, in order:
  *   0 project_count, 1 scan_tiles, 2 emit_pairs, 3 tile_sort, 4 composite_fwd, 5 l1_count,
- *   6 composite_bwd, 7 pose_finalize, 8 instantiate, 9 pose_adam, 10 keyframe_pose_grad, 11 ssim. */
-#define VTGS_NUM_STAGES 12
+ *   6 composite_bwd, 7 pose_finalize, 8 instantiate, 9 pose_adam, 10 keyframe_pose_grad, 11 ssim,
+ *   12 densify. */
+#define VTGS_NUM_STAGES 13
 VTGS_API vtgs_status vtgs_set_profiling(vtgs_ctx *ctx, int32_t enable);
 /* Synchronous: sum of event-timed milliseconds (ms[VTGS_NUM_STAGES], host) and launch counts
  * (counts[VTGS_NUM_STAGES], host, may be NULL) per stage since the previous call; resets. */

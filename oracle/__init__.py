@@ -66,6 +66,9 @@ def _load():
             f = getattr(lib, f"or_keyframe_pose_grad_{m}")
             f.restype = None
             f.argtypes = [_D, _D, ctypes.c_int, _D, ctypes.c_int, ctypes.c_int, _D, _D]
+        f = lib.or_densify_f32
+        f.restype = ctypes.c_int64
+        f.argtypes = [_D, _D, _D, _D, ctypes.c_int, ctypes.c_int, _D, ctypes.c_double, _D, ctypes.c_double, _D, _D]
         f = lib.or_ssim_loss
         f.restype = ctypes.c_double
         f.argtypes = [_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_double, _D, _D]
@@ -237,3 +240,18 @@ def ssim_loss(render_rgb, target_rgb, tau=0.2, want_map=False):
     smap = np.zeros((H, W, 3)) if want_map else None
     loss = lib.or_ssim_loss(_p(x), _p(y), W, H, float(tau), _p(grad), _p(smap))
     return (loss, grad, smap) if want_map else (loss, grad)
+
+
+def densify(depth, rgb, pose, intr, sil, threshold=0.5, opacity=None, opacity_default=0.5):
+    """Regular-frame densification: new Gaussians at valid pixels with S < threshold,
+    row-major → (pos_rad [M,4], col_opa [M,4])."""
+    lib = _load()
+    depth = _d(depth)
+    H, W = depth.shape
+    rgb, sil = _d(rgb), _d(sil)
+    opa = None if opacity is None else _d(opacity)
+    pr = np.zeros((H * W, 4))
+    co = np.zeros((H * W, 4))
+    n = lib.or_densify_f32(_p(depth), _p(rgb), _p(_d(pose)), _p(_intr(intr)), W, H, _p(sil), float(threshold), _p(opa),
+                           float(opacity_default), _p(pr), _p(co))
+    return pr[:n], co[:n]

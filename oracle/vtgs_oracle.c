@@ -15,6 +15,7 @@
  *   or_keyframe_pose_grad_*  head-frame bundle adjustment: keyframe poses
  *   or_l1_upstream          masked L1 terms of Eq. 1 / Eq. 2
  *   or_ssim_loss            SSIM term τ·L_S of Eq. 2 and its gradient
+ *   or_densify_f32          regular-frame densification (S < 0.5)
  * Two builds of the same source (oracle_impl.inc): *_f32 takes every decision in fp32 (the
  * kernel's precision) with fp64 values; *_f64 is fp64 throughout.
  *
@@ -179,4 +180,39 @@ double or_ssim_loss(const double *x, const double *y, int W, int H, double tau, 
     }
     free(dS);
     return tau * (1.0 - sum / n);
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Densification on a regular frame ("complement Gaussians at pixels uncovered by the
+ * current Gaussians' renderings"; "we will choose 0.5 as a mask threshold to determine if
+ * current Gaussians in S_k cover a pixel, if they do not, we will initialize a Gaussian as a
+ * complement").  A pixel gets a new Gaussian iff its depth is valid (> 0, finite)
+ * and the section's silhouette there is below the threshold (strict <).  The new Gaussians are
+ * initialised exactly as or_instantiate does and appended in row-major pixel
+ * order.  depth [H,W], rgb [H,W,3], pose [7], sil [H,W], opacity [H,W] or NULL; out pos_rad /
+ * col_opa [H·W,4] (the first `count` rows written).  Returns count.
+ * ------------------------------------------------------------------------------------- */
+int64_t or_densify_f32(const double *depth, const double *rgb, const double *pose, const double *intr, int W,
+                       int H, const double *sil, double threshold, const double *opacity,
+                       double opacity_default, double *pos_rad, double *col_opa)
+{
+    const int64_t npx = (int64_t)W * H;
+    double *pr = (double *)malloc(sizeof(double) * 4 * (size_t)npx);
+    double *co = (double *)malloc(sizeof(double) * 4 * (size_t)npx);
+    if (!pr || !co) return -1;
+    or_instantiate_f32(depth, rgb, pose, 1, intr, W, H, opacity, opacity_default, pr, co);
+    int64_t n = 0;
+    for (int64_t p = 0; p < npx; ++p) {
+        const double d = (double)(float)depth[p];
+        if (!(d > 0.0) || !isfinite(d)) continue;
+        if (!((float)sil[p] < (float)threshold)) continue;
+        for (int i = 0; i < 4; ++i) {
+            pos_rad[4 * n + i] = pr[4 * p + i];
+            col_opa[4 * n + i] = co[4 * p + i];
+        }
+        ++n;
+    }
+    free(pr);
+    free(co);
+    return n;
 }

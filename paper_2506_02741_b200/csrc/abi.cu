@@ -271,6 +271,25 @@ vtgs_status vtgs_keyframe_pose_grad(vtgs_ctx *ctx, const float *pos_rad, const f
     return e ? cuda_fail(ctx, e, "vtgs_keyframe_pose_grad") : VTGS_OK;
 }
 
+vtgs_status vtgs_densify(vtgs_ctx *ctx, const float *depth, const float *rgb, const vtgs_pose *pose,
+                         vtgs_intrinsics intr, const float *silhouette, float threshold, const float *opacity,
+                         float opacity_default, float *pos_rad_out, float *col_opa_out, int64_t *n_new,
+                         void *stream) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    c.last_error[0] = 0;
+    if (!depth || !rgb || !pose || !silhouette || !pos_rad_out || !col_opa_out || !n_new)
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "NULL argument to vtgs_densify");
+    vtgs_status st = check_intr(ctx, intr);
+    if (st) return st;
+    if (!aligned16(pos_rad_out) || !aligned16(col_opa_out))
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "pos_rad_out / col_opa_out must be 16-byte aligned float4 arrays");
+    cudaSetDevice(c.device);
+    cudaError_t e = vtgs::launch_densify(c, depth, rgb, pose, intr, silhouette, threshold, opacity, opacity_default,
+                                         (float4 *)pos_rad_out, (float4 *)col_opa_out, n_new, (cudaStream_t)stream);
+    return e ? cuda_fail(ctx, e, "vtgs_densify") : VTGS_OK;
+}
+
 vtgs_status vtgs_ssim_loss(vtgs_ctx *ctx, const float *color, const float *target_rgb, int32_t width,
                            int32_t height, float tau, float *d_color, float *loss_out, void *stream) {
     if (!ctx) return VTGS_ERR_INVALID_ARG;

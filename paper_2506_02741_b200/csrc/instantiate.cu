@@ -45,6 +45,100 @@ __global__ void __launch_bounds__(256) k_instantiate(const float *__restrict__ d
     }
 }
 
+// Densification on a regular frame: a new Gaussian at every
+// pixel with valid depth and silhouette < threshold, initialised as above, appended in row-major
+// order (deterministic).  Three passes: per-256-pixel counts, one-CTA scan, ranked write.
+__device__ __forceinline__ bool densify_sel(const float *depth, const float *sil, float thr, int p) {
+    const float d = depth[p];
+    return d > 0.0f && isfinite(d) && sil[p] < thr;
+}
+
+__global__ void __launch_bounds__(256) k_densify_count(const float *__restrict__ depth, const float *__restrict__ sil,
+                                                       float thr, int HW, uint32_t *__restrict__ counts) {
+    const int p = blockIdx.x * 256 + threadIdx.x;
+    const unsigned b = __ballot_sync(0xffffffffu, p < HW && densify_sel(depth, sil, thr, p));
+    __shared__ uint32_t w[8];
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = __popc(b);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int i = 0; i < 8; ++i) t += w[i];
+        counts[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_densify_scan(uint32_t *__restrict__ counts, int nblk,
+                                                       int64_t *__restrict__ n_new) {
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nblk; base += 1024) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < nblk ? counts[i] : 0u;
+        uint32_t incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((threadIdx.x & 31) >= o) incl += y;
+        }
+        if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = incl;
+        __syncthreads();
+        uint32_t pre = carry;
+        for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) pre += ws[w];
+        if (i < nblk) counts[i] = pre + incl - v;   // exclusive offsets
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = pre + incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_new = (int64_t)carry;
+}
+
+__global__ void __launch_bounds__(256) k_densify_write(const float *__restrict__ depth, const float *__restrict__ rgb,
+                                                       const vtgs_pose *__restrict__ pose, int HW, int W,
+                                                       vtgs_intrinsics in, const float *__restrict__ sil, float thr,
+                                                       const float *__restrict__ opacity, float opacity_default,
+                                                       const uint32_t *__restrict__ offsets,
+                                                       float4 *__restrict__ pos_rad, float4 *__restrict__ col_opa) {
+    __shared__ PoseR P;
+    __shared__ uint32_t w[8];
+    if (threadIdx.x == 0) pose_rotation(*pose, P);
+    const int p = blockIdx.x * 256 + threadIdx.x;
+    const bool sel = p < HW && densify_sel(depth, sil, thr, p);
+    const unsigned b = __ballot_sync(0xffffffffu, sel);
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = __popc(b);
+    __syncthreads();
+    if (!sel) return;
+    uint32_t r = offsets[blockIdx.x] + __popc(b & lanemask_lt());
+    for (int i = 0; i < (int)(threadIdx.x >> 5); ++i) r += w[i];
+    const float fmean = __fmul_rn(0.5f, __fadd_rn(in.fx, in.fy));
+    const float d = depth[p];
+    const int y = p / W, x = p - y * W;
+    const float X0 = __fdiv_rn(__fmul_rn(__fsub_rn((float)x, in.cx), d), in.fx);
+    const float X1 = __fdiv_rn(__fmul_rn(__fsub_rn((float)y, in.cy), d), in.fy);
+    float Xw[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        Xw[a] = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(P.R[3 * a], X0), __fmul_rn(P.R[3 * a + 1], X1)),
+                                    __fmul_rn(P.R[3 * a + 2], d)),
+                          P.t[a]);
+    pos_rad[r] = make_float4(Xw[0], Xw[1], Xw[2], __fdiv_rn(d, fmean));
+    col_opa[r] = make_float4(rgb[3 * p], rgb[3 * p + 1], rgb[3 * p + 2], opacity ? opacity[p] : opacity_default);
+}
+
+cudaError_t launch_densify(Ctx &c, const float *depth, const float *rgb, const vtgs_pose *pose, vtgs_intrinsics intr,
+                           const float *sil, float thr, const float *opacity, float opacity_default,
+                           float4 *pos_rad, float4 *col_opa, int64_t *n_new, cudaStream_t s) {
+    const int HW = intr.width * intr.height;
+    const int nblk = (HW + 255) / 256;
+    LaunchScope ls(&c, kDensify, s);
+    k_densify_count<<<nblk, 256, 0, s>>>(depth, sil, thr, HW, c.offs);
+    k_densify_scan<<<1, 1024, 0, s>>>(c.offs, nblk, n_new);
+    k_densify_write<<<nblk, 256, 0, s>>>(depth, rgb, pose, HW, intr.width, intr, sil, thr, opacity, opacity_default,
+                                         c.offs, pos_rad, col_opa);
+    c.launches += 2;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_instantiate(Ctx &c, const float *depth, const float *rgb, const vtgs_pose *poses, int K,
                                vtgs_intrinsics intr, const float *opacity, float opacity_default,
                                float4 *pos_rad, float4 *col_opa, cudaStream_t s) {

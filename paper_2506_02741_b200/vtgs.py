@@ -67,6 +67,7 @@ _SIGS = {
     "vtgs_render_fwd": (_c.c_int32, [_P, _P, _P, _c.c_int64, _P, vtgs_intrinsics, _P, _P, _P, _P]),
     "vtgs_render_bwd": (_c.c_int32, [_P, _P, _P, _P, _c.POINTER(vtgs_l1_loss), _c.c_uint32, _c.c_int64, _c.c_int64,
                                      _P, _P, _P, _P, _P, _P]),
+    "vtgs_densify": (_c.c_int32, [_P, _P, _P, _P, vtgs_intrinsics, _P, _c.c_float, _P, _c.c_float, _P, _P, _P, _P]),
     "vtgs_ssim_loss": (_c.c_int32, [_P, _P, _P, _c.c_int32, _c.c_int32, _c.c_float, _P, _P, _P]),
     "vtgs_keyframe_pose_grad": (_c.c_int32, [_P, _P, _P, _P, _c.c_int32, _c.c_int64, _P, _P]),
     "vtgs_pose_adam_step": (_c.c_int32, [_P, _P, _P, _P, _c.c_float, _c.c_float, _P]),
@@ -188,6 +189,17 @@ class Renderer:
                             int(learn[1]), _ptr(d_col_opa), _ptr(d_radius), _ptr(d_position), _ptr(d_pose),
                             _ptr(loss_out), _stream(stream)), self.ctx)
 
+    def densify(self, depth: torch.Tensor, rgb: torch.Tensor, pose: torch.Tensor, intr, silhouette: torch.Tensor,
+                pos_rad_out: torch.Tensor, col_opa_out: torch.Tensor, threshold: float = 0.5, opacity=None,
+                opacity_default: float = 0.5, stream=None) -> int:
+        """Regular-frame densification: returns the number of new Gaussians
+        written to pos_rad_out / col_opa_out (synchronises the stream to read it)."""
+        n = torch.zeros(1, dtype=torch.int64, device=self.device)
+        _ok(vtgs_densify(self.ctx, _ptr(depth), _ptr(rgb), _ptr(pose), intrinsics(intr), _ptr(silhouette),
+                         float(threshold), _ptr(opacity), float(opacity_default), _ptr(pos_rad_out), _ptr(col_opa_out),
+                         _ptr(n), _stream(stream)), self.ctx)
+        return int(n.item())
+
     def ssim_loss(self, color: torch.Tensor, target_rgb: torch.Tensor, tau: float = 0.2, d_color=None,
                   loss_out=None, stream=None):
         """SSIM term τ·L_S of Eq. 2: d_color += dL/dcolor, loss_out = τ·L_S."""
@@ -219,7 +231,8 @@ class Renderer:
         return d
 
     STAGES = ("project_count", "scan_tiles", "emit_pairs", "tile_sort", "composite_fwd", "l1_count",
-              "composite_bwd", "pose_finalize", "instantiate", "pose_adam", "keyframe_pose_grad", "ssim")
+              "composite_bwd", "pose_finalize", "instantiate", "pose_adam", "keyframe_pose_grad", "ssim",
+              "densify")
 
     def set_work_counters(self, enable: bool):
         _ok(vtgs_set_work_counters(self.ctx, int(bool(enable))), self.ctx)

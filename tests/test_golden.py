@@ -51,7 +51,7 @@ def test_golden_radius_and_footprint():
 
 
 def test_golden_l1_example():
-    """SPEC.md:314: α = 0.5, β = 0.025 with unit colour error and zero depth error, full mask
+    """SPEC.md:277: α = 0.5, β = 0.025 with unit colour error and zero depth error, full mask
     (mean form) → 0.5."""
     g = _load("paper_hyperparameters.json")["l1_example"]
     H, W = 4, 5

@@ -656,3 +656,60 @@ def test_mapping_objective_with_ssim_parity(vt):
     _, gss = oracle.ssim_loss(img["color"], tg.rgb, 0.2)
     ref, g = _oracle_grads(cfg, opr, oco, v, gC + gss, gD, gS, extra_flags=lflags)
     _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt)
+
+
+# ------------------------------------------------------------------------------ f4 (densification)
+def test_densify_parity(vt):
+    """Regular-frame densification: on a synthetic silhouette field given to
+    both sides, the appended Gaussians are bit-exact with the oracle (same rows, same order,
+    same count), including a pixel exactly at the threshold and invalid depths."""
+    rng = np.random.default_rng(11)
+    H, W = 37, 53
+    intr = Intrinsics(40.0, 41.0, (W - 1) / 2, (H - 1) / 2, W, H)
+    depth = np.where(rng.random((H, W)) < 0.1, 0.0, rng.uniform(0.5, 4.0, (H, W))).astype(np.float32)
+    rgb = rng.random((H, W, 3)).astype(np.float32)
+    sil = rng.random((H, W)).astype(np.float32)
+    sil[3, 4] = 0.5
+    depth[3, 4] = 2.0
+    opa = rng.random((H, W)).astype(np.float32)
+    from synth.scenes import perturb_pose
+    pose = perturb_pose(np.array([1.0, 0, 0, 0, 0, 0, 0]), 7.0, 0.3, rng).astype(np.float32)
+    R = vt.Renderer(0, H * W, W, H)
+    dev = "cuda"
+    out_pr = torch.zeros((H * W, 4), device=dev)
+    out_co = torch.zeros((H * W, 4), device=dev)
+    n = R.densify(torch.from_numpy(depth).to(dev), torch.from_numpy(rgb).to(dev), vt.pose_tensor(pose, dev), intr,
+                  torch.from_numpy(sil).to(dev), out_pr, out_co, 0.5, torch.from_numpy(opa).to(dev))
+    opr, oco = oracle.densify(depth, rgb, pose.astype(np.float64), intr, sil, 0.5, opa)
+    assert n == len(opr)
+    assert np.array_equal(out_pr.cpu().numpy()[:n], opr.astype(np.float32))
+    assert np.array_equal(out_co.cpu().numpy()[:n], oco.astype(np.float32))
+    assert not out_pr.cpu().numpy()[n:].any()
+
+
+def test_densify_after_render(vt):
+    """End to end: render the section (config 3's keyframes) from the frame to track, densify
+    where the rendered silhouette is < 0.5; the new set equals the oracle's {valid ∧ S < 0.5}
+    except at pixels whose silhouette lies within 1e-4 of the threshold (the render bar)."""
+    cfg = cached_config(3)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    v = view32(cfg.extra["gt_pose"])
+    vv, out = _render_gpu(vt, R, cfg, pr, co, v)
+    tg = cfg.targets[0]
+    H, W = cfg.intr.height, cfg.intr.width
+    dev = "cuda"
+    out_pr = torch.zeros((H * W, 4), device=dev)
+    out_co = torch.zeros((H * W, 4), device=dev)
+    n = R.densify(torch.from_numpy(tg.depth).to(dev), torch.from_numpy(tg.rgb).to(dev), vv, cfg.intr, out[2],
+                  out_pr, out_co, 0.5)
+    opr, oco = oracle_instantiate(cfg)
+    img = oracle.render(opr, oco, v, cfg.intr)
+    near = np.abs(img["sil"] - 0.5) <= 1e-4
+    sel = (tg.depth > 0) & (img["sil"] < 0.5)
+    assert abs(n - int(sel.sum())) <= int(near.sum())
+    # the oracle's densification of its own silhouette, compared on pixels away from the threshold
+    dpr, _ = oracle.densify(tg.depth, tg.rgb, v, cfg.intr, img["sil"], 0.5)
+    g = out_pr.cpu().numpy()[:n]
+    if not near.any():
+        assert np.array_equal(g, dpr.astype(np.float32))

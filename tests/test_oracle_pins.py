@@ -624,3 +624,31 @@ def test_ssim_gradient_central_differences():
         fd = (oracle.ssim_loss(xp, y)[0] - oracle.ssim_loss(xm, y)[0]) / (2 * eps)
         worst = max(worst, abs(fd - g[idx]) / max(abs(g[idx]), 1e-6))
     assert worst < 1e-5
+
+
+# ------------------------------------------------------------------------------ f4 (densification)
+def test_densify_special_cases():
+    """silhouette ≡ 1 → no new Gaussians; silhouette ≡ 0 (empty section) → exactly
+    init_gaussians' valid slots, in row-major order; otherwise the new set is {valid ∧ S < 0.5}
+    (strict), each initialised as init_gaussians."""
+    rng = np.random.default_rng(4)
+    H, W = 9, 11
+    intr = Intrinsics(10.0, 11.0, 5.0, 4.0, W, H)
+    depth = np.where(rng.random((H, W)) < 0.2, 0.0, rng.uniform(0.5, 3.0, (H, W)))
+    rgb = rng.random((H, W, 3))
+    pose = perturb_pose(IDENT, 5.0, 0.1, rng)
+    opa = rng.random((H, W))
+    pr, co = oracle.densify(depth, rgb, pose, intr, np.ones((H, W)), 0.5, opa)
+    assert len(pr) == 0
+    pr, co = oracle.densify(depth, rgb, pose, intr, np.zeros((H, W)), 0.5, opa)
+    ipr, ico, n = oracle.instantiate(depth[None], rgb[None], pose[None], intr, opa[None])
+    valid = depth.reshape(-1) > 0
+    assert len(pr) == n and np.array_equal(pr, ipr[valid]) and np.array_equal(co, ico[valid])
+    sil = rng.random((H, W))
+    sil[0, 0] = 0.5                      # exactly at the threshold: covered (strict <)
+    depth[0, 0] = 1.0
+    pr, co = oracle.densify(depth, rgb, pose, intr, sil, 0.5, opa)
+    ipr, ico, _ = oracle.instantiate(depth[None], rgb[None], pose[None], intr, opa[None])
+    sel = (depth.reshape(-1) > 0) & (sil.reshape(-1) < 0.5)
+    assert not sel[0] and len(pr) == sel.sum()
+    assert np.array_equal(pr, ipr[sel]) and np.array_equal(co, ico[sel])
