@@ -118,6 +118,21 @@ VTGS_API vtgs_status vtgs_densify(vtgs_ctx *ctx, const float *depth, const float
                          float opacity_default, float *pos_rad_out, float *col_opa_out, int64_t *n_new,
                          void *stream);
 
+/* Visibility mask of a frame to a section — PAPER.md:186 (§3.3 "Visibility Check": a point is
+ * visible to a view "if its projected depth is within 1% of the interpolated depth at its
+ * projection on the depth map"; the section's mask is the union over its head, middle and last
+ * frames).  Every valid pixel of `depth` (the frame, at device `pose`) is
+ * back-projected, transformed into each reference view r (ref_poses[r], device) and tested:
+ * z > 0.01, projection inside [0, W−1] × [0, H−1], bilinear reference depth valid (four
+ * neighbours > 0), |z − d_r| ≤ tol·d_r (tol = 0.01 in the paper).
+ *   depth [H×W], ref_depth [R×H×W] (device), 1 ≤ R ≤ 8; mask [H×W] uint8 (device, OVERWRITTEN:
+ *   1 = visible to some reference) — pass it as vtgs_l1_loss.vis_mask for Eq. 1's W_i;
+ *   n_visible: device int64 or NULL (OVERWRITTEN with the count).  Asynchronous on `stream`. */
+VTGS_API vtgs_status vtgs_visibility_mask(vtgs_ctx *ctx, const float *depth, const vtgs_pose *pose,
+                                 const float *ref_depth, const vtgs_pose *ref_poses, int32_t R,
+                                 vtgs_intrinsics intr, float tol, uint8_t *mask, int64_t *n_visible,
+                                 void *stream);
+
 /* (2)–(4) Forward render of N Gaussians from `view` — PAPER.md:146 (Eq. 1 `splat`),
  * PAPER.md:192 (Eq. 2 multi-set render: concatenate the sets, pass the union).
  *   projection: X_c = Rᵀ(X_w − t), culled if r ≤ 0 or z ≤ 0.01 m; σ = max(f_mean·r/z, 0.3) px;
@@ -233,8 +248,8 @@ VTGS_API vtgs_status vtgs_set_work_counters(vtgs_ctx *ctx, int32_t enable);
  * while enabled; not for use inside CUDA-graph capture).  Stages, in order:
  *   0 project_count, 1 scan_tiles, 2 emit_pairs, 3 tile_sort, 4 composite_fwd, 5 l1_count,
  *   6 composite_bwd, 7 pose_finalize, 8 instantiate, 9 pose_adam, 10 keyframe_pose_grad, 11 ssim,
- *   12 densify. */
-#define VTGS_NUM_STAGES 13
+ *   12 densify, 13 visibility. */
+#define VTGS_NUM_STAGES 14
 VTGS_API vtgs_status vtgs_set_profiling(vtgs_ctx *ctx, int32_t enable);
 /* Synchronous: sum of event-timed milliseconds (ms[VTGS_NUM_STAGES], host) and launch counts
  * (counts[VTGS_NUM_STAGES], host, may be NULL) per stage since the previous call; resets. */

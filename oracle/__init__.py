@@ -63,6 +63,9 @@ def _load():
             f = getattr(lib, f"or_render_bwd_{m}")
             f.restype = ctypes.c_int
             f.argtypes = [_D, _D, ctypes.c_int64, _D, _D, ctypes.c_int, ctypes.c_int, _D, _D, _D, _D, _D, _D, _D, _D, _D, _D]
+            f = getattr(lib, f"or_visibility_{m}")
+            f.restype = ctypes.c_int64
+            f.argtypes = [_D, _D, _D, _D, ctypes.c_int, _D, ctypes.c_int, ctypes.c_int, ctypes.c_double, _U8]
             f = getattr(lib, f"or_keyframe_pose_grad_{m}")
             f.restype = None
             f.argtypes = [_D, _D, ctypes.c_int, _D, ctypes.c_int, ctypes.c_int, _D, _D]
@@ -255,3 +258,18 @@ def densify(depth, rgb, pose, intr, sil, threshold=0.5, opacity=None, opacity_de
     n = lib.or_densify_f32(_p(depth), _p(rgb), _p(_d(pose)), _p(_intr(intr)), W, H, _p(sil), float(threshold), _p(opa),
                            float(opacity_default), _p(pr), _p(co))
     return pr[:n], co[:n]
+
+
+def visibility(depth, pose, ref_depth, ref_poses, intr, tol=0.01, mode="f32"):
+    """Visibility mask of a frame (depth [H,W] at pose) to reference views (ref_depth [R,H,W],
+    ref_poses [R,7]); union over the references → bool [H,W]."""
+    lib = _load()
+    depth = _d(depth)
+    H, W = depth.shape
+    ref_depth = _d(ref_depth).reshape(-1, H, W)
+    R = ref_depth.shape[0]
+    ref_poses = _d(ref_poses).reshape(R, 7)
+    mask = np.zeros((H, W), dtype=np.uint8)
+    getattr(lib, f"or_visibility_{mode}")(_p(depth), _p(_d(pose)), _p(ref_depth), _p(ref_poses), R, _p(_intr(intr)),
+                                          W, H, float(tol), _p(mask, _U8))
+    return mask.astype(bool)

@@ -16,6 +16,7 @@
  *   or_l1_upstream          masked L1 terms of Eq. 1 / Eq. 2
  *   or_ssim_loss            SSIM term τ·L_S of Eq. 2 and its gradient
  *   or_densify_f32          regular-frame densification (S < 0.5)
+ *   or_visibility_*         visibility mask to a section (1% depth band)
  * Two builds of the same source (oracle_impl.inc): *_f32 takes every decision in fp32 (the
  * kernel's precision) with fp64 values; *_f64 is fp64 throughout.
  *

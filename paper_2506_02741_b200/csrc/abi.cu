@@ -271,6 +271,23 @@ vtgs_status vtgs_keyframe_pose_grad(vtgs_ctx *ctx, const float *pos_rad, const f
     return e ? cuda_fail(ctx, e, "vtgs_keyframe_pose_grad") : VTGS_OK;
 }
 
+vtgs_status vtgs_visibility_mask(vtgs_ctx *ctx, const float *depth, const vtgs_pose *pose, const float *ref_depth,
+                                 const vtgs_pose *ref_poses, int32_t R, vtgs_intrinsics intr, float tol, uint8_t *mask,
+                                 int64_t *n_visible, void *stream) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    c.last_error[0] = 0;
+    if (!depth || !pose || !ref_depth || !ref_poses || !mask)
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "NULL argument to vtgs_visibility_mask");
+    if (R < 1 || R > 8) return fail(ctx, VTGS_ERR_SHAPE, "R = %d reference views (1..8)", R);
+    vtgs_status st = check_intr(ctx, intr);
+    if (st) return st;
+    cudaSetDevice(c.device);
+    cudaError_t e = vtgs::launch_visibility(c, depth, pose, ref_depth, ref_poses, R, intr, tol, mask, n_visible,
+                                            (cudaStream_t)stream);
+    return e ? cuda_fail(ctx, e, "vtgs_visibility_mask") : VTGS_OK;
+}
+
 vtgs_status vtgs_densify(vtgs_ctx *ctx, const float *depth, const float *rgb, const vtgs_pose *pose,
                          vtgs_intrinsics intr, const float *silhouette, float threshold, const float *opacity,
                          float opacity_default, float *pos_rad_out, float *col_opa_out, int64_t *n_new,

@@ -139,6 +139,80 @@ cudaError_t launch_densify(Ctx &c, const float *depth, const float *rgb, const v
     return cudaGetLastError();
 }
 
+// Visibility mask of a frame to a section's reference views ("Visibility Check",
+// SPEC.md:313-331): a valid pixel's back-projected point is visible to reference r iff it lies in
+// front of it (z > 0.01), projects inside the image, the bilinearly interpolated reference depth
+// there is valid (all four neighbours > 0) and |z − d_r| ≤ tol·d_r; the mask is the union over
+// the references.  One thread per pixel; decisions in fp32 with the oracle's operation order
+// (R25).
+constexpr int kMaxVisRefs = 8;
+
+__global__ void __launch_bounds__(256) k_visibility(const float *__restrict__ depth, const vtgs_pose *__restrict__ pose,
+                                                    const float *__restrict__ ref_depth,
+                                                    const vtgs_pose *__restrict__ ref_poses, int R, int W, int H,
+                                                    vtgs_intrinsics in, float tol, uint8_t *__restrict__ mask,
+                                                    unsigned long long *__restrict__ n_vis) {
+    __shared__ PoseR P, Pr[kMaxVisRefs];
+    if (threadIdx.x == 0) pose_rotation(*pose, P);
+    if (threadIdx.x < R) pose_rotation(ref_poses[threadIdx.x], Pr[threadIdx.x]);
+    __syncthreads();
+    const int HW = W * H;
+    const float Wm1 = (float)(W - 1), Hm1 = (float)(H - 1);
+    unsigned cnt = 0;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < HW; p += gridDim.x * blockDim.x) {
+        uint8_t vis = 0;
+        const float d = depth[p];
+        if (d > 0.0f && isfinite(d)) {
+            const int y = p / W, x = p - y * W;
+            const float X0 = __fdiv_rn(__fmul_rn(__fsub_rn((float)x, in.cx), d), in.fx);
+            const float X1 = __fdiv_rn(__fmul_rn(__fsub_rn((float)y, in.cy), d), in.fy);
+            float Xw[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                Xw[a] = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(P.R[3 * a], X0), __fmul_rn(P.R[3 * a + 1], X1)),
+                                            __fmul_rn(P.R[3 * a + 2], d)),
+                                  P.t[a]);
+            for (int r = 0; r < R && !vis; ++r) {
+                float X[3];
+                view_transform(Pr[r].R, Pr[r].t, make_float4(Xw[0], Xw[1], Xw[2], 0.f), X);
+                const float z = X[2];
+                if (!(z > kNearClip)) continue;
+                const float u = __fadd_rn(__fdiv_rn(__fmul_rn(in.fx, X[0]), z), in.cx);
+                const float v = __fadd_rn(__fdiv_rn(__fmul_rn(in.fy, X[1]), z), in.cy);
+                if (!(u >= 0.0f && u <= Wm1 && v >= 0.0f && v <= Hm1)) continue;
+                const int x0 = (int)floorf(u), y0 = (int)floorf(v);
+                const int x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
+                const float fa = __fsub_rn(u, (float)x0), fb = __fsub_rn(v, (float)y0);
+                const float *D = ref_depth + (size_t)r * HW;
+                const float d00 = D[y0 * W + x0], d10 = D[y0 * W + x1], d01 = D[y1 * W + x0], d11 = D[y1 * W + x1];
+                if (!(d00 > 0.0f && d10 > 0.0f && d01 > 0.0f && d11 > 0.0f)) continue;
+                const float ia = __fsub_rn(1.0f, fa), ib = __fsub_rn(1.0f, fb);
+                const float di = __fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(d00, ia), __fmul_rn(d10, fa)), ib),
+                                           __fmul_rn(__fadd_rn(__fmul_rn(d01, ia), __fmul_rn(d11, fa)), fb));
+                if (fabsf(__fsub_rn(z, di)) <= __fmul_rn(tol, di)) vis = 1;
+            }
+        }
+        mask[p] = vis;
+        cnt += vis;
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (n_vis && (threadIdx.x & 31) == 0 && cnt) atomicAdd(n_vis, (unsigned long long)cnt);
+}
+
+cudaError_t launch_visibility(Ctx &c, const float *depth, const vtgs_pose *pose, const float *ref_depth,
+                              const vtgs_pose *ref_poses, int R, vtgs_intrinsics intr, float tol, uint8_t *mask,
+                              int64_t *n_vis, cudaStream_t s) {
+    const int HW = intr.width * intr.height;
+    int g = (HW + 255) / 256;
+    if (g > c.num_sms * 8) g = c.num_sms * 8;
+    cudaError_t e = cudaSuccess;
+    if (n_vis && (e = cudaMemsetAsync(n_vis, 0, sizeof(int64_t), s))) return e;
+    LaunchScope ls(&c, kVisibility, s);
+    k_visibility<<<g, 256, 0, s>>>(depth, pose, ref_depth, ref_poses, R, intr.width, intr.height, intr, tol, mask,
+                                   (unsigned long long *)n_vis);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_instantiate(Ctx &c, const float *depth, const float *rgb, const vtgs_pose *poses, int K,
                                vtgs_intrinsics intr, const float *opacity, float opacity_default,
                                float4 *pos_rad, float4 *col_opa, cudaStream_t s) {

@@ -40,7 +40,7 @@ struct DevScalars {
 };
 
 enum Stage { kProject = 0, kScan, kEmit, kSort, kCompFwd, kL1Count, kCompBwd, kFinalize, kInstantiate,
-             kPoseAdam, kKfPose, kSsim, kDensify, kNumStages };
+             kPoseAdam, kKfPose, kSsim, kDensify, kVisibility, kNumStages };
 
 struct ProfEvent {
     int stage;
@@ -218,6 +218,9 @@ cudaError_t forward_set_attributes();
 cudaError_t backward_set_attributes();
 cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s);
 cudaError_t ssim_set_constants();
+cudaError_t launch_visibility(Ctx &c, const float *depth, const vtgs_pose *pose, const float *ref_depth,
+                              const vtgs_pose *ref_poses, int R, vtgs_intrinsics intr, float tol, uint8_t *mask,
+                              int64_t *n_vis, cudaStream_t s);
 cudaError_t launch_densify(Ctx &c, const float *depth, const float *rgb, const vtgs_pose *pose, vtgs_intrinsics intr,
                            const float *sil, float thr, const float *opacity, float opacity_default,
                            float4 *pos_rad, float4 *col_opa, int64_t *n_new, cudaStream_t s);

@@ -67,6 +67,7 @@ _SIGS = {
     "vtgs_render_fwd": (_c.c_int32, [_P, _P, _P, _c.c_int64, _P, vtgs_intrinsics, _P, _P, _P, _P]),
     "vtgs_render_bwd": (_c.c_int32, [_P, _P, _P, _P, _c.POINTER(vtgs_l1_loss), _c.c_uint32, _c.c_int64, _c.c_int64,
                                      _P, _P, _P, _P, _P, _P]),
+    "vtgs_visibility_mask": (_c.c_int32, [_P, _P, _P, _P, _P, _c.c_int32, vtgs_intrinsics, _c.c_float, _P, _P, _P]),
     "vtgs_densify": (_c.c_int32, [_P, _P, _P, _P, vtgs_intrinsics, _P, _c.c_float, _P, _c.c_float, _P, _P, _P, _P]),
     "vtgs_ssim_loss": (_c.c_int32, [_P, _P, _P, _c.c_int32, _c.c_int32, _c.c_float, _P, _P, _P]),
     "vtgs_keyframe_pose_grad": (_c.c_int32, [_P, _P, _P, _P, _c.c_int32, _c.c_int64, _P, _P]),
@@ -189,6 +190,17 @@ class Renderer:
                             int(learn[1]), _ptr(d_col_opa), _ptr(d_radius), _ptr(d_position), _ptr(d_pose),
                             _ptr(loss_out), _stream(stream)), self.ctx)
 
+    def visibility_mask(self, depth: torch.Tensor, pose: torch.Tensor, ref_depth: torch.Tensor,
+                        ref_poses: torch.Tensor, intr, tol: float = 0.01, mask=None, stream=None):
+        """Visibility of a frame's back-projected pixels to reference views → uint8 [H, W]."""
+        H, W = depth.shape
+        R = ref_poses.reshape(-1, 7).shape[0]
+        if mask is None:
+            mask = torch.empty((H, W), dtype=torch.uint8, device=self.device)
+        _ok(vtgs_visibility_mask(self.ctx, _ptr(depth), _ptr(pose), _ptr(ref_depth), _ptr(ref_poses), R,
+                                 intrinsics(intr), float(tol), _ptr(mask), None, _stream(stream)), self.ctx)
+        return mask
+
     def densify(self, depth: torch.Tensor, rgb: torch.Tensor, pose: torch.Tensor, intr, silhouette: torch.Tensor,
                 pos_rad_out: torch.Tensor, col_opa_out: torch.Tensor, threshold: float = 0.5, opacity=None,
                 opacity_default: float = 0.5, stream=None) -> int:
@@ -232,7 +244,7 @@ class Renderer:
 
     STAGES = ("project_count", "scan_tiles", "emit_pairs", "tile_sort", "composite_fwd", "l1_count",
               "composite_bwd", "pose_finalize", "instantiate", "pose_adam", "keyframe_pose_grad", "ssim",
-              "densify")
+              "densify", "visibility")
 
     def set_work_counters(self, enable: bool):
         _ok(vtgs_set_work_counters(self.ctx, int(bool(enable))), self.ctx)

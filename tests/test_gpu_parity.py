@@ -713,3 +713,55 @@ def test_densify_after_render(vt):
     g = out_pr.cpu().numpy()[:n]
     if not near.any():
         assert np.array_equal(g, dpr.astype(np.float32))
+
+
+# ------------------------------------------------------------------------------ f3 (visibility, pre-tracking)
+def test_visibility_mask_parity(vt):
+    """the frame to track (config 3) against its section's head, middle and last
+    keyframes — bit-exact with the oracle's fp32 decisions (same operation order, R25)."""
+    cfg = cached_config(3)
+    R = _renderer(vt, cfg)
+    tg = cfg.targets[0]
+    K = cfg.K
+    idx = [0, K // 2, K - 1]
+    kd = cfg.depth_stack()[idx]
+    kp = cfg.pose_stack()[idx].astype(np.float32)
+    pose = view32(cfg.views[0]).astype(np.float32)
+    m = R.visibility_mask(torch.from_numpy(tg.depth).cuda(), vt.pose_tensor(pose, "cuda"),
+                          torch.from_numpy(np.ascontiguousarray(kd)).cuda(), vt.pose_tensor(kp, "cuda"), cfg.intr)
+    ref = oracle.visibility(tg.depth, pose.astype(np.float64), kd, kp.astype(np.float64), cfg.intr)
+    g = m.cpu().numpy().astype(bool)
+    assert 0.05 < ref.mean() < 1.0
+    assert np.array_equal(g, ref), int((g != ref).sum())
+
+
+def test_pretrack_select_concurrent_matches_sequential(vt):
+    """PAPER.md:180-182 pre-tracking: three candidate sections (config 3's keyframes split in
+    three) tracked for 10 iterations each, concurrently on three streams; the losses equal a
+    sequential run bit for bit, the selection is their argmin, and the selected section's
+    pre-tracking reduces its rendering error."""
+    from paper_2506_02741_b200 import tracking
+    cfg = cached_config(3)
+    tg = cfg.targets[0]
+    dev = "cuda"
+    rgb, depth = torch.from_numpy(tg.rgb).to(dev), torch.from_numpy(tg.depth).to(dev)
+    init = vt.pose_tensor(view32(cfg.views[0]), dev)
+    H, W = cfg.intr.height, cfg.intr.width
+    groups = [[0, 1, 2], [3, 4, 5], [6, 7, 8, 9]]
+    secs, rends = [], []
+    for gidx in groups:
+        n = len(gidx) * H * W
+        Rg = vt.Renderer(0, n, W, H)
+        ds = torch.from_numpy(np.ascontiguousarray(cfg.depth_stack()[gidx])).to(dev)
+        ps = vt.pose_tensor(cfg.pose_stack()[gidx], dev)
+        pr, co = Rg.instantiate(ds, torch.from_numpy(np.ascontiguousarray(cfg.rgb_stack()[gidx])).to(dev), ps,
+                                cfg.intr, torch.from_numpy(np.ascontiguousarray(cfg.opacity[gidx])).to(dev))
+        vis = tracking.section_visibility(Rg, depth, init, ds, ps, cfg.intr)
+        secs.append(dict(pos_rad=pr, col_opa=co, vis_mask=vis))
+        rends.append(Rg)
+    best, finals, res = tracking.pretrack_select(rends, secs, cfg.intr, rgb, depth, init, 10, 0.002, 0.002)
+    best2, finals2, _ = tracking.pretrack_select(rends, secs, cfg.intr, rgb, depth, init, 10, 0.002, 0.002,
+                                                 concurrent=False)
+    assert finals == finals2 and best == best2 == int(np.argmin(finals))
+    ls = res[best].losses.cpu().numpy()
+    assert ls[-1] < ls[0]                      # the selected section's pre-tracking reduces the error

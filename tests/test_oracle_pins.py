@@ -652,3 +652,43 @@ def test_densify_special_cases():
     sel = (depth.reshape(-1) > 0) & (sil.reshape(-1) < 0.5)
     assert not sel[0] and len(pr) == sel.sum()
     assert np.array_equal(pr, ipr[sel]) and np.array_equal(co, ico[sel])
+
+
+# ------------------------------------------------------------------------------ f3 (visibility)
+def _plane_frame(W=24, H=18, f=20.0, seed=0):
+    rng = np.random.default_rng(seed)
+    intr = Intrinsics(f, f, (W - 1) / 2, (H - 1) / 2, W, H)
+    xs, ys = np.meshgrid(np.arange(W), np.arange(H))
+    depth = 2.0 + 0.02 * xs + 0.01 * ys
+    return intr, depth, rng
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_visibility_special_cases(mode):
+    """P:186 / S:313-322: a frame's own back-projected points are visible to itself (SPEC
+    "self-consistency"), a depth band of 1% decides (z = 1.02·d → not visible, 1.005·d →
+    visible), points outside the reference frustum are not visible, and the section mask is the
+    union of the per-reference masks."""
+    intr, depth, rng = _plane_frame()
+    pose = IDENT
+    own = oracle.visibility(depth, pose, depth[None], pose[None], intr, mode=mode)
+    assert own.mean() > 0.99
+    far = oracle.visibility(depth, pose, (depth / 1.02)[None], pose[None], intr, mode=mode)
+    assert not far.any()
+    near = oracle.visibility(depth, pose, (depth / 1.005)[None], pose[None], intr, mode=mode)
+    assert near.mean() > 0.99
+    away = np.array([0.0, 0.0, 1.0, 0.0, 0, 0, 0])          # 180° about y: looking backwards
+    assert not oracle.visibility(depth, pose, depth[None], away[None], intr, mode=mode).any()
+    # fronto-parallel wall 2 m away seen from a camera 30 cm to the side: partial overlap
+    wall = np.full_like(depth, 2.0)
+    shifted = np.array([1.0, 0, 0, 0, 0.3, 0.0, 0.0])
+    m_a = oracle.visibility(wall, pose, wall[None], shifted[None], intr, mode=mode)
+    u_ref = np.arange(intr.width) - 0.3 * intr.fx / 2.0      # each column's wall point in the shifted view
+    assert m_a[:, (u_ref > 0.5) & (u_ref < intr.width - 1.5)].all()
+    assert not m_a[:, u_ref < -0.5].any()
+    m_b = oracle.visibility(wall, pose, (wall / 1.005)[None], pose[None], intr, mode=mode)
+    m_c = oracle.visibility(wall, pose, (wall / 1.02)[None], pose[None], intr, mode=mode)
+    m_ab = oracle.visibility(wall, pose, np.stack([wall, wall / 1.02]), np.stack([shifted, pose]), intr, mode=mode)
+    assert 0 < m_a.mean() < 1 and m_b.all() and not m_c.any() and np.array_equal(m_ab, m_a | m_c)
+    loose = oracle.visibility(depth, pose, (depth / 1.015)[None], pose[None], intr, tol=0.02, mode=mode)
+    assert loose.mean() > 0.99          # monotone in the tolerance (S:339)
