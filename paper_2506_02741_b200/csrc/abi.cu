@@ -112,7 +112,6 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = dalloc(&c.tile_start, (size_t)c.max_tiles + 1);
     if (!e) e = dalloc(&c.tile_cursor, (size_t)c.max_tiles);
     if (!e) e = dalloc(&c.tile_flag, (size_t)c.max_tiles);
-    if (!e) e = cudaMemset(c.tile_flag, 0, sizeof(uint32_t) * c.max_tiles);
     if (!e) e = dalloc(&c.keys, (size_t)max_pairs);
     if (!e) e = dalloc(&c.vals, (size_t)max_pairs);
     if (!e) e = dalloc(&c.pbits, (size_t)max_pairs);

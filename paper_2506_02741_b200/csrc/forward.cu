@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t *__restrict__ tile
                                                      unsigned long long cap,
                                                      DevScalars *__restrict__ dev,
                                                      const vtgs_pose *__restrict__ view,
-                                                     vtgs_pose *__restrict__ view_copy) {
+                                                     vtgs_pose *__restrict__ view_copy,
+                                                     uint32_t *__restrict__ radix_list) {
     if (threadIdx.x == 0) *view_copy = *view;  // the backward reads the copy (caller may reuse view)
     __shared__ unsigned long long warp_sum[32];
     __shared__ unsigned int warp_max[32];
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t *__restrict__ tile
         tile_start[i] = overflow ? 0u : (uint32_t)run;
         cursor[i] = overflow ? 0u : (uint32_t)run;
         if (overflow) tile_count[i] = 0;
+        else if (c > (uint32_t)kSortCap) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)i;
         run += c;
     }
     if (tid == 0) tile_start[T] = overflow ? 0u : (uint32_t)total_s;
@@ -369,14 +371,19 @@ __global__ void __launch_bounds__(kBlock) k_tile_sort(const uint32_t *__restrict
                                                       const uint2 *__restrict__ rect, int ntx,
                                                       uint32_t *__restrict__ sub_lists,
                                                       uint32_t *__restrict__ sub_count,
-                                                      const uint32_t *__restrict__ tile_flag) {
+                                                      const uint32_t *__restrict__ work_list,
+                                                      const DevScalars *__restrict__ dev) {
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t hist[8 * 256];
     __shared__ uint32_t red[32];
-    const int tile = blockIdx.x;
+    // without a work list: one CTA per tile, tiles in (LO, CAP]; with one (the bucket-sort path):
+    // a small grid walks the list of long / degenerate tiles that k_scan_tiles and
+    // k_tile_sort_bucket appended (no wave of empty CTAs over every tile)
+    const int nwork = work_list ? (int)dev->radix_count : 1;
+    for (int w = blockIdx.x; w < (work_list ? nwork : 1); w += gridDim.x) {
+    const int tile = work_list ? (int)work_list[w] : (int)blockIdx.x;
     const int n = (int)tile_count[tile];
-    // tiles longer than LO, or flagged by the bucket sort (degenerate depth distribution)
-    if ((n <= LO && !(tile_flag && tile_flag[tile])) || (!GLOBAL && n > CAP)) return;
+    if (!work_list && (n <= LO || (!GLOBAL && n > CAP))) return;
     const uint32_t base = tile_start[tile];
     const int ty = tile / ntx, tx = tile - ty * ntx;
     uint32_t *out = sub_lists + (size_t)8 * base;
@@ -399,6 +406,8 @@ __global__ void __launch_bounds__(kBlock) k_tile_sort(const uint32_t *__restrict
         __syncthreads();
         uint8_t *bits8 = reinterpret_cast<uint8_t *>(odd ? keys + base : keys2 + base);
         build_sublists(vals + base, n, rect, tx * kTile, ty * kTile, out, sub_count + 8 * tile, hist, bits8);
+    }
+    __syncthreads();
     }
 }
 
@@ -495,7 +504,8 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
                                                          const uint8_t *__restrict__ pbits,
                                                          uint32_t *__restrict__ sub_lists,
                                                          uint32_t *__restrict__ sub_count,
-                                                         uint32_t *__restrict__ tile_flag) {
+                                                         uint32_t *__restrict__ radix_list,
+                                                         DevScalars *__restrict__ dev) {
     constexpr int NW = NT / 32;
     constexpr int PT = NB / NT;
     static_assert(PT >= 1 && PT * NT == NB, "NB must be a multiple of NT");
@@ -580,11 +590,10 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
             run += c[j];
         }
     }
-    if (cmax > (uint32_t)kMaxBucket) {   // degenerate depth distribution → the radix kernel
-        if (tid == 0) tile_flag[tile] = 1u;
+    if (cmax > (uint32_t)kMaxBucket) {   // degenerate depth distribution → the radix kernel's list
+        if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;
         return;
     }
-    if (tid == 0) tile_flag[tile] = 0u;
     __syncthreads();
     for (int i = tid; i < n; i += NT) {
         const uint32_t k = K[i];
@@ -642,7 +651,7 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     {
         LaunchScope ls(&c, kScan, s);
         k_scan_tiles<<<1, 1024, 0, s>>>(c.tile_count, c.tile_start, c.tile_cursor, T,
-                                         (unsigned long long)c.max_pairs, c.dev, c.view, c.view_copy);
+                                         (unsigned long long)c.max_pairs, c.dev, c.view, c.view_copy, c.tile_flag);
     }
     if ((err = cudaGetLastError())) return err;
     if (N > 0) {
@@ -657,20 +666,20 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
             // lists ≤ 2048: 512 threads, 4 CTAs / SM; (2048, 4096]: 1024 threads, 2 CTAs / SM;
             // longer lists and flagged tiles: the radix kernel on global scratch / 8192 on chip
             k_tile_sort_bucket<-1, 2048, 4096, 512><<<T, 512, bucket_smem(2048, 4096), s>>>(
-                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag);
+                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev);
             k_tile_sort_bucket<2048, kSortCap, 4096, 1024><<<T, 1024, bucket_smem(kSortCap, 4096), s>>>(
-                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag);
-            k_tile_sort<kSortCap, kSortCapBig, true><<<T, kBlock, kSortSmemBig, s>>>(
+                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev);
+            k_tile_sort<kSortCap, kSortCapBig, true><<<c.num_sms, kBlock, kSortSmemBig, s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists,
-                c.sub_count, c.tile_flag);
+                c.sub_count, c.tile_flag, c.dev);
             c.launches += 2;
         } else {
             k_tile_sort<-1, kSortCap, false><<<T, kBlock, kSortSmem, s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists,
-                c.sub_count, nullptr);
+                c.sub_count, nullptr, c.dev);
             k_tile_sort<kSortCap, kSortCapBig, true><<<T, kBlock, kSortSmemBig, s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists,
-                c.sub_count, nullptr);
+                c.sub_count, nullptr, c.dev);
             ++c.launches;
         }
     }

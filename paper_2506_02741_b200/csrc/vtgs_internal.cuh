@@ -37,6 +37,7 @@ struct DevScalars {
     unsigned int count_c;     // fused-L1 mask counts (normalize = 1)
     unsigned int count_d;
     unsigned int fin_ticket;  // k_pose_finalize last-block ticket (self-resetting)
+    unsigned int radix_count; // entries in the radix-sort work list (Ctx::tile_flag)
 };
 
 enum Stage { kProject = 0, kScan, kEmit, kSort, kCompFwd, kL1Count, kCompBwd, kFinalize, kInstantiate,
@@ -61,7 +62,7 @@ struct Ctx {
     uint32_t *tile_count = nullptr;  // [max_tiles]
     uint32_t *tile_start = nullptr;  // [max_tiles + 1]
     uint32_t *tile_cursor = nullptr; // [max_tiles]
-    uint32_t *tile_flag = nullptr;   // [max_tiles] bucket sort → radix sort hand-off
+    uint32_t *tile_flag = nullptr;   // [max_tiles] work list of the radix sort (long / degenerate tiles)
     uint32_t *keys = nullptr;        // bucket: z bits   [max_pairs]
     uint32_t *vals = nullptr;        // bucket: gid      [max_pairs] — sorted in place
     uint8_t *pbits = nullptr;        // bucket: the 8×4 sub-tiles of its tile the pair's rect touches [max_pairs]
