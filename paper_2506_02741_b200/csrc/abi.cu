@@ -111,7 +111,7 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = dalloc(&c.tile_count, (size_t)c.max_tiles);
     if (!e) e = dalloc(&c.tile_start, (size_t)c.max_tiles + 1);
     if (!e) e = dalloc(&c.tile_cursor, (size_t)c.max_tiles);
-    if (!e) e = dalloc(&c.tile_flag, (size_t)c.max_tiles);
+    if (!e) e = dalloc(&c.tile_flag, (size_t)2 * c.max_tiles);
     if (!e) e = dalloc(&c.keys, (size_t)max_pairs);
     if (!e) e = dalloc(&c.vals, (size_t)max_pairs);
     if (!e) e = dalloc(&c.pbits, (size_t)max_pairs);

@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t *__restrict__ tile
         tile_start[i] = overflow ? 0u : (uint32_t)run;
         cursor[i] = overflow ? 0u : (uint32_t)run;
         if (overflow) tile_count[i] = 0;
-        else if (c > (uint32_t)kSortCap) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)i;
+        else if (c > 8192u) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)i;
+        else if (c > (uint32_t)kSortCap) radix_list[T + atomicAdd(&dev->big_count, 1u)] = (uint32_t)i;
         run += c;
     }
     if (tid == 0) tile_start[T] = overflow ? 0u : (uint32_t)total_s;
@@ -505,18 +506,36 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
                                                          uint32_t *__restrict__ sub_lists,
                                                          uint32_t *__restrict__ sub_count,
                                                          uint32_t *__restrict__ radix_list,
-                                                         DevScalars *__restrict__ dev) {
+                                                         DevScalars *__restrict__ dev, int T) {
     constexpr int NW = NT / 32;
     constexpr int PT = NB / NT;
     static_assert(PT >= 1 && PT * NT == NB, "NB must be a multiple of NT");
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t red[4][32];
     __shared__ unsigned long long red64[2][33];
-    const int tile = blockIdx.x;
+    __shared__ int s_tile;
+    // LISTED (lists of 4097..8192 entries, rare except at high layer counts): a grid of one CTA
+    // per SM fetches the tiles k_scan_tiles listed, one at a time; otherwise one CTA per tile
+    constexpr bool LISTED = CAP > 4096;
+    for (int it = 0;; ++it) {
+    int tile;
+    if (LISTED) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned w = atomicAdd(&dev->big_next, 1u);
+            s_tile = w < dev->big_count ? (int)radix_list[T + w] : -1;
+        }
+        __syncthreads();
+        tile = s_tile;
+        if (tile < 0) return;
+    } else {
+        if (it > 0) return;
+        tile = blockIdx.x;
+    }
     const int n = (int)tile_count[tile];
-    if (n <= LO || n > CAP) return;
-    constexpr int kLogNB = NB == 4096 ? 12 : (NB == 2048 ? 11 : 10);
-    static_assert((1 << kLogNB) == NB, "NB must be 1024, 2048 or 4096");
+    if (n <= LO || n > CAP) continue;
+    constexpr int kLogNB = NB == 8192 ? 13 : (NB == 4096 ? 12 : (NB == 2048 ? 11 : 10));
+    static_assert((1 << kLogNB) == NB, "NB must be 1024 … 8192");
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t base = tile_start[tile];
     uint32_t *K = sm, *V = sm + CAP, *K2 = sm + 2 * CAP, *V2 = sm + 3 * CAP, *H = sm + 4 * CAP;
@@ -592,7 +611,7 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
     }
     if (cmax > (uint32_t)kMaxBucket) {   // degenerate depth distribution → the radix kernel's list
         if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;
-        return;
+        continue;
     }
     __syncthreads();
     for (int i = tid; i < n; i += NT) {
@@ -618,6 +637,7 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
     __syncthreads();
     for (int i = tid; i < n; i += NT) vals[base + i] = V[i];
     sublists_from_bits<NT>(V, B, n, sub_lists + (size_t)8 * base, sub_count + 8 * tile, red64);
+    }
 }
 
 constexpr int kSortCapBig = 8192;
@@ -666,9 +686,13 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
             // lists ≤ 2048: 512 threads, 4 CTAs / SM; (2048, 4096]: 1024 threads, 2 CTAs / SM;
             // longer lists and flagged tiles: the radix kernel on global scratch / 8192 on chip
             k_tile_sort_bucket<-1, 2048, 4096, 512><<<T, 512, bucket_smem(2048, 4096), s>>>(
-                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev);
+                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T);
             k_tile_sort_bucket<2048, kSortCap, 4096, 1024><<<T, 1024, bucket_smem(kSortCap, 4096), s>>>(
-                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev);
+                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T);
+            k_tile_sort_bucket<kSortCap, kSortCapBig, 8192, 1024><<<c.num_sms, 1024,
+                                                                    bucket_smem(kSortCapBig, 8192), s>>>(
+                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T);
+            ++c.launches;
             k_tile_sort<kSortCap, kSortCapBig, true><<<c.num_sms, kBlock, kSortSmemBig, s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists,
                 c.sub_count, c.tile_flag, c.dev);
@@ -697,6 +721,9 @@ cudaError_t forward_set_attributes() {
     if (!e)
         e = cudaFuncSetAttribute(k_tile_sort_bucket<2048, kSortCap, 4096, 1024>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, 4096));
+    if (!e)
+        e = cudaFuncSetAttribute(k_tile_sort_bucket<kSortCap, kSortCapBig, 8192, 1024>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCapBig, 8192));
     if (!e)
         e = cudaFuncSetAttribute(k_tile_sort<kSortCap, kSortCapBig, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBig);

@@ -38,6 +38,8 @@ struct DevScalars {
     unsigned int count_d;
     unsigned int fin_ticket;  // k_pose_finalize last-block ticket (self-resetting)
     unsigned int radix_count; // entries in the radix-sort work list (Ctx::tile_flag)
+    unsigned int big_count;   // entries in the 4097..8192 work list (Ctx::tile_flag + max_tiles)
+    unsigned int big_next;    // its dynamic fetch cursor
 };
 
 enum Stage { kProject = 0, kScan, kEmit, kSort, kCompFwd, kL1Count, kCompBwd, kFinalize, kInstantiate,
@@ -62,7 +64,7 @@ struct Ctx {
     uint32_t *tile_count = nullptr;  // [max_tiles]
     uint32_t *tile_start = nullptr;  // [max_tiles + 1]
     uint32_t *tile_cursor = nullptr; // [max_tiles]
-    uint32_t *tile_flag = nullptr;   // [max_tiles] work list of the radix sort (long / degenerate tiles)
+    uint32_t *tile_flag = nullptr;   // [2·max_tiles] work lists: radix sort (> 8192 / degenerate) | 4097..8192
     uint32_t *keys = nullptr;        // bucket: z bits   [max_pairs]
     uint32_t *vals = nullptr;        // bucket: gid      [max_pairs] — sorted in place
     uint8_t *pbits = nullptr;        // bucket: the 8×4 sub-tiles of its tile the pair's rect touches [max_pairs]
