@@ -194,36 +194,60 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             mj = lane_mask(Aj, cur.r, sx, sy) & onmask;
         }
         __syncwarp();
-        unsigned bits = transpose32(mj, lane);
-        // ---- phase 1: lane = pixel, back to front ----
-        while (bits) {
-            const int k = 31 - __clz(bits);
-            bits &= ~(1u << k);
-            float om = 0.f, dAe = 0.f;
-            if (bb + k < (int)L) {
-                const float4 A = sA[wl_][k];
-                const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
-                const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-                if (d2 <= A.z) {
-                    const float4 B = sB[wl_][k];
-                    const float wgt = fast_exp2(d2 * A.w);
-                    const float raw = __fmul_rn(B.w, wgt);
-                    const bool aclamp = raw > kAlphaMax;
-                    const float a = aclamp ? kAlphaMax : raw;
-                    if (a >= 1.0f / 255.0f) {
-                        const float oma = 1.0f - a;
-                        const float Ti = T * rcp_approx(oma);
-                        om = a * Ti;
-                        const float fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (sZ[wl_][k] - rz);
-                        // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
-                        dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
-                        Fb = a * fi + oma * Fb;
-                        Tb = oma * Tb;
-                        T = Ti;
-                    }
-                }
+        // candidates at positions ≥ the pixel's `last` were not composited: drop them from the
+        // lane's column (phase 1) and, through the transposed threshold masks, from each entry's
+        // pixel set (phase 2), so no zero pair is ever written or read for them
+        const int rem = (int)L - bb;
+        const unsigned alive = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+        unsigned bits = transpose32(mj, lane) & alive;
+        mj &= transpose32(alive, lane);
+        // ---- phase 1: lane = pixel, back to front, software-pipelined: the next candidate's
+        // loads, footprint, α, 1/(1−α) and f are computed (stage A, no loop-carried state) while
+        // the current one runs the recursion (stage B: T, Fb, Tb) ----
+        struct StA {
+            float a, rc, wgt, fi;
+            int k;
+            bool v, comp, aclamp;
+        };
+        auto stage_a = [&](StA &st) {
+            st.v = bits != 0u;
+            st.k = 31 - __clz(bits);
+            bits &= ~(1u << (st.k & 31));
+            float4 A, B;
+            float zk;
+            if (st.v) {   // predicated loads: lanes without a candidate add no shared-memory traffic
+                A = sA[wl_][st.k];
+                B = sB[wl_][st.k];
+                zk = sZ[wl_][st.k];
             }
-            M[k][lane] = make_float2(om, dAe);
+            const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
+            const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+            st.wgt = fast_exp2(d2 * A.w);
+            const float raw = __fmul_rn(B.w, st.wgt);
+            st.aclamp = raw > kAlphaMax;
+            st.a = st.aclamp ? kAlphaMax : raw;
+            st.comp = st.v && d2 <= A.z && st.a >= 1.0f / 255.0f;
+            st.rc = rcp_approx(1.0f - st.a);
+            st.fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (zk - rz);
+        };
+        StA cs;
+        stage_a(cs);
+        while (cs.v) {
+            StA ns;
+            stage_a(ns);
+            float om = 0.f, dAe = 0.f;
+            if (cs.comp) {
+                const float oma = 1.0f - cs.a;
+                const float Ti = T * cs.rc;
+                om = cs.a * Ti;
+                // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
+                dAe = cs.aclamp ? 0.f : Ti * (cs.fi - Fb + Kr * Tb) * cs.wgt;
+                Fb = cs.a * cs.fi + oma * Fb;
+                Tb = oma * Tb;
+                T = Ti;
+            }
+            M[cs.k][lane] = make_float2(om, dAe);
+            cs = ns;
         }
         __syncwarp();
         // ---- phase 2: lane = entry, over the pixels its footprint covers ----
