@@ -256,26 +256,45 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             const float z = cur.pr.z;
             float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, sw2 = 0.f, swx = 0.f, swy = 0.f, dzd = 0.f;
             unsigned mm = __funnelshift_r(mj, mj, lane);  // rotate right by lane
-            while (mm) {
+            // software-pipelined: the next pixel's M and upstream loads are issued before the
+            // current pixel's terms are accumulated
+            struct StB {
+                float2 md;
+                float4 gp;
+                int i;
+                bool v;
+            };
+            auto fetch = [&](StB &st) {
+                st.v = mm != 0u;
                 const int r = __ffs(mm) - 1;
                 mm &= mm - 1u;
-                const int i = (r + (int)lane) & 31;
-                const float2 md = M[lane][i];
-                if (md.x == 0.f) continue;  // not composited (ω > 0 for every composited pair)
-                const float4 gp = sG[wl_][i];
-                dc0 = fmaf(gp.x, md.x, dc0);
-                dc1 = fmaf(gp.y, md.x, dc1);
-                dc2 = fmaf(gp.z, md.x, dc2);
-                dzd = fmaf(gp.w, md.x, dzd);
-                if (md.y != 0.f) {
-                    const float dx = (float)(sx + (i & 7)) - Aj.x, dy = (float)(sy + (i >> 3)) - Aj.y;
+                st.i = (r + (int)lane) & 31;
+                if (st.v) {
+                    st.md = M[lane][st.i];
+                    st.gp = sG[wl_][st.i];
+                }
+            };
+            StB cb;
+            fetch(cb);
+            while (cb.v) {
+                StB nb;
+                fetch(nb);
+                if (cb.md.x != 0.f) {   // composited (ω > 0 for every composited pair)
+                    const float2 md = cb.md;
+                    const float4 gp = cb.gp;
+                    dc0 = fmaf(gp.x, md.x, dc0);
+                    dc1 = fmaf(gp.y, md.x, dc1);
+                    dc2 = fmaf(gp.z, md.x, dc2);
+                    dzd = fmaf(gp.w, md.x, dzd);
+                    const float dx = (float)(sx + (cb.i & 7)) - Aj.x, dy = (float)(sy + (cb.i >> 3)) - Aj.y;
                     const float d2 = dx * dx + dy * dy;
-                    const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution)
+                    const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution; 0 when α clamped)
                     dop += dw;
                     sw2 = fmaf(dw, d2, sw2);
                     swx = fmaf(dw, dx, swx);
                     swy = fmaf(dw, dy, swy);
                 }
+                cb = nb;
             }
             // dL/dw·w = dL/dα·o·w;  ∂w/∂σ = w d²/σ³, ∂w/∂u = w (x−u)/σ², ∂w/∂v = w (y−v)/σ²
             const float s = fabsf(cur.pr.w);
