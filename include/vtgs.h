@@ -270,7 +270,9 @@ VTGS_API vtgs_status vtgs_export_tiles(vtgs_ctx *ctx, int64_t *tile_start, int32
  * by the context, runs render_fwd + fused-L1 render_bwd exactly as above, and copies the loss
  * (and, if d_pose_host is non-NULL, the 7 pose gradients) back to the host.  pos_rad /
  * col_opa / d_col_opa / d_radius / color / depth / silhouette are DEVICE buffers (the model
- * state and the outputs stay resident).  Synchronous (returns after the loss is on the host). */
+ * state and the outputs stay resident).  The targets upload on a context-owned second stream
+ * while projection, sort and forward run (the backward waits for them); host buffers should be
+ * pinned for the copy to be asynchronous.  Synchronous (returns after the loss is on the host). */
 VTGS_API vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col_opa, int64_t N,
                            const vtgs_pose *view_host, vtgs_intrinsics intr,
                            const float *target_rgb_host, const float *target_depth_host,

@@ -155,6 +155,9 @@ vtgs_status vtgs_destroy(vtgs_ctx *ctx) {
             cudaEventDestroy(ev.a);
             cudaEventDestroy(ev.b);
         }
+    if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
+    if (ctx->c.ev_ready) cudaEventDestroy(ctx->c.ev_ready);
+    if (ctx->c.ev_copied) cudaEventDestroy(ctx->c.ev_copied);
     free_all(ctx->c);
     delete ctx;
     return VTGS_OK;
@@ -440,12 +443,25 @@ vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col
     float *d_dpose = d_misc + 16;
     cudaStream_t s = (cudaStream_t)stream;
     cudaSetDevice(c.device);
-    cudaError_t e = cudaMemcpyAsync(d_rgb, target_rgb_host, sizeof(float) * 3 * px, cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaMemcpyAsync(d_dep, target_depth_host, sizeof(float) * px, cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaMemcpyAsync(d_view, view_host, sizeof(vtgs_pose), cudaMemcpyHostToDevice, s);
+    cudaError_t e = cudaSuccess;
+    if (!c.copy_stream) {
+        e = cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking);
+        if (!e) e = cudaEventCreateWithFlags(&c.ev_ready, cudaEventDisableTiming);
+        if (!e) e = cudaEventCreateWithFlags(&c.ev_copied, cudaEventDisableTiming);
+        if (e) return cuda_fail(ctx, e, "vtgs_step_host (copy stream)");
+    }
+    // the pose goes first on the compute stream; the targets (read only by the backward's loss
+    // prologue) upload on a second stream while projection, sort and forward run
+    e = cudaMemcpyAsync(d_view, view_host, sizeof(vtgs_pose), cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaEventRecord(c.ev_ready, s);   // the previous step's backward is done with d_rgb / d_dep
+    if (!e) e = cudaStreamWaitEvent(c.copy_stream, c.ev_ready, 0);
+    if (!e) e = cudaMemcpyAsync(d_rgb, target_rgb_host, sizeof(float) * 3 * px, cudaMemcpyHostToDevice, c.copy_stream);
+    if (!e) e = cudaMemcpyAsync(d_dep, target_depth_host, sizeof(float) * px, cudaMemcpyHostToDevice, c.copy_stream);
+    if (!e) e = cudaEventRecord(c.ev_copied, c.copy_stream);
     if (e) return cuda_fail(ctx, e, "vtgs_step_host (H2D)");
     st = vtgs_render_fwd(ctx, pos_rad, col_opa, N, d_view, intr, color, depth, silhouette, stream);
     if (st) return st;
+    if ((e = cudaStreamWaitEvent(s, c.ev_copied, 0))) return cuda_fail(ctx, e, "vtgs_step_host (wait)");
     vtgs_l1_loss L{d_rgb, d_dep, nullptr, w_color, w_depth, color_mask_mode, depth_mask_mode, normalize, nullptr};
     st = vtgs_render_bwd(ctx, nullptr, nullptr, nullptr, &L, want & ~(uint32_t)VTGS_GRAD_POSITION, learn_begin,
                          learn_end, d_col_opa, d_radius, nullptr, (want & VTGS_GRAD_POSE) ? d_dpose : nullptr, d_loss,

@@ -80,6 +80,8 @@ struct Ctx {
     double *ssim_partials = nullptr; // per-CTA Σ SSIM
     DevScalars *dev = nullptr;
     float *host_io = nullptr;        // step_host device staging (targets + pose)
+    cudaStream_t copy_stream = nullptr;  // step_host: target upload overlapped with the forward
+    cudaEvent_t ev_ready = nullptr, ev_copied = nullptr;
     vtgs_pose *view_copy = nullptr;  // the forward's view pose, copied on the device for the backward
     // remembered forward
     bool have_fwd = false;
