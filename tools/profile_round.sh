@@ -11,6 +11,6 @@ python bench.py --ssim 0.2 --steps 50 --warmup 3 --no-cpu-baseline > gpurun_out/
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv \
     python bench.py --steps 2 --warmup 1 --profile-run > gpurun_out/${TAG}_ncu_launches.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_project_count|k_emit_pairs|k_tile_sort_bucket|k_composite_fwd_ring|k_composite_bwd" -c 6 \
+    -k regex:"k_project_count|k_emit_pairs|k_tile_sort_bucket|k_composite_fwd_ring|k_composite_bwd" -c 8 \
     -o gpurun_out/${TAG}_kernels -f python bench.py --steps 1 --warmup 1 --profile-run > gpurun_out/${TAG}_ncu_full.log 2>&1
 ls -la gpurun_out

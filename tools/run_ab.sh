@@ -1,6 +1,3 @@
-python -m pytest tests -m gpu -x -q -k "step_host" 2>&1 | grep -E "Error|assert|FAILED|passed|failed|^E " | head -30
-python bench.py --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/b.json 2>gpurun_out/b.err
-python - <<PY
-import json; d=json.load(open("gpurun_out/b.json")); s=d["stages"]
-print(round(d["ms_per_step"],4), d["value"], d["e2e"])
-PY
+ncu --set full --clock-control none --import-source on \
+    -k regex:"k_project_count|k_emit_pairs|k_tile_sort_bucket|k_composite_fwd_ring|k_composite_bwd" -c 8 \
+    -o gpurun_out/r01c_kernels -f python bench.py --steps 1 --warmup 1 --profile-run > gpurun_out/r01c_ncu_full.log 2>&1
