@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 16) k_composite_fwd(FwdArgs p)
 // (R batches ahead of the slowest live lane).  Compared with walking batch by batch in lock
 // step (the warp runs max-over-lanes candidates per batch), the warp runs ≈ max-over-lanes of
 // the whole-list candidate count — tools/sim_batches.py: lane efficiency 0.27 → 0.87 at R = 16.
-constexpr int kInner = 4;                      // lane-independent steps between warp checks
+constexpr int kInner = 6;                      // lane-independent steps between warp checks
 constexpr float kExpScale9 = -4.5f * kLog2e;  // −log2(e)/(2σ²) = kExpScale9 / (9σ²)
 
 template <int R>

@@ -1,3 +1,8 @@
-ncu --set full --clock-control none --import-source on \
-    -k regex:"k_project_count|k_emit_pairs|k_tile_sort_bucket|k_composite_fwd_ring|k_composite_bwd" -c 8 \
-    -o gpurun_out/r01c_kernels -f python bench.py --steps 1 --warmup 1 --profile-run > gpurun_out/r01c_ncu_full.log 2>&1
+for ki in 2 6 8; do
+  cp tools/ab_libs/libvtgs_k$ki.so paper_2506_02741_b200/libvtgs.so
+  python bench.py --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/b.json 2>gpurun_out/b.err
+  python - <<PY
+import json; d=json.load(open("gpurun_out/b.json")); s=d["stages"]
+print("$ki", round(d["ms_per_step"],4), round(s["composite_fwd"]["ms_per_launch"],4))
+PY
+done
