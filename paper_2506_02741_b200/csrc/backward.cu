@@ -11,6 +11,8 @@
 //   * pose gradient (tracking): each lane chains its pairs straight into 12 register
 //     accumulators (Σ g, Σ X_c gᵀ), reduced per CTA in fp64 into a per-tile partial; a
 //     one-CTA kernel sums the partials in a fixed order and applies the rotation chain.
+#include <stdlib.h>
+
 #include "composite_common.cuh"
 
 namespace vtgs {
@@ -349,6 +351,153 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Pose-only backward (tracking, Eq. 1: "keep all Gaussians in the scene fixed, and merely
+// optimize the pose").  The pose gradient is linear in the per-pair terms, so
+// each composited pair's dL/dX_c contribution goes straight into the lane's 12 accumulators
+// (Σ g, Σ X_c gᵀ) from the recursion of phase 1: no per-Gaussian reduction, no M matrix, no
+// phase 2, and a third of the shared memory (occupancy).  Per entry the build stores the
+// chain's constants: fx/z, fy/z, (u − cx)/z, (v − cy)/z, o/σ², [σ unclamped]/z and X_c; per pair
+//   q = (o/σ²)·dL/dα·w,  g = (q·dx·fx/z, q·dy·fy/z, g_D·ω − q·dx·(u−cx)/z − q·dy·(v−cy)/z − q·d²·[1/z])
+// (the same chain k_composite_bwd applies per (Gaussian, sub-tile) after summing the pairs).
+// ------------------------------------------------------------------------------------------
+template <bool LOSS>
+__global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p) {
+    __shared__ float4 sA[kBwdWarps][32];   // u, v, 9σ², −log2(e)/(2σ²)
+    __shared__ float4 sB[kBwdWarps][32];   // c, o
+    __shared__ float sZ[kBwdWarps][32];
+    __shared__ float4 sP1[kBwdWarps][32];  // fx/z, fy/z, (u − cx)/z, (v − cy)/z
+    __shared__ float4 sP2[kBwdWarps][32];  // X_c (x, y, z), o/σ²
+    __shared__ float sP3[kBwdWarps][32];   // 1/z if σ unclamped else 0
+    const int wl_ = threadIdx.x >> 5;
+    const int gsub = blockIdx.x * kBwdWarps + wl_;
+    const int tile = gsub >> 3;
+    const int sub = gsub & 7;
+    const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
+    const unsigned lane = lane_id();
+    const int sx = tx * kTile + (sub & 1) * 8, sy = ty * kTile + (sub >> 1) * 4;
+    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const bool inside = px < p.W && py < p.H;
+    const float pxf = (float)px, pyf = (float)py;
+    const int n = (int)p.tile_count[tile];
+    const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
+    const int cnt = (int)p.sub_count[tile * 8 + sub];
+    PoseR P;
+    pose_rotation(*p.view, P);
+
+    const PixelUp up = pixel_upstream<LOSS>(p, px, py, inside);
+    const float g0 = up.g0, g1 = up.g1, g2 = up.g2, gD = up.gD, gS = up.gS;
+    const float r0 = up.r0, r1 = up.r1, r2 = up.r2, rz = up.rz;
+    float T = up.T;
+    const bool on = inside && up.L > 0 && (g0 != 0.f || g1 != 0.f || g2 != 0.f || gD != 0.f || gS != 0.f);
+    const uint32_t L = on ? up.L : 0u;
+    const unsigned onmask = __ballot_sync(kFullMask, on);
+    const int wmax = (int)__reduce_max_sync(kFullMask, L);
+    float Fb = 0.f, Tb = 1.0f;
+    const float Kr = g0 * r0 + g1 * r1 + g2 * r2 + gD * rz + gS;
+    float h0 = 0.f, h1 = 0.f, h2 = 0.f;
+    float K00 = 0.f, K01 = 0.f, K02 = 0.f, K10 = 0.f, K11 = 0.f, K12 = 0.f, K20 = 0.f, K21 = 0.f, K22 = 0.f;
+
+    const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
+    EntryRegs nxt;
+    fetch_entry(nxt, list, bb_top + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    for (int bb = bb_top; bb >= 0; bb -= 32) {
+        const EntryRegs cur = nxt;
+        fetch_entry(nxt, list, bb - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        unsigned mj = 0u;
+        if (bb + (int)lane < wmax) {
+            const float4 Aj = entry_geom(cur.pr);
+            sA[wl_][lane] = Aj;
+            sB[wl_][lane] = cur.co;
+            sZ[wl_][lane] = cur.pr.z;
+            float xc[3];
+            view_transform(P.R, P.t, __ldg(p.pos_rad + cur.g), xc);
+            const float z = cur.pr.z, s = fabsf(cur.pr.w), iz = 1.0f / z;
+            sP1[wl_][lane] = make_float4(p.in.fx * iz, p.in.fy * iz, (Aj.x - p.in.cx) * iz, (Aj.y - p.in.cy) * iz);
+            sP2[wl_][lane] = make_float4(xc[0], xc[1], xc[2], cur.co.w / (s * s));
+            sP3[wl_][lane] = cur.pr.w > 0.f ? iz : 0.f;   // ∂σ/∂z = −σ/z only when σ is unclamped
+            mj = lane_mask(Aj, cur.r, sx, sy) & onmask;
+        }
+        __syncwarp();
+        const int rem = (int)L - bb;
+        const unsigned alive = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+        unsigned bits = transpose32(mj, lane) & alive;
+        // software-pipelined as k_composite_bwd's phase 1
+        struct StA {
+            float a, rc, wgt, fi, dx, dy, d2;
+            int k;
+            bool v, comp, aclamp;
+        };
+        auto stage_a = [&](StA &st) {
+            st.v = bits != 0u;
+            st.k = 31 - __clz(bits);
+            bits &= ~(1u << (st.k & 31));
+            float4 A, B;
+            float zk;
+            if (st.v) {
+                A = sA[wl_][st.k];
+                B = sB[wl_][st.k];
+                zk = sZ[wl_][st.k];
+            }
+            st.dx = __fsub_rn(pxf, A.x);
+            st.dy = __fsub_rn(pyf, A.y);
+            st.d2 = __fadd_rn(__fmul_rn(st.dx, st.dx), __fmul_rn(st.dy, st.dy));
+            st.wgt = fast_exp2(st.d2 * A.w);
+            const float raw = __fmul_rn(B.w, st.wgt);
+            st.aclamp = raw > kAlphaMax;
+            st.a = st.aclamp ? kAlphaMax : raw;
+            st.comp = st.v && st.d2 <= A.z && st.a >= 1.0f / 255.0f;
+            st.rc = rcp_approx(1.0f - st.a);
+            st.fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (zk - rz);
+        };
+        StA cs;
+        stage_a(cs);
+        while (cs.v) {
+            StA ns;
+            stage_a(ns);
+            if (cs.comp) {
+                const float oma = 1.0f - cs.a;
+                const float Ti = T * cs.rc;
+                const float om = cs.a * Ti;
+                const float dAe = cs.aclamp ? 0.f : Ti * (cs.fi - Fb + Kr * Tb) * cs.wgt;
+                Fb = cs.a * cs.fi + oma * Fb;
+                Tb = oma * Tb;
+                T = Ti;
+                const float4 c1 = sP1[wl_][cs.k], c2 = sP2[wl_][cs.k];
+                const float kz = sP3[wl_][cs.k];
+                const float q = c2.w * dAe;
+                const float du = q * cs.dx, dv = q * cs.dy;
+                const float gx = du * c1.x, gy = dv * c1.y;
+                const float gz = gD * om - du * c1.z - dv * c1.w - q * cs.d2 * kz;
+                h0 += gx; h1 += gy; h2 += gz;
+                K00 = fmaf(c2.x, gx, K00); K01 = fmaf(c2.x, gy, K01); K02 = fmaf(c2.x, gz, K02);
+                K10 = fmaf(c2.y, gx, K10); K11 = fmaf(c2.y, gy, K11); K12 = fmaf(c2.y, gz, K12);
+                K20 = fmaf(c2.z, gx, K20); K21 = fmaf(c2.z, gy, K21); K22 = fmaf(c2.z, gz, K22);
+            }
+            cs = ns;
+        }
+        __syncwarp();
+    }
+
+    __shared__ double sRed[kBwdWarps][13];   // fixed-order reduction: lanes → warp → CTA
+    double v[13] = {h0, h1, h2, K00, K01, K02, K10, K11, K12, K20, K21, K22, up.lossv};
+#pragma unroll
+    for (int q = 0; q < 13; ++q) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(kFullMask, v[q], o);
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 13; ++q) sRed[wl_][q] = v[q];
+    __syncthreads();
+    if (threadIdx.x < 13) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < kBwdWarps; ++i) s += sRed[i][threadIdx.x];
+        p.partials[(size_t)blockIdx.x * 16 + threadIdx.x] = s;
+    }
+}
+
 // mask counts for the mean-normalised loss (normalize = 1)
 __global__ void __launch_bounds__(256) k_l1_count(const float *__restrict__ sil, const float *__restrict__ tD,
                                                   const uint8_t *__restrict__ vis, int npx, int cmode,
@@ -468,6 +617,15 @@ __global__ void __launch_bounds__(kFinThreads) k_pose_finalize(const double *__r
 
 constexpr size_t kBwdDynSmem = sizeof(float2) * kBwdWarps * 32 * 32;
 
+static bool pose_direct() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("VTGS_BWD_POSE");
+        v = e ? atoi(e) : 1;   // 1: pose-only kernel for tracking; 0: the general two-phase kernel
+    }
+    return v != 0;
+}
+
 template <bool A, bool P, bool L>
 static void launch_bwd_t(const BwdArgs &a, int T, cudaStream_t s) {
     k_composite_bwd<A, P, L><<<T * (8 / kBwdWarps), kBwdWarps * 32, kBwdDynSmem, s>>>(a);
@@ -526,6 +684,11 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     const bool X = (want & VTGS_GRAD_POSITION) != 0 && d_position != nullptr;   // same chain as the pose
     if (!X) a.want &= ~(uint32_t)VTGS_GRAD_POSITION;
     const int sel = (A ? 4 : 0) | ((P || X) ? 2 : 0) | (L ? 1 : 0);
+    if (P && !A && !X && pose_direct()) {   // tracking: pose-only backward without the per-Gaussian reduction
+        LaunchScope ls(&c, kCompBwd, s);
+        if (L) k_composite_bwd_pose<true><<<T * (8 / kBwdWarps), kBwdWarps * 32, 0, s>>>(a);
+        else k_composite_bwd_pose<false><<<T * (8 / kBwdWarps), kBwdWarps * 32, 0, s>>>(a);
+    } else {
     {
     LaunchScope ls(&c, kCompBwd, s);
     switch (sel) {
@@ -537,6 +700,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
         case 5: launch_bwd_t<true, false, true>(a, T, s); break;
         case 6: launch_bwd_t<true, true, false>(a, T, s); break;
         default: launch_bwd_t<true, true, true>(a, T, s); break;
+    }
     }
     }
     if ((err = cudaGetLastError())) return err;

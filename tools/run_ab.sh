@@ -1,8 +1,8 @@
-for ki in 2 6 8; do
-  cp tools/ab_libs/libvtgs_k$ki.so paper_2506_02741_b200/libvtgs.so
-  python bench.py --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/b.json 2>gpurun_out/b.err
-  python - <<PY
-import json; d=json.load(open("gpurun_out/b.json")); s=d["stages"]
-print("$ki", round(d["ms_per_step"],4), round(s["composite_fwd"]["ms_per_launch"],4))
+python -m pytest tests -m gpu -x -q -k "backward or loss or deterministic or tracking or step_host or position or pretrack" 2>&1 | grep -E "Error|assert|FAILED|passed|failed|^E " | head -30
+for v in 1; do
+VTGS_BWD_POSE=$v python bench.py --config 3 --steps 10 --warmup 3 > gpurun_out/t$v.json 2>gpurun_out/t$v.err
+python - <<PY
+import json; d=json.load(open("gpurun_out/t$v.json"))
+print("$v", round(d["ms_per_step"],3), d["tracking"], {k: round(v,3) for k,v in d["stages_eager_frame_ms"].items()})
 PY
 done
