@@ -1,8 +1,6 @@
-python -m pytest tests -m gpu -x -q -k "backward or loss or deterministic or tracking or step_host or position or pretrack" 2>&1 | grep -E "Error|assert|FAILED|passed|failed|^E " | head -30
-for v in 1; do
-VTGS_BWD_POSE=$v python bench.py --config 3 --steps 10 --warmup 3 > gpurun_out/t$v.json 2>gpurun_out/t$v.err
+python -m pytest tests -m gpu -x -q -k "ssim or mapping_objective" 2>&1 | grep -E "Error|assert|FAILED|passed|failed|^E " | head -30
+python bench.py --ssim 0.2 --steps 30 --warmup 3 --no-cpu-baseline > gpurun_out/bs.json 2>gpurun_out/bs.err
 python - <<PY
-import json; d=json.load(open("gpurun_out/t$v.json"))
-print("$v", round(d["ms_per_step"],3), d["tracking"], {k: round(v,3) for k,v in d["stages_eager_frame_ms"].items()})
+import json; d=json.load(open("gpurun_out/bs.json")); s=d["stages"]
+print(round(d["ms_per_step"],4), {k: round(v["ms_per_launch"],4) for k,v in s.items()})
 PY
-done
