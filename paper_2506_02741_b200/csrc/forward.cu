@@ -661,8 +661,12 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     if ((err = cudaMemsetAsync(c.tile_count, 0, sizeof(uint32_t) * T, s))) return err;
     if ((err = cudaMemsetAsync(c.dev, 0, sizeof(DevScalars), s))) return err;
     const int64_t N = c.N;
-    int gN = (int)((N + 255) / 256);
-    if (gN > c.num_sms * 16) gN = c.num_sms * 16;
+    // projection: a capped grid (its CTAs each derive the view rotation in fp64 first); emit: one
+    // Gaussian per thread, many CTAs in flight hiding the load latency
+    int64_t gN64 = (N + 255) / 256;
+    if (gN64 > (int64_t)1 << 30) gN64 = (int64_t)1 << 30;
+    const int gE = (int)gN64;
+    const int gN = (int)(gN64 < (int64_t)c.num_sms * 16 ? gN64 : (int64_t)c.num_sms * 16);
     if (N > 0) {
         LaunchScope ls(&c, kProject, s);
         k_project_count<<<gN, 256, 0, s>>>(c.pos_rad, N, c.view, c.intr, ntx, c.proj, c.rect, c.tile_count);
@@ -676,7 +680,7 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     if ((err = cudaGetLastError())) return err;
     if (N > 0) {
         LaunchScope ls(&c, kEmit, s);
-        k_emit_pairs<<<gN, 256, 0, s>>>(c.proj, c.rect, N, ntx, c.tile_cursor, c.keys, c.vals, c.pbits, c.dev);
+        k_emit_pairs<<<gE, 256, 0, s>>>(c.proj, c.rect, N, ntx, c.tile_cursor, c.keys, c.vals, c.pbits, c.dev);
         if ((err = cudaGetLastError())) return err;
     }
     {
