@@ -39,6 +39,37 @@ __device__ __forceinline__ void fetch_entry(EntryRegs &er, const uint32_t *__res
     }
 }
 
+// Two-level prefetch along a sub-list: the gid of the batch after next is loaded one batch
+// earlier than its attributes (a gather through that gid), so a build never waits on the
+// dependent list → gid → attribute chain, only on loads issued a whole batch before.
+struct EntryStream {
+    EntryRegs e;   // entry (this lane's) of the next batch to build
+    uint32_t gn;   // gid of the batch after it
+    bool gv;
+};
+
+__device__ __forceinline__ void stream_start(EntryStream &s, const uint32_t *__restrict__ list, int idx0, int idx1,
+                                             int n, const float4 *__restrict__ proj, const float4 *__restrict__ col,
+                                             const uint2 *__restrict__ rect) {
+    fetch_entry(s.e, list, idx0, n, proj, col, rect);
+    s.gv = idx1 >= 0 && idx1 < n;
+    if (s.gv) s.gn = __ldg(list + idx1);
+}
+
+// e ← the attributes of gid gn; gn ← the gid at idx2
+__device__ __forceinline__ void stream_next(EntryStream &s, const uint32_t *__restrict__ list, int idx2, int n,
+                                            const float4 *__restrict__ proj, const float4 *__restrict__ col,
+                                            const uint2 *__restrict__ rect) {
+    if (s.gv) {
+        s.e.g = s.gn;
+        s.e.pr = __ldg(proj + s.gn);
+        s.e.co = __ldg(col + s.gn);
+        s.e.r = __ldg(rect + s.gn);
+    }
+    s.gv = idx2 >= 0 && idx2 < n;
+    if (s.gv) s.gn = __ldg(list + idx2);
+}
+
 // (u, v, 9σ² exact fp32 — the truncation threshold, −log2(e)/(2σ²))
 __device__ __forceinline__ float4 entry_geom(const float4 pr) {
     const float s = fabsf(pr.w);

@@ -155,8 +155,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     const int nb = (cnt + 31) >> 5;
     const unsigned inmask = __ballot_sync(kFullMask, inside);
 
-    EntryRegs nxt;
-    fetch_entry(nxt, list, (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    EntryStream st;
+    stream_start(st, list, (int)lane, 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    const EntryRegs &nxt = st.e;
     int built = 0;
     // build batch `built` from the prefetched registers, prefetch the one after it
     auto build = [&]() {
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
         }
         ring.bits[slot + lane] = __brev(transpose32(mj, lane));  // bit 31 − j = entry j
         ++built;
-        fetch_entry(nxt, list, built * 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        stream_next(st, list, (built + 1) * 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
     };
     while (built < nb && built < R) build();
     __syncwarp();

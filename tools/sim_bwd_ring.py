@@ -32,6 +32,8 @@ def main(n_sub=300, seed=0):
     confs = [(R, C) for R in (2, 4, 8, 16) for C in (1024, 2048, 4096)]
     steps = {c: 0 for c in confs}
     lock = 0
+    wins = [(2, 1024), (4, 1024), (4, 2048), (8, 2048)]
+    lockw = {w: 0 for w in wins}
     ideal = 0.0
     pairs_per_batch = []
     for _ in range(n_sub):
@@ -77,6 +79,16 @@ def main(n_sub=300, seed=0):
         pairs_per_batch += bp
         for b in range(nb):
             lock += bits[:, 32 * b:32 * b + 32].sum(1).max()
+        # lock-step over windows of up to 4 batches whose pairs fit in C (back to front)
+        for (Wn, Cw) in wins:
+            b = nb - 1
+            while b >= 0:
+                lo_b, tot = b, bp[b]
+                while b - (lo_b - 1) < Wn and lo_b - 1 >= 0 and tot + bp[lo_b - 1] <= Cw:
+                    lo_b -= 1
+                    tot += bp[lo_b]
+                lockw[(Wn, Cw)] += bits[:, 32 * lo_b:32 * b + 32].sum(1).max()
+                b = lo_b - 1
         # back to front: batch order nb-1 .. 0 ; per lane sequence of (batch) of its candidates
         seqs = [[k // 32 for k in np.nonzero(bits[l])[0][::-1]] for l in range(32)]
         for (R, C) in confs:
@@ -104,6 +116,8 @@ def main(n_sub=300, seed=0):
     print(f"ideal warp steps {ideal:.0f}; lock-step per batch {lock}  eff {ideal / lock:.2f}")
     pb = np.array(pairs_per_batch)
     print(f"pairs per batch: mean {pb.mean():.0f}  p99 {np.percentile(pb, 99):.0f}  max {pb.max()}")
+    for w in wins:
+        print(f"lock-step window <= {w[0]} batches, <= {w[1]} pairs: steps {lockw[w]:8d}  eff {ideal / lockw[w]:.2f}")
     for c in confs:
         print(f"ring R={c[0]:2d} C={c[1]:5d}: steps {steps[c]:8d}  eff {ideal / steps[c]:.2f}")
 
