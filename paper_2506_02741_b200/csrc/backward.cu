@@ -498,6 +498,183 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Pose-only backward, ring walk.  k_composite_bwd_pose walks each 32-entry batch in lock step,
+// so the warp runs max-over-lanes candidates per batch (depth-sorted batches are spatially
+// coherent: a batch loads a few pixels).  With no per-Gaussian reduction there is no phase 2 to
+// synchronise on, so the lanes can walk back to front ACROSS batch boundaries at their own pace
+// over a ring of R resident batches, exactly like the forward's ring (k_composite_fwd_ring):
+// a lane only waits when it needs a batch not yet built and the ring is R batches ahead of the
+// slowest lane.  Per entry the slot keeps A = (u, v, 9σ², o), B = (c, z), Xq = (X_c, o/σ²) and
+// ±1/z (−: σ clamped, ∂σ/∂z = 0).  α is computed exactly as the forward ring computes it.
+// ------------------------------------------------------------------------------------------
+template <int R>
+struct PoseRing {
+    float4 A[R * 32];
+    float4 B[R * 32];
+    float4 Xq[R * 32];
+    float iz[R * 32];
+    uint32_t bits[R * 32];   // per lane: its candidates of the batch (bit k = entry k)
+};
+
+constexpr int kPoseRingWarps = 2;
+constexpr int kPoseInner = 4;
+constexpr float kExpScale9P = -4.5f * kLog2e;   // −log2(e)/(2σ²) = kExpScale9P / (9σ²), as the forward
+
+template <int R, bool LOSS>
+__global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring(BwdArgs p) {
+    extern __shared__ float4 pose_ring_smem[];
+    static_assert((R & (R - 1)) == 0, "ring depth must be a power of two");
+    const int wl_ = threadIdx.x >> 5;
+    PoseRing<R> &ring = reinterpret_cast<PoseRing<R> *>(pose_ring_smem)[wl_];
+    const int gsub = blockIdx.x * kPoseRingWarps + wl_;
+    const int tile = gsub >> 3;
+    const int sub = gsub & 7;
+    const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
+    const unsigned lane = lane_id();
+    const int sx = tx * kTile + (sub & 1) * 8, sy = ty * kTile + (sub >> 1) * 4;
+    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const bool inside = px < p.W && py < p.H;
+    const float pxf = (float)px, pyf = (float)py;
+    const int n = (int)p.tile_count[tile];
+    const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
+    const int cnt = (int)p.sub_count[tile * 8 + sub];
+    PoseR P;
+    pose_rotation(*p.view, P);
+
+    const PixelUp up = pixel_upstream<LOSS>(p, px, py, inside);
+    const float g0 = up.g0, g1 = up.g1, g2 = up.g2, gD = up.gD, gS = up.gS;
+    const float r0 = up.r0, r1 = up.r1, r2 = up.r2, rz = up.rz;
+    float T = up.T;
+    const bool on = inside && up.L > 0 && (g0 != 0.f || g1 != 0.f || g2 != 0.f || gD != 0.f || gS != 0.f);
+    const int L = on ? (int)up.L : 0;
+    const unsigned onmask = __ballot_sync(kFullMask, on);
+    const int wmax = (int)__reduce_max_sync(kFullMask, (unsigned)L);
+    const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
+    const int nb = (bb_top >> 5) + 1;   // batch t covers sub-list positions [bb_top − 32t, +32)
+    float Fb = 0.f, Tb = 1.0f;
+    const float Kr = g0 * r0 + g1 * r1 + g2 * r2 + gD * rz + gS;
+    float h0 = 0.f, h1 = 0.f, h2 = 0.f;
+    float K00 = 0.f, K01 = 0.f, K02 = 0.f, K10 = 0.f, K11 = 0.f, K12 = 0.f, K20 = 0.f, K21 = 0.f, K22 = 0.f;
+    const float fx = p.in.fx, fy = p.in.fy, cxp = p.in.cx, cyp = p.in.cy;
+
+    EntryStream st;
+    stream_start(st, list, bb_top + (int)lane, bb_top - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    float4 posn = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (bb_top + (int)lane >= 0 && bb_top + (int)lane < cnt) posn = __ldg(p.pos_rad + st.e.g);
+    int built = 0;
+    auto build = [&]() {
+        const int bb = bb_top - 32 * built;
+        const int slot = (built & (R - 1)) * 32;
+        unsigned mj = 0u;
+        if (bb + (int)lane < wmax) {   // wmax ≤ cnt
+            const EntryRegs &e = st.e;
+            const float s = fabsf(e.pr.w);
+            const float s2 = __fmul_rn(s, s);
+            const float4 A = make_float4(e.pr.x, e.pr.y, __fmul_rn(9.0f, s2), e.co.w);
+            ring.A[slot + lane] = A;
+            ring.B[slot + lane] = make_float4(e.co.x, e.co.y, e.co.z, e.pr.z);
+            float xc[3];
+            view_transform(P.R, P.t, posn, xc);
+            const float iz = 1.0f / e.pr.z;
+            ring.Xq[slot + lane] = make_float4(xc[0], xc[1], xc[2], e.co.w / s2);
+            ring.iz[slot + lane] = e.pr.w > 0.f ? iz : -iz;
+            mj = lane_mask(A, e.r, sx, sy) & onmask;
+        }
+        // positions ≥ the pixel's `last` were not composited
+        const int rem = L - bb;
+        const unsigned alive = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+        ring.bits[slot + lane] = transpose32(mj, lane) & alive;
+        ++built;
+        const int nidx = bb - 32 + (int)lane;
+        stream_next(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        if (nidx >= 0 && nidx < cnt) posn = __ldg(p.pos_rad + st.e.g);
+    };
+    while (built < nb && built < R) build();
+    __syncwarp();
+
+    int b = -1;
+    unsigned cur = 0u;
+    int soff = 0;
+    auto advance = [&]() {
+        ++b;
+        soff = (b & (R - 1)) * 32;
+        cur = ring.bits[soff + lane];
+    };
+    for (;;) {
+#pragma unroll
+        for (int it = 0; it < kPoseInner; ++it) {
+            if (cur == 0u && b + 1 < built) advance();
+            const bool has = cur != 0u;
+            const int k = 31 - __clz(cur);   // highest remaining entry (back to front)
+            cur &= ~(1u << (k & 31));
+            float4 A, B;
+            if (has) {   // predicated loads: idle lanes add no shared-memory traffic
+                A = ring.A[soff + k];
+                B = ring.B[soff + k];
+            }
+            const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
+            const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+            const float wgt = fast_exp2(d2 * (kExpScale9P * rcp_approx(A.z)));
+            const float raw = __fmul_rn(A.w, wgt);
+            const bool aclamp = raw > kAlphaMax;
+            const float a = aclamp ? kAlphaMax : raw;
+            const bool comp = has && d2 <= A.z && a >= 1.0f / 255.0f;
+            if (comp) {
+                const float4 Xq = ring.Xq[soff + k];
+                const float izs = ring.iz[soff + k];
+                const float oma = 1.0f - a;
+                const float Ti = T * rcp_approx(oma);
+                const float om = a * Ti;
+                const float fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (B.w - rz);
+                const float dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
+                Fb = a * fi + oma * Fb;
+                Tb = oma * Tb;
+                T = Ti;
+                const float iz = fabsf(izs), kz = izs > 0.f ? izs : 0.f;
+                const float q = Xq.w * dAe;
+                const float du = q * dx, dv = q * dy;
+                const float gx = du * fx * iz, gy = dv * fy * iz;
+                const float gz = gD * om - (du * (A.x - cxp) + dv * (A.y - cyp)) * iz - q * d2 * kz;
+                h0 += gx; h1 += gy; h2 += gz;
+                K00 = fmaf(Xq.x, gx, K00); K01 = fmaf(Xq.x, gy, K01); K02 = fmaf(Xq.x, gz, K02);
+                K10 = fmaf(Xq.y, gx, K10); K11 = fmaf(Xq.y, gy, K11); K12 = fmaf(Xq.y, gz, K12);
+                K20 = fmaf(Xq.z, gx, K20); K21 = fmaf(Xq.z, gy, K21); K22 = fmaf(Xq.z, gz, K22);
+            }
+        }
+        while (cur == 0u && b + 1 < built) advance();
+        const bool live = cur != 0u || b + 1 < nb;
+        if (!__any_sync(kFullMask, live)) break;
+        const bool blocked = cur == 0u && b + 1 < nb && b + 1 >= built;
+        if (__any_sync(kFullMask, blocked)) {
+            const int need = !live ? 0x7fffffff : (cur ? b : b + 1);   // earliest batch still needed
+            const int lo = (int)__reduce_min_sync(kFullMask, (unsigned)need);
+            if (built < nb && built < lo + R) {
+                while (built < nb && built < lo + R) build();
+                __syncwarp();
+            }
+        }
+    }
+
+    __shared__ double sRed[kPoseRingWarps][13];   // fixed-order reduction: lanes → warp → CTA
+    double v[13] = {h0, h1, h2, K00, K01, K02, K10, K11, K12, K20, K21, K22, up.lossv};
+#pragma unroll
+    for (int q = 0; q < 13; ++q) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(kFullMask, v[q], o);
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 13; ++q) sRed[wl_][q] = v[q];
+    __syncthreads();
+    if (threadIdx.x < 13) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < kPoseRingWarps; ++i) s += sRed[i][threadIdx.x];
+        p.partials[(size_t)blockIdx.x * 16 + threadIdx.x] = s;
+    }
+}
+
 // mask counts for the mean-normalised loss (normalize = 1)
 __global__ void __launch_bounds__(256) k_l1_count(const float *__restrict__ sil, const float *__restrict__ tD,
                                                   const uint8_t *__restrict__ vis, int npx, int cmode,
@@ -617,13 +794,13 @@ __global__ void __launch_bounds__(kFinThreads) k_pose_finalize(const double *__r
 
 constexpr size_t kBwdDynSmem = sizeof(float2) * kBwdWarps * 32 * 32;
 
-static bool pose_direct() {
+static int pose_direct() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("VTGS_BWD_POSE");
-        v = e ? atoi(e) : 1;   // 1: pose-only kernel for tracking; 0: the general two-phase kernel
+        v = e ? atoi(e) : 2;   // 2: pose-only ring kernel, 1: pose-only lock-step kernel, 0: the general two-phase kernel
     }
-    return v != 0;
+    return v;
 }
 
 template <bool A, bool P, bool L>
@@ -686,8 +863,17 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     const int sel = (A ? 4 : 0) | ((P || X) ? 2 : 0) | (L ? 1 : 0);
     if (P && !A && !X && pose_direct()) {   // tracking: pose-only backward without the per-Gaussian reduction
         LaunchScope ls(&c, kCompBwd, s);
-        if (L) k_composite_bwd_pose<true><<<T * (8 / kBwdWarps), kBwdWarps * 32, 0, s>>>(a);
-        else k_composite_bwd_pose<false><<<T * (8 / kBwdWarps), kBwdWarps * 32, 0, s>>>(a);
+        if (pose_direct() == 2) {
+            constexpr int R = 4;
+            const size_t sm = sizeof(PoseRing<R>) * kPoseRingWarps;
+            static_assert(kPoseRingWarps == kBwdWarps, "k_pose_finalize rows: one partial per CTA of kBwdWarps warps");
+            if (L) k_composite_bwd_pose_ring<R, true><<<T * (8 / kPoseRingWarps), kPoseRingWarps * 32, sm, s>>>(a);
+            else k_composite_bwd_pose_ring<R, false><<<T * (8 / kPoseRingWarps), kPoseRingWarps * 32, sm, s>>>(a);
+        } else if (L) {
+            k_composite_bwd_pose<true><<<T * (8 / kBwdWarps), kBwdWarps * 32, 0, s>>>(a);
+        } else {
+            k_composite_bwd_pose<false><<<T * (8 / kBwdWarps), kBwdWarps * 32, 0, s>>>(a);
+        }
     } else {
     {
     LaunchScope ls(&c, kCompBwd, s);

@@ -254,6 +254,27 @@ def test_backward_parity_upstream(vt, which):
 
 
 @pytest.mark.parametrize("which", [1, 2, 3])
+def test_backward_pose_only_upstream(vt, which):
+    """Pose-only backward (the tracking kernel, no per-Gaussian reduction) with explicit
+    upstream gradients: d_pose against the oracle's, attribute buffers untouched."""
+    cfg = cached_config(which)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    _render_gpu(vt, R, cfg, pr, co)
+    H, W = cfg.intr.height, cfg.intr.width
+    rng = np.random.default_rng(10 + which)
+    gC = rng.normal(size=(H, W, 3)).astype(np.float32)
+    gD = rng.normal(size=(H, W)).astype(np.float32)
+    gS = rng.normal(size=(H, W)).astype(np.float32)
+    dco, drad, dpose = _run_bwd(vt, R, cfg, vt.VTGS_GRAD_POSE, cfg.n_slots, dL_dcolor=torch.from_numpy(gC).cuda(),
+                                dL_ddepth=torch.from_numpy(gD).cuda(), dL_dsil=torch.from_numpy(gS).cuda())
+    assert not dco.any() and not drad.any()
+    opr, oco = oracle_instantiate(cfg)
+    ref, g = _oracle_grads(cfg, opr, oco, _view(cfg), gC, gD, gS)
+    _check_grads(vt.VTGS_GRAD_POSE, dco, drad, dpose, g, ref["tainted"], vt)
+
+
+@pytest.mark.parametrize("which", [1, 2, 3])
 def test_backward_parity_fused_l1(vt, which):
     """The config's own objective: masked L1 of Eq. 1 (tracking) / L1 terms of Eq. 2 (mapping),
     sum form (SURVEY §8(c) pin note), fused into the backward."""
