@@ -203,92 +203,69 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
         const unsigned alive = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
         unsigned bits = transpose32(mj, lane) & alive;
         mj &= transpose32(alive, lane);
-        // ---- phase 1: lane = pixel, back to front, software-pipelined: the next candidate's
-        // loads, footprint, α, 1/(1−α) and f are computed (stage A, no loop-carried state) while
-        // the current one runs the recursion (stage B: T, Fb, Tb) ----
-        struct StA {
-            float a, rc, wgt, fi;
-            int k;
-            bool v, comp, aclamp;
-        };
-        auto stage_a = [&](StA &st) {
-            st.v = bits != 0u;
-            st.k = 31 - __clz(bits);
-            bits &= ~(1u << (st.k & 31));
+        // ---- phase 1: lane = pixel, back to front, two candidates per iteration: both
+        // candidates' loads, footprint, α, 1/(1−α) and f carry no loop state and are computed
+        // together; the recursion (T, Fb, Tb) then runs over the two in order ----
+        auto stage_a = [&](int k, bool v, float &a, float &rc, float &wgt, float &fi, bool &comp, bool &aclamp) {
             float4 A, B;
             float zk;
-            if (st.v) {   // predicated loads: lanes without a candidate add no shared-memory traffic
-                A = sA[wl_][st.k];
-                B = sB[wl_][st.k];
-                zk = sZ[wl_][st.k];
+            if (v) {   // predicated loads: lanes without a candidate add no shared-memory traffic
+                A = sA[wl_][k];
+                B = sB[wl_][k];
+                zk = sZ[wl_][k];
             }
             const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
             const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-            st.wgt = fast_exp2(d2 * A.w);
-            const float raw = __fmul_rn(B.w, st.wgt);
-            st.aclamp = raw > kAlphaMax;
-            st.a = st.aclamp ? kAlphaMax : raw;
-            st.comp = st.v && d2 <= A.z && st.a >= 1.0f / 255.0f;
-            st.rc = rcp_approx(1.0f - st.a);
-            st.fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (zk - rz);
+            wgt = fast_exp2(d2 * A.w);
+            const float raw = __fmul_rn(B.w, wgt);
+            aclamp = raw > kAlphaMax;
+            a = aclamp ? kAlphaMax : raw;
+            comp = v && d2 <= A.z && a >= 1.0f / 255.0f;
+            rc = rcp_approx(1.0f - a);
+            fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (zk - rz);
         };
-        StA cs;
-        stage_a(cs);
-        while (cs.v) {
-            StA ns;
-            stage_a(ns);
+        auto stage_b = [&](int k, bool comp, bool aclamp, float a, float rc, float wgt, float fi) {
             float om = 0.f, dAe = 0.f;
-            if (cs.comp) {
-                const float oma = 1.0f - cs.a;
-                const float Ti = T * cs.rc;
-                om = cs.a * Ti;
+            if (comp) {
+                const float oma = 1.0f - a;
+                const float Ti = T * rc;
+                om = a * Ti;
                 // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
-                dAe = cs.aclamp ? 0.f : Ti * (cs.fi - Fb + Kr * Tb) * cs.wgt;
-                Fb = cs.a * cs.fi + oma * Fb;
+                dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
+                Fb = a * fi + oma * Fb;
                 Tb = oma * Tb;
                 T = Ti;
             }
-            M[cs.k][lane] = make_float2(om, dAe);
-            cs = ns;
+            M[k][lane] = make_float2(om, dAe);
+        };
+        while (bits) {
+            const int k0 = 31 - __clz(bits);
+            bits &= ~(1u << k0);
+            const bool v1 = bits != 0u;
+            const int k1 = (31 - __clz(bits)) & 31;
+            if (v1) bits &= ~(1u << k1);
+            float a0, rc0, w0, f0, a1, rc1, w1, f1;
+            bool c0, cl0, c1, cl1;
+            stage_a(k0, true, a0, rc0, w0, f0, c0, cl0);
+            stage_a(k1, v1, a1, rc1, w1, f1, c1, cl1);
+            stage_b(k0, c0, cl0, a0, rc0, w0, f0);
+            if (v1) stage_b(k1, c1, cl1, a1, rc1, w1, f1);
         }
         __syncwarp();
-        // ---- phase 2: lane = entry, over the pixels its footprint covers ----
+        // ---- phase 2: lane = entry, over the pixels its footprint covers, two pixels per
+        // iteration (both pixels' M and upstream loads issued before either is accumulated) ----
         if (mj) {
             const float4 B = cur.co;
             const float z = cur.pr.z;
             float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, sw2 = 0.f, swx = 0.f, swy = 0.f, dzd = 0.f;
             unsigned mm = __funnelshift_r(mj, mj, lane);  // rotate right by lane
-            // software-pipelined: the next pixel's M and upstream loads are issued before the
-            // current pixel's terms are accumulated
-            struct StB {
-                float2 md;
-                float4 gp;
-                int i;
-                bool v;
-            };
-            auto fetch = [&](StB &st) {
-                st.v = mm != 0u;
-                const int r = __ffs(mm) - 1;
-                mm &= mm - 1u;
-                st.i = (r + (int)lane) & 31;
-                if (st.v) {
-                    st.md = M[lane][st.i];
-                    st.gp = sG[wl_][st.i];
-                }
-            };
-            StB cb;
-            fetch(cb);
-            while (cb.v) {
-                StB nb;
-                fetch(nb);
-                if (cb.md.x != 0.f) {   // composited (ω > 0 for every composited pair)
-                    const float2 md = cb.md;
-                    const float4 gp = cb.gp;
+            auto accum = [&](int i, float2 md, float4 gp) {
+                if (md.x != 0.f) {   // composited (ω > 0 for every composited pair)
                     dc0 = fmaf(gp.x, md.x, dc0);
                     dc1 = fmaf(gp.y, md.x, dc1);
                     dc2 = fmaf(gp.z, md.x, dc2);
                     dzd = fmaf(gp.w, md.x, dzd);
-                    const float dx = (float)(sx + (cb.i & 7)) - Aj.x, dy = (float)(sy + (cb.i >> 3)) - Aj.y;
+                    const float dx = (float)(sx + (i & 7)) - Aj.x, dy = (float)(sy + (i >> 3)) - Aj.y;
                     const float d2 = dx * dx + dy * dy;
                     const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution; 0 when α clamped)
                     dop += dw;
@@ -296,7 +273,23 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
                     swx = fmaf(dw, dx, swx);
                     swy = fmaf(dw, dy, swy);
                 }
-                cb = nb;
+            };
+            while (mm) {
+                const int i0 = ((__ffs(mm) - 1) + (int)lane) & 31;
+                mm &= mm - 1u;
+                const bool v1 = mm != 0u;
+                const int i1 = ((__ffs(mm) - 1) + (int)lane) & 31;
+                mm &= mm - 1u;
+                const float2 md0 = M[lane][i0];
+                const float4 gp0 = sG[wl_][i0];
+                float2 md1 = make_float2(0.f, 0.f);
+                float4 gp1;
+                if (v1) {
+                    md1 = M[lane][i1];
+                    gp1 = sG[wl_][i1];
+                }
+                accum(i0, md0, gp0);
+                accum(i1, md1, gp1);   // md1.x == 0 when there is no second pixel
             }
             // dL/dw·w = dL/dα·o·w;  ∂w/∂σ = w d²/σ³, ∂w/∂u = w (x−u)/σ², ∂w/∂v = w (y−v)/σ²
             const float s = fabsf(cur.pr.w);
@@ -792,6 +785,26 @@ __global__ void __launch_bounds__(kFinThreads) k_pose_finalize(const double *__r
     }
 }
 
+// Loss only (mapping): the fixed-order sum of one column of the per-CTA partials, one CTA.
+constexpr int kLossThreads = 1024;
+__global__ void __launch_bounds__(kLossThreads) k_loss_finalize(const double *__restrict__ partials, int T,
+                                                                float *__restrict__ loss_out) {
+    __shared__ double red[kLossThreads / 32];
+    const int tid = threadIdx.x;
+    double acc = 0.0;
+    for (int t = tid; t < T; t += kLossThreads) acc += __ldg(partials + (size_t)t * 16 + 12);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid < 32) {
+        double v = red[tid];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        if (tid == 0) *loss_out = (float)v;
+    }
+}
+
 constexpr size_t kBwdDynSmem = sizeof(float2) * kBwdWarps * 32 * 32;
 
 static int pose_direct() {
@@ -893,7 +906,8 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     if (P || (L && loss_out)) {
         LaunchScope ls(&c, kFinalize, s);
         const int rows = T * (8 / kBwdWarps);
-        k_pose_finalize<<<kFinBlocks, kFinThreads, 0, s>>>(c.partials, rows, c.view_copy, P ? d_pose : nullptr,
+        if (!P) k_loss_finalize<<<1, kLossThreads, 0, s>>>(c.partials, rows, loss_out);
+        else k_pose_finalize<<<kFinBlocks, kFinThreads, 0, s>>>(c.partials, rows, c.view_copy, P ? d_pose : nullptr,
                                                            L ? loss_out : nullptr, c.partials + (size_t)c.max_tiles * 8 * 16,
                                                            &c.dev->fin_ticket);
         if ((err = cudaGetLastError())) return err;
