@@ -28,6 +28,7 @@ struct BwdArgs {
     const uint32_t *tile_start;
     const uint32_t *sub_lists;
     const uint32_t *sub_count;
+    const uint32_t *sub_masks;   // the forward's per-entry pixel masks
     int W, H, ntx;
     const float *color, *depth, *sil, *T_final;
     const uint32_t *last;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
     const float pxf = (float)px, pyf = (float)py;
     const int n = (int)p.tile_count[tile];
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
+    const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const int cnt = (int)p.sub_count[tile * 8 + sub];
     PoseR P;
     if (POSE) pose_rotation(*p.view, P);
@@ -176,10 +178,13 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
 
     const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
     EntryRegs nxt;
-    fetch_entry(nxt, list, bb_top + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    fetch_entry<false>(nxt, list, bb_top + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, cnt);
     for (int bb = bb_top; bb >= 0; bb -= 32) {
         const EntryRegs cur = nxt;
-        fetch_entry(nxt, list, bb - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);  // next (lower) batch
+        const uint32_t mcur = mnx;
+        fetch_entry<false>(nxt, list, bb - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        mnx = load_mask(mlist, bb - 32 + (int)lane, cnt);  // next (lower) batch
         const int jj = bb + (int)lane;
         unsigned mj = 0u;
         float4 Aj = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -193,7 +198,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
                 view_transform(P.R, P.t, __ldg(p.pos_rad + cur.g), xc);
                 sX[wl_][lane] = make_float4(xc[0], xc[1], xc[2], cur.pr.w);
             }
-            mj = lane_mask(Aj, cur.r, sx, sy) & onmask;
+            mj = mcur & onmask;
         }
         __syncwarp();
         // candidates at positions ≥ the pixel's `last` were not composited: drop them from the
@@ -374,6 +379,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p
     const float pxf = (float)px, pyf = (float)py;
     const int n = (int)p.tile_count[tile];
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
+    const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const int cnt = (int)p.sub_count[tile * 8 + sub];
     PoseR P;
     pose_rotation(*p.view, P);
@@ -393,10 +399,13 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p
 
     const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
     EntryRegs nxt;
-    fetch_entry(nxt, list, bb_top + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    fetch_entry<false>(nxt, list, bb_top + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, cnt);
     for (int bb = bb_top; bb >= 0; bb -= 32) {
         const EntryRegs cur = nxt;
-        fetch_entry(nxt, list, bb - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        const uint32_t mcur = mnx;
+        fetch_entry<false>(nxt, list, bb - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        mnx = load_mask(mlist, bb - 32 + (int)lane, cnt);
         unsigned mj = 0u;
         if (bb + (int)lane < wmax) {
             const float4 Aj = entry_geom(cur.pr);
@@ -409,7 +418,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p
             sP1[wl_][lane] = make_float4(p.in.fx * iz, p.in.fy * iz, (Aj.x - p.in.cx) * iz, (Aj.y - p.in.cy) * iz);
             sP2[wl_][lane] = make_float4(xc[0], xc[1], xc[2], cur.co.w / (s * s));
             sP3[wl_][lane] = cur.pr.w > 0.f ? iz : 0.f;   // ∂σ/∂z = −σ/z only when σ is unclamped
-            mj = lane_mask(Aj, cur.r, sx, sy) & onmask;
+            mj = mcur & onmask;
         }
         __syncwarp();
         const int rem = (int)L - bb;
@@ -531,6 +540,7 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
     const float pxf = (float)px, pyf = (float)py;
     const int n = (int)p.tile_count[tile];
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
+    const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const int cnt = (int)p.sub_count[tile * 8 + sub];
     PoseR P;
     pose_rotation(*p.view, P);
@@ -552,7 +562,8 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
     const float fx = p.in.fx, fy = p.in.fy, cxp = p.in.cx, cyp = p.in.cy;
 
     EntryStream st;
-    stream_start(st, list, bb_top + (int)lane, bb_top - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    stream_start<false>(st, list, bb_top + (int)lane, bb_top - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, cnt);
     float4 posn = make_float4(0.f, 0.f, 0.f, 0.f);
     if (bb_top + (int)lane >= 0 && bb_top + (int)lane < cnt) posn = __ldg(p.pos_rad + st.e.g);
     int built = 0;
@@ -572,7 +583,7 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
             const float iz = 1.0f / e.pr.z;
             ring.Xq[slot + lane] = make_float4(xc[0], xc[1], xc[2], e.co.w / s2);
             ring.iz[slot + lane] = e.pr.w > 0.f ? iz : -iz;
-            mj = lane_mask(A, e.r, sx, sy) & onmask;
+            mj = mnx & onmask;
         }
         // positions ≥ the pixel's `last` were not composited
         const int rem = L - bb;
@@ -580,7 +591,8 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
         ring.bits[slot + lane] = transpose32(mj, lane) & alive;
         ++built;
         const int nidx = bb - 32 + (int)lane;
-        stream_next(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        stream_next<false>(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        mnx = load_mask(mlist, nidx, cnt);
         if (nidx >= 0 && nidx < cnt) posn = __ldg(p.pos_rad + st.e.g);
     };
     while (built < nb && built < R) build();
@@ -849,6 +861,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     BwdArgs a{};
     a.proj = c.proj; a.rect = c.rect; a.col_opa = c.col_opa; a.pos_rad = c.pos_rad;
     a.tile_count = c.tile_count; a.tile_start = c.tile_start; a.sub_lists = c.sub_lists; a.sub_count = c.sub_count;
+    a.sub_masks = c.sub_masks;
     a.W = W; a.H = H; a.ntx = ntx;
     a.color = c.color; a.depth = c.depth; a.sil = c.sil; a.T_final = c.T_final; a.last = c.last;
     a.dC = dC; a.dD = dD; a.dS = dS;

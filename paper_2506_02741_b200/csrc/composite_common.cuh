@@ -28,6 +28,7 @@ struct EntryRegs {
     uint2 r;
 };
 
+template <bool RECT = true>
 __device__ __forceinline__ void fetch_entry(EntryRegs &er, const uint32_t *__restrict__ list, int idx, int n,
                                             const float4 *__restrict__ proj, const float4 *__restrict__ col,
                                             const uint2 *__restrict__ rect) {
@@ -35,7 +36,7 @@ __device__ __forceinline__ void fetch_entry(EntryRegs &er, const uint32_t *__res
         er.g = __ldg(list + idx);
         er.pr = __ldg(proj + er.g);
         er.co = __ldg(col + er.g);
-        er.r = __ldg(rect + er.g);
+        if (RECT) er.r = __ldg(rect + er.g);
     }
 }
 
@@ -48,15 +49,17 @@ struct EntryStream {
     bool gv;
 };
 
+template <bool RECT = true>
 __device__ __forceinline__ void stream_start(EntryStream &s, const uint32_t *__restrict__ list, int idx0, int idx1,
                                              int n, const float4 *__restrict__ proj, const float4 *__restrict__ col,
                                              const uint2 *__restrict__ rect) {
-    fetch_entry(s.e, list, idx0, n, proj, col, rect);
+    fetch_entry<RECT>(s.e, list, idx0, n, proj, col, rect);
     s.gv = idx1 >= 0 && idx1 < n;
     if (s.gv) s.gn = __ldg(list + idx1);
 }
 
 // e ← the attributes of gid gn; gn ← the gid at idx2
+template <bool RECT = true>
 __device__ __forceinline__ void stream_next(EntryStream &s, const uint32_t *__restrict__ list, int idx2, int n,
                                             const float4 *__restrict__ proj, const float4 *__restrict__ col,
                                             const uint2 *__restrict__ rect) {
@@ -64,10 +67,16 @@ __device__ __forceinline__ void stream_next(EntryStream &s, const uint32_t *__re
         s.e.g = s.gn;
         s.e.pr = __ldg(proj + s.gn);
         s.e.co = __ldg(col + s.gn);
-        s.e.r = __ldg(rect + s.gn);
+        if (RECT) s.e.r = __ldg(rect + s.gn);
     }
     s.gv = idx2 >= 0 && idx2 < n;
     if (s.gv) s.gn = __ldg(list + idx2);
+}
+
+// The forward stores each sub-list entry's pixel mask (lane_mask, below) next to the sub-list;
+// the backward reads it instead of recomputing it (same entry, same sub-tile, same mask).
+__device__ __forceinline__ uint32_t load_mask(const uint32_t *__restrict__ mlist, int idx, int n) {
+    return (idx >= 0 && idx < n) ? __ldg(mlist + idx) : 0u;
 }
 
 // (u, v, 9σ² exact fp32 — the truncation threshold, −log2(e)/(2σ²))

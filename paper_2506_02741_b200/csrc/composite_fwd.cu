@@ -16,6 +16,7 @@ struct FwdArgs {
     const uint32_t *tile_start;
     const uint32_t *sub_lists;
     const uint32_t *sub_count;
+    uint32_t *sub_masks;   // per sub-list entry: its 32-pixel lane_mask (read by the backward)
     int W, H, ntx;
     float *color, *depth, *sil, *T_final;
     uint32_t *last;
@@ -41,6 +42,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 16) k_composite_fwd(FwdArgs p)
     const float pxf = (float)px, pyf = (float)py;
     const int n = (int)p.tile_count[tile];
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)w * n;
+    uint32_t *mout = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)w * n;
     const int cnt = (int)p.sub_count[tile * 8 + w];
 
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f, Sl = 0.f;
@@ -59,7 +61,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 16) k_composite_fwd(FwdArgs p)
             sA[wl][lane] = A;
             sB[wl][lane] = cur.co;
             sZ[wl][lane] = cur.pr.z;
-            mj = lane_mask(A, cur.r, sx, sy) & active;
+            const unsigned m0 = lane_mask(A, cur.r, sx, sy);
+            mout[bb + lane] = m0;
+            mj = m0 & active;
         }
         __syncwarp();
         unsigned bits = transpose32(mj, lane);
@@ -151,6 +155,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     const float pxf = (float)px, pyf = (float)py;
     const int n = (int)p.tile_count[tile];
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)w * n;
+    uint32_t *mout = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)w * n;
     const int cnt = (int)p.sub_count[tile * 8 + w];
     const int nb = (cnt + 31) >> 5;
     const unsigned inmask = __ballot_sync(kFullMask, inside);
@@ -170,7 +175,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
             const float4 A = make_float4(nxt.pr.x, nxt.pr.y, s9, nxt.co.w);
             ring.A[slot + lane] = A;
             ring.B[slot + lane] = make_float4(nxt.co.x, nxt.co.y, nxt.co.z, nxt.pr.z);
-            mj = lane_mask(A, nxt.r, sx, sy) & inmask;
+            const unsigned m0 = lane_mask(A, nxt.r, sx, sy);
+            mout[idx] = m0;
+            mj = m0 & inmask;
         }
         ring.bits[slot + lane] = __brev(transpose32(mj, lane));  // bit 31 − j = entry j
         ++built;
@@ -302,7 +309,7 @@ static cudaError_t launch_ring(const FwdArgs &a, int T, bool stats, cudaStream_t
 cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
     const int W = c.intr.width, H = c.intr.height;
     const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile;
-    FwdArgs a{c.proj, c.rect, c.col_opa, c.tile_count, c.tile_start, c.sub_lists, c.sub_count, W, H, ntx,
+    FwdArgs a{c.proj, c.rect, c.col_opa, c.tile_count, c.tile_start, c.sub_lists, c.sub_count, c.sub_masks, W, H, ntx,
               c.color, c.depth, c.sil, c.T_final, c.last, c.dev};
     switch (fwd_variant()) {
         case 0:

@@ -71,6 +71,7 @@ struct Ctx {
     uint32_t *keys2 = nullptr;       // fallback sort scratch [max_pairs]
     uint32_t *vals2 = nullptr;
     uint32_t *offs = nullptr;        // fallback sort ranks [max_pairs]
+    uint32_t *sub_masks = nullptr;   // per sub-list entry: its 32-pixel mask (forward → backward) [8·max_pairs]
     uint32_t *sub_lists = nullptr;   // per tile 8 sub-lists (8×4 sub-tiles), capacity 8·n_tile [8·max_pairs]
     uint32_t *sub_count = nullptr;   // [8·max_tiles]
     float *T_final = nullptr;        // per pixel
