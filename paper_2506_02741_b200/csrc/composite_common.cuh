@@ -129,11 +129,10 @@ __device__ __forceinline__ unsigned subtile_bits(uint2 r, int tx0, int ty0) {
     const int x0 = (int)(r.x & 0xffffu), x1 = (int)(r.x >> 16);
     const int y0 = (int)(r.y & 0xffffu), y1 = (int)(r.y >> 16);
     const unsigned cols = (x0 <= tx0 + 7 ? 1u : 0u) | (x1 >= tx0 + 8 ? 2u : 0u);
-    unsigned wm = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        if (y0 <= ty0 + 4 * k + 3 && y1 >= ty0 + 4 * k) wm |= cols << (2 * k);
-    return wm;
+    // sub-tile rows k0 .. k1 the rect touches (the rect overlaps the tile: k0 ≤ 3, k1 ≥ 0)
+    const int k0 = max(y0 - ty0, 0) >> 2, k1 = min(y1 - ty0, 15) >> 2;
+    const unsigned rows = (0xffu >> (6 - 2 * k1)) & (0xffu << (2 * k0)) & 0x55u;   // bit 2k per row k
+    return ((cols & 1u) ? rows : 0u) | ((cols & 2u) ? rows << 1 : 0u);
 }
 
 }  // namespace vtgs

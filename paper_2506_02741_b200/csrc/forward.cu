@@ -81,12 +81,11 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
         const int tx0 = f.vis ? f.x0 >> 4 : 0, ty0 = f.vis ? f.y0 >> 4 : 0;
         const int ntg = f.vis ? (f.x1 >> 4) - tx0 + 1 : 0;
         const int cnt = f.vis ? ntg * ((f.y1 >> 4) - ty0 + 1) : 0;
+        // tiles in row-major order, (kx, ky) stepped incrementally (no integer division)
+        int kx = 0, trow = ty0 * ntx + tx0;
         for (int k = 0; __any_sync(kFull, k < cnt); ++k) {
-            int tile = -1;
-            if (k < cnt) {
-                const int dy = k / ntg;
-                tile = (ty0 + dy) * ntx + tx0 + (k - dy * ntg);
-            }
+            const int tile = k < cnt ? trow + kx : -1;
+            if (++kx == ntg) { kx = 0; trow += ntx; }
             const unsigned peers = __match_any_sync(kFull, tile);
             if (tile >= 0 && (int)lane_id() == __ffs(peers) - 1) atomicAdd(&tile_count[tile], (uint32_t)__popc(peers));
         }
@@ -192,12 +191,11 @@ __global__ void __launch_bounds__(256) k_emit_pairs(const float4 *__restrict__ p
                 zb = __float_as_uint(proj[g].z);
             }
         }
+        int kx = 0, ky = 0;   // (tile column, row) offsets stepped incrementally (no integer division)
         for (int k = 0; __any_sync(kFull, k < cnt); ++k) {
-            int tile = -1;
-            if (k < cnt) {
-                const int dy = k / ntg;
-                tile = (ty0 + dy) * ntx + tx0 + (k - dy * ntg);
-            }
+            const int tile = k < cnt ? (ty0 + ky) * ntx + tx0 + kx : -1;
+            const int tcx = tx0 + kx, tcy = ty0 + ky;
+            if (++kx == ntg) { kx = 0; ++ky; }
             const unsigned peers = __match_any_sync(kFull, tile);
             const int leader = __ffs(peers) - 1;
             uint32_t base = 0;
@@ -205,10 +203,9 @@ __global__ void __launch_bounds__(256) k_emit_pairs(const float4 *__restrict__ p
             base = __shfl_sync(kFull, base, leader);
             if (tile >= 0) {
                 const uint32_t slot = base + __popc(peers & lanemask_lt());
-                const int tyy = tile / ntx;
                 keys[slot] = zb;
                 vals[slot] = (uint32_t)g;
-                pbits[slot] = (uint8_t)subtile_bits(r, (tile - tyy * ntx) * kTile, tyy * kTile);
+                pbits[slot] = (uint8_t)subtile_bits(r, tcx * kTile, tcy * kTile);
             }
         }
     }
