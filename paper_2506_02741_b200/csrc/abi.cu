@@ -51,7 +51,7 @@ cudaError_t dalloc(T **p, size_t n) {
 
 void free_all(Ctx &c) {
     void *ptrs[] = {c.proj, c.rect, c.tile_count, c.tile_start, c.tile_cursor, c.tile_flag, c.keys, c.vals, c.pbits, c.keys2,
-                    c.vals2, c.offs, c.sub_lists, c.sub_masks, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy, c.ssim_abc, c.ssim_partials};
+                    c.vals2, c.offs, c.sub_lists, c.sub_masks, c.chunk_list, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy, c.ssim_abc, c.ssim_partials};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -120,6 +120,7 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = dalloc(&c.offs, (size_t)max_pairs);
     if (!e) e = dalloc(&c.sub_lists, (size_t)8 * max_pairs);
     if (!e) e = dalloc(&c.sub_masks, (size_t)8 * max_pairs);
+    if (!e) e = dalloc(&c.chunk_list, (size_t)12 * ((size_t)max_pairs / 2048 + c.max_tiles + 1));
     if (!e) e = dalloc(&c.sub_count, (size_t)8 * c.max_tiles);
     if (!e) e = dalloc(&c.T_final, px);
     if (!e) e = dalloc(&c.last, px);

@@ -154,7 +154,6 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t *__restrict__ tile
         tile_start[i] = overflow ? 0u : (uint32_t)run;
         cursor[i] = overflow ? 0u : (uint32_t)run;
         if (overflow) tile_count[i] = 0;
-        else if (c > 8192u) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)i;
         else if (c > (uint32_t)kSortCap) radix_list[T + atomicAdd(&dev->big_count, 1u)] = (uint32_t)i;
         run += c;
     }
@@ -425,10 +424,14 @@ constexpr int kMaxBucket = 256;
 
 // Sub-lists from the sorted gids V and their sub-tile bits B: thread-local runs of E entries,
 // one block scan of the 8 per-sub-tile counts packed 4 × 16 bits into two 64-bit words.
+// stride = the tile's list length (sub-list capacity); sub_off (chunked tiles, else nullptr) =
+// where this part of the tile starts in each of the 8 sub-lists; sub_count is written only for
+// whole tiles (sub_off == nullptr).
 template <int NT>
 __device__ __forceinline__ void sublists_from_bits(const uint32_t *V, const uint8_t *B, int n,
                                                    uint32_t *__restrict__ out, uint32_t *__restrict__ sub_count,
-                                                   unsigned long long (*red64)[33]) {
+                                                   unsigned long long (*red64)[33], int stride,
+                                                   const uint32_t *sub_off) {
     constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int E = (n + NT - 1) / NT;
@@ -465,18 +468,21 @@ __device__ __forceinline__ void sublists_from_bits(const uint32_t *V, const uint
     __syncthreads();
     const unsigned long long p0 = s0 - c0 + red64[0][w], p1 = s1 - c1 + red64[1][w];
     const unsigned long long t0 = red64[0][NW], t1 = red64[1][NW];
-    if (tid < 8) sub_count[tid] = (uint32_t)(((tid < 4 ? t0 : t1) >> (16 * (tid & 3))) & 0xffffu);
+    if (!sub_off && tid < 8) sub_count[tid] = (uint32_t)(((tid < 4 ? t0 : t1) >> (16 * (tid & 3))) & 0xffffu);
     uint32_t off[8];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         off[q] = (uint32_t)((p0 >> (16 * q)) & 0xffffu);
         off[4 + q] = (uint32_t)((p1 >> (16 * q)) & 0xffffu);
     }
+    if (sub_off)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) off[q] += sub_off[q];
     for (int i = i0; i < i1; ++i) {
         const uint32_t b = B[i], g = V[i];
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-            if ((b >> q) & 1u) out[(size_t)q * n + off[q]++] = g;
+            if ((b >> q) & 1u) out[(size_t)q * stride + off[q]++] = g;
     }
 }
 
@@ -494,7 +500,10 @@ __device__ __forceinline__ void sublists_from_bits(const uint32_t *V, const uint
 // A tile whose largest bucket exceeds kMaxBucket (many equal or nearly equal depths) is flagged
 // and left to the radix sort kernel.  Lists in (LO, CAP] are handled; others return at once.
 // ------------------------------------------------------------------------------------------
-template <int LO, int CAP, int NB, int NT>
+// CHUNKED = false: one CTA per tile, lists in (LO, CAP].  CHUNKED = true: a grid walks the chunk
+// work list of k_chunk_plan (parts of long tiles, each ≤ CAP entries, already bucketed by depth
+// into keys2 / vals2 / bits2) and writes each part at its place in the tile's list and sub-lists.
+template <int LO, int CAP, int NB, int NT, bool CHUNKED = false>
 __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restrict__ tile_count,
                                                          const uint32_t *__restrict__ tile_start,
                                                          const uint32_t *__restrict__ keys,
@@ -503,34 +512,40 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
                                                          uint32_t *__restrict__ sub_lists,
                                                          uint32_t *__restrict__ sub_count,
                                                          uint32_t *__restrict__ radix_list,
-                                                         DevScalars *__restrict__ dev, int T) {
+                                                         DevScalars *__restrict__ dev, int T,
+                                                         const uint32_t *__restrict__ chunk_list = nullptr,
+                                                         const uint32_t *__restrict__ ckeys = nullptr,
+                                                         const uint32_t *__restrict__ cvals = nullptr,
+                                                         const uint32_t *__restrict__ cbits = nullptr) {
     constexpr int NW = NT / 32;
     constexpr int PT = NB / NT;
     static_assert(PT >= 1 && PT * NT == NB, "NB must be a multiple of NT");
     extern __shared__ uint32_t sm[];
     __shared__ uint32_t red[4][32];
     __shared__ unsigned long long red64[2][33];
-    __shared__ int s_tile;
-    // LISTED (lists of 4097..8192 entries, rare except at high layer counts): a grid of one CTA
-    // per SM fetches the tiles k_scan_tiles listed, one at a time; otherwise one CTA per tile
-    constexpr bool LISTED = CAP > 4096;
+    __shared__ uint32_t s_desc[12];
     for (int it = 0;; ++it) {
-    int tile;
-    if (LISTED) {
+    int tile, n, off = 0, ntile;
+    if (CHUNKED) {
         __syncthreads();
         if (threadIdx.x == 0) {
-            const unsigned w = atomicAdd(&dev->big_next, 1u);
-            s_tile = w < dev->big_count ? (int)radix_list[T + w] : -1;
+            const unsigned w = atomicAdd(&dev->chunk_next, 1u);
+            s_desc[0] = w < dev->chunk_count ? 1u : 0u;
+            if (w < dev->chunk_count)
+                for (int q = 0; q < 11; ++q) s_desc[1 + q] = chunk_list[(size_t)12 * w + q];
         }
         __syncthreads();
-        tile = s_tile;
-        if (tile < 0) return;
+        if (!s_desc[0]) return;
+        tile = (int)s_desc[1];
+        off = (int)s_desc[2];
+        n = (int)s_desc[3];
+        ntile = (int)tile_count[tile];
     } else {
         if (it > 0) return;
         tile = blockIdx.x;
+        n = ntile = (int)tile_count[tile];
+        if (n <= LO || n > CAP) continue;
     }
-    const int n = (int)tile_count[tile];
-    if (n <= LO || n > CAP) continue;
     constexpr int kLogNB = NB == 8192 ? 13 : (NB == 4096 ? 12 : (NB == 2048 ? 11 : 10));
     static_assert((1 << kLogNB) == NB, "NB must be 1024 … 8192");
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -539,10 +554,10 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
     uint8_t *B = reinterpret_cast<uint8_t *>(sm + 4 * CAP + NB), *B2 = B + CAP;
     uint32_t kmin = 0xffffffffu, kmax = 0u;
     for (int i = tid; i < n; i += NT) {
-        const uint32_t k = __ldg(keys + base + i);
+        const uint32_t k = CHUNKED ? __ldg(ckeys + base + off + i) : __ldg(keys + base + i);
         K[i] = k;
-        V[i] = __ldg(vals + base + i);
-        B[i] = __ldg(pbits + base + i);
+        V[i] = CHUNKED ? __ldg(cvals + base + off + i) : __ldg(vals + base + i);
+        B[i] = CHUNKED ? (uint8_t)__ldg(cbits + base + off + i) : __ldg(pbits + base + i);
         kmin = min(kmin, k);
         kmax = max(kmax, k);
     }
@@ -606,7 +621,7 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
             run += c[j];
         }
     }
-    if (cmax > (uint32_t)kMaxBucket) {   // degenerate depth distribution → the radix kernel's list
+    if (!CHUNKED && cmax > (uint32_t)kMaxBucket) {   // degenerate depth distribution → the radix kernel's list
         if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;
         continue;
     }
@@ -632,8 +647,175 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
         B[s0 + rank] = B2[p];
     }
     __syncthreads();
-    for (int i = tid; i < n; i += NT) vals[base + i] = V[i];
-    sublists_from_bits<NT>(V, B, n, sub_lists + (size_t)8 * base, sub_count + 8 * tile, red64);
+    for (int i = tid; i < n; i += NT) vals[base + off + i] = V[i];
+    sublists_from_bits<NT>(V, B, n, sub_lists + (size_t)8 * base, sub_count + 8 * tile, red64, ntile,
+                           CHUNKED ? s_desc + 4 : nullptr);
+    }
+}
+
+
+// ------------------------------------------------------------------------------------------
+// K5, long lists (> kSortCap entries, configs 4 / 5): instead of one CTA sorting the whole list
+// on global scratch, one CTA per long tile buckets it by depth — block min / max of the z bits,
+// NB buckets over that range, bucket b's segment start s_b — and cuts it into CHUNKS:
+// chunk(b) = ⌊s_b / tgt⌋ with tgt = kSortCap − max(largest bucket, kMaxBucket), so a chunk holds
+// ≤ kSortCap entries and chunks are depth-ordered.  The pairs are scattered into bucket order (keys2 /
+// vals2 / bits2), and per chunk the plan records its offset in the tile, its size and where it
+// starts in each of the 8 sub-lists; k_tile_sort_bucket<…, CHUNKED> then sorts every chunk on
+// chip (many CTAs per long tile).  A tile with a bucket > kSortCap / 2 (near-equal depths) or
+// more than kMaxChunks chunks goes to the radix kernel as before.
+// ------------------------------------------------------------------------------------------
+constexpr int kMaxChunks = 64;
+
+template <int NB, int NT>
+__global__ void __launch_bounds__(NT) k_chunk_plan(const uint32_t *__restrict__ tile_count,
+                                                   const uint32_t *__restrict__ tile_start,
+                                                   const uint32_t *__restrict__ keys,
+                                                   const uint32_t *__restrict__ vals,
+                                                   const uint8_t *__restrict__ pbits,
+                                                   uint32_t *__restrict__ keys2, uint32_t *__restrict__ vals2,
+                                                   uint32_t *__restrict__ bits2, uint32_t *__restrict__ sub_count,
+                                                   uint32_t *__restrict__ radix_list, uint32_t *__restrict__ chunk_list,
+                                                   DevScalars *__restrict__ dev, int T) {
+    constexpr int NW = NT / 32;
+    constexpr int PT = NB / NT;
+    constexpr int kLogNB = NB == 8192 ? 13 : (NB == 4096 ? 12 : (NB == 2048 ? 11 : 10));
+    static_assert(PT >= 1 && PT * NT == NB && (1 << kLogNB) == NB, "bucket count");
+    __shared__ uint32_t H[NB];
+    __shared__ uint8_t CH[NB];                 // chunk of each bucket
+    __shared__ uint32_t csub[kMaxChunks][8];   // per chunk, per sub-tile counts
+    __shared__ uint32_t ccnt[kMaxChunks], cbeg[kMaxChunks];
+    __shared__ uint32_t red[4][32];
+    __shared__ int s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned x = atomicAdd(&dev->big_next, 1u);
+            s_tile = x < dev->big_count ? (int)radix_list[T + x] : -1;
+        }
+        __syncthreads();
+        const int tile = s_tile;
+        if (tile < 0) return;
+        const int n = (int)tile_count[tile];
+        const uint32_t base = tile_start[tile];
+        if (n > kMaxChunks * (kSortCap / 2)) {   // beyond the plan's capacity: radix sort
+            if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;
+            continue;
+        }
+        uint32_t kmin = 0xffffffffu, kmax = 0u;
+        for (int i = tid; i < n; i += NT) {
+            const uint32_t k = __ldg(keys + base + i);
+            kmin = min(kmin, k);
+            kmax = max(kmax, k);
+        }
+        for (int i = tid; i < NB; i += NT) H[i] = 0u;
+        for (int i = tid; i < kMaxChunks * 8; i += NT) (&csub[0][0])[i] = 0u;
+        if (tid < kMaxChunks) { ccnt[tid] = 0u; cbeg[tid] = 0xffffffffu; }
+        kmin = __reduce_min_sync(kFull, kmin);
+        kmax = __reduce_max_sync(kFull, kmax);
+        if (lane == 0) { red[0][w] = kmin; red[1][w] = kmax; }
+        __syncthreads();
+        if (w == 0) {
+            const uint32_t a = __reduce_min_sync(kFull, lane < NW ? red[0][lane] : 0xffffffffu);
+            const uint32_t b = __reduce_max_sync(kFull, lane < NW ? red[1][lane] : 0u);
+            __syncwarp();
+            if (lane == 0) { red[0][0] = a; red[1][0] = b; }
+        }
+        __syncthreads();
+        kmin = red[0][0];
+        kmax = red[1][0];
+        const uint32_t range = kmax - kmin;
+        const int nbits = range ? 32 - __clz(range) : 0;
+        const int shift = nbits > kLogNB ? nbits - kLogNB : 0;
+        for (int i = tid; i < n; i += NT) atomicAdd(&H[(__ldg(keys + base + i) - kmin) >> shift], 1u);
+        __syncthreads();
+        uint32_t c[PT], tot = 0, cmax = 0;
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+            c[j] = H[tid * PT + j];
+            tot += c[j];
+            cmax = max(cmax, c[j]);
+        }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        cmax = __reduce_max_sync(kFull, cmax);
+        if (lane == 31) red[2][w] = incl;
+        if (lane == 0) red[3][w] = cmax;
+        __syncthreads();
+        if (w == 0) {
+            const uint32_t a = lane < NW ? red[2][lane] : 0u;
+            uint32_t ia = a;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, ia, o);
+                if (lane >= o) ia += y;
+            }
+            const uint32_t m = __reduce_max_sync(kFull, lane < NW ? red[3][lane] : 0u);
+            __syncwarp();
+            red[2][lane] = ia - a;
+            red[3][lane] = m;
+        }
+        __syncthreads();
+        // chunk target: a chunk holds the buckets starting in [c·tgt, (c + 1)·tgt), so it has
+        // ≤ tgt + (largest bucket) ≤ kSortCap entries
+        const uint32_t bmax = red[3][0];
+        const uint32_t tgt = (uint32_t)kSortCap - max(bmax, (uint32_t)kMaxBucket);
+        if (bmax > (uint32_t)kSortCap / 2 || (uint32_t)(n - 1) / tgt >= (uint32_t)kMaxChunks) {
+            if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;   // degenerate: radix
+            continue;
+        }
+        uint32_t run = incl - tot + red[2][w];
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {   // segment starts; chunk of each bucket; chunk sizes / starts
+            const int bkt = tid * PT + j;
+            H[bkt] = run;
+            const uint32_t ch = run / tgt;
+            CH[bkt] = (uint8_t)ch;
+            if (c[j]) {
+                atomicAdd(&ccnt[ch], c[j]);
+                atomicMin(&cbeg[ch], run);
+            }
+            run += c[j];
+        }
+        __syncthreads();
+        for (int i = tid; i < n; i += NT) {   // scatter into bucket order, count sub-tile entries per chunk
+            const uint32_t k = __ldg(keys + base + i);
+            const uint32_t bkt = (k - kmin) >> shift;
+            const uint32_t pos = atomicAdd(&H[bkt], 1u);
+            const uint32_t b = __ldg(pbits + base + i);
+            keys2[base + pos] = k;
+            vals2[base + pos] = __ldg(vals + base + i);
+            bits2[base + pos] = b;
+            const int ch = CH[bkt];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if ((b >> q) & 1u) atomicAdd(&csub[ch][q], 1u);
+        }
+        __syncthreads();
+        if (tid < 8) {   // sub-list offsets of each chunk (exclusive over chunks), tile totals
+            uint32_t r = 0;
+            for (int ch = 0; ch < kMaxChunks; ++ch) {
+                const uint32_t x = csub[ch][tid];
+                csub[ch][tid] = r;
+                r += x;
+            }
+            sub_count[8 * tile + tid] = r;
+        }
+        __syncthreads();
+        if (tid < kMaxChunks && ccnt[tid]) {
+            const unsigned x = atomicAdd(&dev->chunk_count, 1u);
+            uint32_t *d = chunk_list + (size_t)12 * x;
+            d[0] = (uint32_t)tile;
+            d[1] = cbeg[tid];
+            d[2] = ccnt[tid];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) d[3 + q] = csub[tid][q];
+        }
     }
 }
 
@@ -685,15 +867,19 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
         // every launch exits at once for the tiles it does not own
         if (sort_variant()) {
             // lists ≤ 2048: 512 threads, 4 CTAs / SM; (2048, 4096]: 1024 threads, 2 CTAs / SM;
-            // longer lists and flagged tiles: the radix kernel on global scratch / 8192 on chip
+            // longer lists: chunked (k_chunk_plan); flagged (degenerate) tiles: the radix kernel
             k_tile_sort_bucket<-1, 2048, 4096, 512><<<T, 512, bucket_smem(2048, 4096), s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T);
             k_tile_sort_bucket<2048, kSortCap, 4096, 1024><<<T, 1024, bucket_smem(kSortCap, 4096), s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T);
-            k_tile_sort_bucket<kSortCap, kSortCapBig, 8192, 1024><<<c.num_sms, 1024,
-                                                                    bucket_smem(kSortCapBig, 8192), s>>>(
-                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T);
-            ++c.launches;
+            // lists > kSortCap: depth-bucketed into chunks of ≤ kSortCap entries, chunks sorted on chip
+            k_chunk_plan<4096, 1024><<<c.num_sms, 1024, 0, s>>>(
+                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.keys2, c.vals2, c.offs, c.sub_count,
+                c.tile_flag, c.chunk_list, c.dev, T);
+            k_tile_sort_bucket<0, kSortCap, 4096, 1024, true><<<2 * c.num_sms, 1024, bucket_smem(kSortCap, 4096), s>>>(
+                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T,
+                c.chunk_list, c.keys2, c.vals2, c.offs);
+            c.launches += 2;
             k_tile_sort<kSortCap, kSortCapBig, true><<<c.num_sms, kBlock, kSortSmemBig, s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists,
                 c.sub_count, c.tile_flag, c.dev);
@@ -723,8 +909,8 @@ cudaError_t forward_set_attributes() {
         e = cudaFuncSetAttribute(k_tile_sort_bucket<2048, kSortCap, 4096, 1024>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, 4096));
     if (!e)
-        e = cudaFuncSetAttribute(k_tile_sort_bucket<kSortCap, kSortCapBig, 8192, 1024>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCapBig, 8192));
+        e = cudaFuncSetAttribute(k_tile_sort_bucket<0, kSortCap, 4096, 1024, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, 4096));
     if (!e)
         e = cudaFuncSetAttribute(k_tile_sort<kSortCap, kSortCapBig, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBig);

@@ -95,15 +95,18 @@ def test_tile_lists_micro_scenes(vt):
         assert np.array_equal(start, ostart) and np.array_equal(gid.astype(np.int64), ogid)
 
 
-@pytest.mark.parametrize("case", ["equal_depth", "two_depths", "long_lists"])
+@pytest.mark.parametrize("case", ["equal_depth", "two_depths", "long_lists", "very_long_lists"])
 def test_tile_lists_sort_paths(vt, case):
-    """The per-tile sort's three paths, bit-exact against the oracle: equal or nearly equal
-    depths (a bucket larger than the bucket sort takes → radix hand-off, ties broken by gid),
-    and lists longer than the on-chip bucket sort (> 4096 entries per tile)."""
-    rng = np.random.Generator(np.random.PCG64([7, {"equal_depth": 0, "two_depths": 1, "long_lists": 2}[case]]))
+    """The per-tile sort's paths, bit-exact against the oracle: equal or nearly equal depths (a
+    bucket larger than the bucket sort takes → radix hand-off, ties broken by gid), and lists
+    longer than the on-chip bucket sort (> 4096 entries per tile: depth-bucketed into chunks that
+    are sorted on chip, several chunks per tile for the very long lists).  The sub-lists of the
+    long tiles are checked through the forward render against the oracle's."""
+    rng = np.random.Generator(np.random.PCG64([7, {"equal_depth": 0, "two_depths": 1, "long_lists": 2,
+                                                   "very_long_lists": 3}[case]]))
     W, H = 40, 36
     intr = Intrinsics(30.0, 30.0, (W - 1) / 2, (H - 1) / 2, W, H)
-    n = 6000 if case != "long_lists" else 20000
+    n = {"long_lists": 20000, "very_long_lists": 60000}.get(case, 6000)
     if case == "equal_depth":
         z = np.full(n, 2.0)
     elif case == "two_depths":
@@ -122,12 +125,16 @@ def test_tile_lists_sort_paths(vt, case):
     pr = torch.from_numpy(pos_rad).cuda()
     co = torch.from_numpy(col_opa).cuda()
     pv = vt.pose_tensor(view32(view), "cuda")
-    R.render_fwd(pr, co, pv, intr)
+    out = R.render_fwd(pr, co, pv, intr)
     start, gid = R.export_tiles(intr)
     ostart, ogid = oracle.tile_lists(pos_rad, view32(view), intr)
     assert np.array_equal(start, ostart) and np.array_equal(gid.astype(np.int64), ogid)
     if case == "long_lists":
         assert np.diff(ostart).max() > 4096
+    if case == "very_long_lists":
+        assert np.diff(ostart).max() > 3 * 4096
+    ref = oracle.render(pos_rad, col_opa, view32(view), intr)
+    _check_images(out, ref, ref["flags"], max_flagged=2e-2)
 
 
 # ------------------------------------------------------------------------------ (a4)
