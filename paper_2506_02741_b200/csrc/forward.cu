@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
 // ------------------------------------------------------------------------------------------
 // K5, long lists (> kSortCap entries, configs 4 / 5): instead of one CTA sorting the whole list
 // on global scratch, one CTA per long tile buckets it by depth — block min / max of the z bits,
-// NB buckets over that range, bucket b's segment start s_b — and cuts it into CHUNKS:
+// NB buckets over that range (4,096 / 16,384 by length), segment starts s_b — and cuts it into CHUNKS:
 // chunk(b) = ⌊s_b / tgt⌋ with tgt = kSortCap − max(largest bucket, kMaxBucket), so a chunk holds
 // ≤ kSortCap entries and chunks are depth-ordered.  The pairs are scattered into bucket order (keys2 /
 // vals2 / bits2), and per chunk the plan records its offset in the tile, its size and where it
@@ -666,8 +666,140 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
 // more than kMaxChunks chunks goes to the radix kernel as before.
 // ------------------------------------------------------------------------------------------
 constexpr int kMaxChunks = 64;
+constexpr int kPlanBuckets = 16384;   // fine enough that config 5's densest wall stays ≤ 2048 per bucket
+constexpr size_t kPlanSmem = (size_t)kPlanBuckets * (sizeof(uint32_t) + sizeof(uint8_t));
 
+// One long tile's plan with NB depth buckets (NB = 4,096 for lists ≤ 16,384, else 16,384: fine
+// enough that config 5's densest wall stays ≤ 2,048 entries per bucket).
 template <int NB, int NT>
+__device__ __forceinline__ void plan_tile(int tile, int n, uint32_t base, const uint32_t *__restrict__ keys,
+                                          const uint32_t *__restrict__ vals, const uint8_t *__restrict__ pbits,
+                                          uint32_t *__restrict__ keys2, uint32_t *__restrict__ vals2,
+                                          uint32_t *__restrict__ bits2, uint32_t *__restrict__ sub_count,
+                                          uint32_t *__restrict__ radix_list, uint32_t *__restrict__ chunk_list,
+                                          DevScalars *__restrict__ dev, uint32_t *H, uint8_t *CH,
+                                          uint32_t (*csub)[8], uint32_t *ccnt, uint32_t *cbeg, uint32_t (*red)[32]) {
+    constexpr int NW = NT / 32;
+    constexpr int PT = NB / NT;
+    constexpr int kLogNB = NB == 16384 ? 14 : (NB == 8192 ? 13 : (NB == 4096 ? 12 : (NB == 2048 ? 11 : 10)));
+    static_assert(PT >= 1 && PT * NT == NB && (1 << kLogNB) == NB, "bucket count");
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (int i = tid; i < n; i += NT) {
+        const uint32_t k = __ldg(keys + base + i);
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
+    }
+    for (int i = tid; i < NB; i += NT) H[i] = 0u;
+    for (int i = tid; i < kMaxChunks * 8; i += NT) (&csub[0][0])[i] = 0u;
+    if (tid < kMaxChunks) { ccnt[tid] = 0u; cbeg[tid] = 0xffffffffu; }
+    kmin = __reduce_min_sync(kFull, kmin);
+    kmax = __reduce_max_sync(kFull, kmax);
+    if (lane == 0) { red[0][w] = kmin; red[1][w] = kmax; }
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t a = __reduce_min_sync(kFull, lane < NW ? red[0][lane] : 0xffffffffu);
+        const uint32_t b = __reduce_max_sync(kFull, lane < NW ? red[1][lane] : 0u);
+        __syncwarp();
+        if (lane == 0) { red[0][0] = a; red[1][0] = b; }
+    }
+    __syncthreads();
+    kmin = red[0][0];
+    kmax = red[1][0];
+    const uint32_t range = kmax - kmin;
+    const int nbits = range ? 32 - __clz(range) : 0;
+    const int shift = nbits > kLogNB ? nbits - kLogNB : 0;
+    for (int i = tid; i < n; i += NT) atomicAdd(&H[(__ldg(keys + base + i) - kmin) >> shift], 1u);
+    __syncthreads();
+    uint32_t c[PT], tot = 0, cmax = 0;
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {
+        c[j] = H[tid * PT + j];
+        tot += c[j];
+        cmax = max(cmax, c[j]);
+    }
+    uint32_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    cmax = __reduce_max_sync(kFull, cmax);
+    if (lane == 31) red[2][w] = incl;
+    if (lane == 0) red[3][w] = cmax;
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t a = lane < NW ? red[2][lane] : 0u;
+        uint32_t ia = a;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, ia, o);
+            if (lane >= o) ia += y;
+        }
+        const uint32_t m = __reduce_max_sync(kFull, lane < NW ? red[3][lane] : 0u);
+        __syncwarp();
+        red[2][lane] = ia - a;
+        red[3][lane] = m;
+    }
+    __syncthreads();
+    // chunk target: a chunk holds the buckets starting in [c·tgt, (c + 1)·tgt), so it has
+    // ≤ tgt + (largest bucket) ≤ kSortCap entries
+    const uint32_t bmax = red[3][0];
+    const uint32_t tgt = (uint32_t)kSortCap - max(bmax, (uint32_t)kMaxBucket);
+    if (bmax > (uint32_t)kSortCap / 2 || (uint32_t)(n - 1) / tgt >= (uint32_t)kMaxChunks) {
+        if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;   // degenerate: radix
+        return;
+    }
+    uint32_t run = incl - tot + red[2][w];
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {   // segment starts; chunk of each bucket; chunk sizes / starts
+        const int bkt = tid * PT + j;
+        H[bkt] = run;
+        const uint32_t ch = run / tgt;
+        CH[bkt] = (uint8_t)ch;
+        if (c[j]) {
+            atomicAdd(&ccnt[ch], c[j]);
+            atomicMin(&cbeg[ch], run);
+        }
+        run += c[j];
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) {   // scatter into bucket order, count sub-tile entries per chunk
+        const uint32_t k = __ldg(keys + base + i);
+        const uint32_t bkt = (k - kmin) >> shift;
+        const uint32_t pos = atomicAdd(&H[bkt], 1u);
+        const uint32_t b = __ldg(pbits + base + i);
+        keys2[base + pos] = k;
+        vals2[base + pos] = __ldg(vals + base + i);
+        bits2[base + pos] = b;
+        const int ch = CH[bkt];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if ((b >> q) & 1u) atomicAdd(&csub[ch][q], 1u);
+    }
+    __syncthreads();
+    if (tid < 8) {   // sub-list offsets of each chunk (exclusive over chunks), tile totals
+        uint32_t r = 0;
+        for (int ch = 0; ch < kMaxChunks; ++ch) {
+            const uint32_t x = csub[ch][tid];
+            csub[ch][tid] = r;
+            r += x;
+        }
+        sub_count[8 * tile + tid] = r;
+    }
+    __syncthreads();
+    if (tid < kMaxChunks && ccnt[tid]) {
+        const unsigned x = atomicAdd(&dev->chunk_count, 1u);
+        uint32_t *d = chunk_list + (size_t)12 * x;
+        d[0] = (uint32_t)tile;
+        d[1] = cbeg[tid];
+        d[2] = ccnt[tid];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) d[3 + q] = csub[tid][q];
+    }
+}
+
+template <int NT>
 __global__ void __launch_bounds__(NT) k_chunk_plan(const uint32_t *__restrict__ tile_count,
                                                    const uint32_t *__restrict__ tile_start,
                                                    const uint32_t *__restrict__ keys,
@@ -677,17 +809,14 @@ __global__ void __launch_bounds__(NT) k_chunk_plan(const uint32_t *__restrict__ 
                                                    uint32_t *__restrict__ bits2, uint32_t *__restrict__ sub_count,
                                                    uint32_t *__restrict__ radix_list, uint32_t *__restrict__ chunk_list,
                                                    DevScalars *__restrict__ dev, int T) {
-    constexpr int NW = NT / 32;
-    constexpr int PT = NB / NT;
-    constexpr int kLogNB = NB == 8192 ? 13 : (NB == 4096 ? 12 : (NB == 2048 ? 11 : 10));
-    static_assert(PT >= 1 && PT * NT == NB && (1 << kLogNB) == NB, "bucket count");
-    __shared__ uint32_t H[NB];
-    __shared__ uint8_t CH[NB];                 // chunk of each bucket
+    extern __shared__ uint32_t plan_smem[];
+    uint32_t *H = plan_smem;                                                  // [kPlanBuckets]
+    uint8_t *CH = reinterpret_cast<uint8_t *>(plan_smem + kPlanBuckets);     // [kPlanBuckets]
     __shared__ uint32_t csub[kMaxChunks][8];   // per chunk, per sub-tile counts
     __shared__ uint32_t ccnt[kMaxChunks], cbeg[kMaxChunks];
     __shared__ uint32_t red[4][32];
     __shared__ int s_tile;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int tid = threadIdx.x;
     for (;;) {
         __syncthreads();
         if (tid == 0) {
@@ -703,119 +832,12 @@ __global__ void __launch_bounds__(NT) k_chunk_plan(const uint32_t *__restrict__ 
             if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;
             continue;
         }
-        uint32_t kmin = 0xffffffffu, kmax = 0u;
-        for (int i = tid; i < n; i += NT) {
-            const uint32_t k = __ldg(keys + base + i);
-            kmin = min(kmin, k);
-            kmax = max(kmax, k);
-        }
-        for (int i = tid; i < NB; i += NT) H[i] = 0u;
-        for (int i = tid; i < kMaxChunks * 8; i += NT) (&csub[0][0])[i] = 0u;
-        if (tid < kMaxChunks) { ccnt[tid] = 0u; cbeg[tid] = 0xffffffffu; }
-        kmin = __reduce_min_sync(kFull, kmin);
-        kmax = __reduce_max_sync(kFull, kmax);
-        if (lane == 0) { red[0][w] = kmin; red[1][w] = kmax; }
-        __syncthreads();
-        if (w == 0) {
-            const uint32_t a = __reduce_min_sync(kFull, lane < NW ? red[0][lane] : 0xffffffffu);
-            const uint32_t b = __reduce_max_sync(kFull, lane < NW ? red[1][lane] : 0u);
-            __syncwarp();
-            if (lane == 0) { red[0][0] = a; red[1][0] = b; }
-        }
-        __syncthreads();
-        kmin = red[0][0];
-        kmax = red[1][0];
-        const uint32_t range = kmax - kmin;
-        const int nbits = range ? 32 - __clz(range) : 0;
-        const int shift = nbits > kLogNB ? nbits - kLogNB : 0;
-        for (int i = tid; i < n; i += NT) atomicAdd(&H[(__ldg(keys + base + i) - kmin) >> shift], 1u);
-        __syncthreads();
-        uint32_t c[PT], tot = 0, cmax = 0;
-#pragma unroll
-        for (int j = 0; j < PT; ++j) {
-            c[j] = H[tid * PT + j];
-            tot += c[j];
-            cmax = max(cmax, c[j]);
-        }
-        uint32_t incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += y;
-        }
-        cmax = __reduce_max_sync(kFull, cmax);
-        if (lane == 31) red[2][w] = incl;
-        if (lane == 0) red[3][w] = cmax;
-        __syncthreads();
-        if (w == 0) {
-            const uint32_t a = lane < NW ? red[2][lane] : 0u;
-            uint32_t ia = a;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(kFull, ia, o);
-                if (lane >= o) ia += y;
-            }
-            const uint32_t m = __reduce_max_sync(kFull, lane < NW ? red[3][lane] : 0u);
-            __syncwarp();
-            red[2][lane] = ia - a;
-            red[3][lane] = m;
-        }
-        __syncthreads();
-        // chunk target: a chunk holds the buckets starting in [c·tgt, (c + 1)·tgt), so it has
-        // ≤ tgt + (largest bucket) ≤ kSortCap entries
-        const uint32_t bmax = red[3][0];
-        const uint32_t tgt = (uint32_t)kSortCap - max(bmax, (uint32_t)kMaxBucket);
-        if (bmax > (uint32_t)kSortCap / 2 || (uint32_t)(n - 1) / tgt >= (uint32_t)kMaxChunks) {
-            if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;   // degenerate: radix
-            continue;
-        }
-        uint32_t run = incl - tot + red[2][w];
-#pragma unroll
-        for (int j = 0; j < PT; ++j) {   // segment starts; chunk of each bucket; chunk sizes / starts
-            const int bkt = tid * PT + j;
-            H[bkt] = run;
-            const uint32_t ch = run / tgt;
-            CH[bkt] = (uint8_t)ch;
-            if (c[j]) {
-                atomicAdd(&ccnt[ch], c[j]);
-                atomicMin(&cbeg[ch], run);
-            }
-            run += c[j];
-        }
-        __syncthreads();
-        for (int i = tid; i < n; i += NT) {   // scatter into bucket order, count sub-tile entries per chunk
-            const uint32_t k = __ldg(keys + base + i);
-            const uint32_t bkt = (k - kmin) >> shift;
-            const uint32_t pos = atomicAdd(&H[bkt], 1u);
-            const uint32_t b = __ldg(pbits + base + i);
-            keys2[base + pos] = k;
-            vals2[base + pos] = __ldg(vals + base + i);
-            bits2[base + pos] = b;
-            const int ch = CH[bkt];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if ((b >> q) & 1u) atomicAdd(&csub[ch][q], 1u);
-        }
-        __syncthreads();
-        if (tid < 8) {   // sub-list offsets of each chunk (exclusive over chunks), tile totals
-            uint32_t r = 0;
-            for (int ch = 0; ch < kMaxChunks; ++ch) {
-                const uint32_t x = csub[ch][tid];
-                csub[ch][tid] = r;
-                r += x;
-            }
-            sub_count[8 * tile + tid] = r;
-        }
-        __syncthreads();
-        if (tid < kMaxChunks && ccnt[tid]) {
-            const unsigned x = atomicAdd(&dev->chunk_count, 1u);
-            uint32_t *d = chunk_list + (size_t)12 * x;
-            d[0] = (uint32_t)tile;
-            d[1] = cbeg[tid];
-            d[2] = ccnt[tid];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) d[3 + q] = csub[tid][q];
-        }
+        if (n <= 16384)
+            plan_tile<4096, NT>(tile, n, base, keys, vals, pbits, keys2, vals2, bits2, sub_count, radix_list,
+                                chunk_list, dev, H, CH, csub, ccnt, cbeg, red);
+        else
+            plan_tile<kPlanBuckets, NT>(tile, n, base, keys, vals, pbits, keys2, vals2, bits2, sub_count,
+                                        radix_list, chunk_list, dev, H, CH, csub, ccnt, cbeg, red);
     }
 }
 
@@ -873,7 +895,7 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
             k_tile_sort_bucket<2048, kSortCap, 4096, 1024><<<T, 1024, bucket_smem(kSortCap, 4096), s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T);
             // lists > kSortCap: depth-bucketed into chunks of ≤ kSortCap entries, chunks sorted on chip
-            k_chunk_plan<4096, 1024><<<c.num_sms, 1024, 0, s>>>(
+            k_chunk_plan<1024><<<c.num_sms, 1024, kPlanSmem, s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.keys2, c.vals2, c.offs, c.sub_count,
                 c.tile_flag, c.chunk_list, c.dev, T);
             k_tile_sort_bucket<0, kSortCap, 4096, 1024, true><<<2 * c.num_sms, 1024, bucket_smem(kSortCap, 4096), s>>>(
@@ -908,6 +930,9 @@ cudaError_t forward_set_attributes() {
     if (!e)
         e = cudaFuncSetAttribute(k_tile_sort_bucket<2048, kSortCap, 4096, 1024>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, 4096));
+    if (!e)
+        e = cudaFuncSetAttribute(k_chunk_plan<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kPlanSmem);
     if (!e)
         e = cudaFuncSetAttribute(k_tile_sort_bucket<0, kSortCap, 4096, 1024, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, 4096));
