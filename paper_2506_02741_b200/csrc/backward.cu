@@ -179,12 +179,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
     const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
     EntryRegs nxt;
     fetch_entry<false>(nxt, list, bb_top + (int)lane, cnt, p.proj, p.col_opa, p.rect);
-    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, cnt);
+    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
     for (int bb = bb_top; bb >= 0; bb -= 32) {
         const EntryRegs cur = nxt;
         const uint32_t mcur = mnx;
         fetch_entry<false>(nxt, list, bb - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
-        mnx = load_mask(mlist, bb - 32 + (int)lane, cnt);  // next (lower) batch
+        mnx = load_mask(mlist, bb - 32 + (int)lane, wmax);  // next (lower) batch
         const int jj = bb + (int)lane;
         unsigned mj = 0u;
         float4 Aj = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -400,12 +400,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p
     const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
     EntryRegs nxt;
     fetch_entry<false>(nxt, list, bb_top + (int)lane, cnt, p.proj, p.col_opa, p.rect);
-    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, cnt);
+    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
     for (int bb = bb_top; bb >= 0; bb -= 32) {
         const EntryRegs cur = nxt;
         const uint32_t mcur = mnx;
         fetch_entry<false>(nxt, list, bb - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
-        mnx = load_mask(mlist, bb - 32 + (int)lane, cnt);
+        mnx = load_mask(mlist, bb - 32 + (int)lane, wmax);
         unsigned mj = 0u;
         if (bb + (int)lane < wmax) {
             const float4 Aj = entry_geom(cur.pr);
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
 
     EntryStream st;
     stream_start<false>(st, list, bb_top + (int)lane, bb_top - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
-    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, cnt);
+    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
     float4 posn = make_float4(0.f, 0.f, 0.f, 0.f);
     if (bb_top + (int)lane >= 0 && bb_top + (int)lane < cnt) posn = __ldg(p.pos_rad + st.e.g);
     int built = 0;
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
         ++built;
         const int nidx = bb - 32 + (int)lane;
         stream_next<false>(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
-        mnx = load_mask(mlist, nidx, cnt);
+        mnx = load_mask(mlist, nidx, wmax);
         if (nidx >= 0 && nidx < cnt) posn = __ldg(p.pos_rad + st.e.g);
     };
     while (built < nb && built < R) build();
