@@ -149,7 +149,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
     const int n = (int)p.tile_count[tile];
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
-    const int cnt = (int)p.sub_count[tile * 8 + sub];
     PoseR P;
     if (POSE) pose_rotation(*p.view, P);
 
@@ -178,17 +177,17 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
 
     const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
     EntryRegs nxt;
-    fetch_entry<false>(nxt, list, bb_top + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    fetch_entry<false>(nxt, list, bb_top + (int)lane, wmax, p.proj, p.col_opa, p.rect);
     uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
     for (int bb = bb_top; bb >= 0; bb -= 32) {
         const EntryRegs cur = nxt;
         const uint32_t mcur = mnx;
-        fetch_entry<false>(nxt, list, bb - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        fetch_entry<false>(nxt, list, bb - 32 + (int)lane, wmax, p.proj, p.col_opa, p.rect);
         mnx = load_mask(mlist, bb - 32 + (int)lane, wmax);  // next (lower) batch
         const int jj = bb + (int)lane;
         unsigned mj = 0u;
         float4 Aj = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (jj < wmax) {   // wmax ≤ cnt
+        if (jj < wmax) {   // wmax ≤ the sub-list length
             Aj = entry_geom(cur.pr);
             sA[wl_][lane] = Aj;
             sB[wl_][lane] = cur.co;
@@ -380,7 +379,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p
     const int n = (int)p.tile_count[tile];
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
-    const int cnt = (int)p.sub_count[tile * 8 + sub];
     PoseR P;
     pose_rotation(*p.view, P);
 
@@ -399,12 +397,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p
 
     const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
     EntryRegs nxt;
-    fetch_entry<false>(nxt, list, bb_top + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    fetch_entry<false>(nxt, list, bb_top + (int)lane, wmax, p.proj, p.col_opa, p.rect);
     uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
     for (int bb = bb_top; bb >= 0; bb -= 32) {
         const EntryRegs cur = nxt;
         const uint32_t mcur = mnx;
-        fetch_entry<false>(nxt, list, bb - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        fetch_entry<false>(nxt, list, bb - 32 + (int)lane, wmax, p.proj, p.col_opa, p.rect);
         mnx = load_mask(mlist, bb - 32 + (int)lane, wmax);
         unsigned mj = 0u;
         if (bb + (int)lane < wmax) {
@@ -691,11 +689,19 @@ __global__ void __launch_bounds__(256) k_l1_count(const float *__restrict__ sil,
         cc += cmode ? Wm : 1u;
         cd += dmode ? Wm : U;
     }
-    cc = __reduce_add_sync(kFull, cc);
+    cc = __reduce_add_sync(kFull, cc);   // warp → block (shared) → one atomic pair per block
     cd = __reduce_add_sync(kFull, cd);
-    if (lane_id() == 0) {
-        atomicAdd(&dev->count_c, cc);
-        atomicAdd(&dev->count_d, cd);
+    __shared__ unsigned sc[8], sd[8];
+    const int w = threadIdx.x >> 5;
+    if (lane_id() == 0) { sc[w] = cc; sd[w] = cd; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const unsigned a = __reduce_add_sync(kFull, threadIdx.x < 8 ? sc[threadIdx.x] : 0u);
+        const unsigned b = __reduce_add_sync(kFull, threadIdx.x < 8 ? sd[threadIdx.x] : 0u);
+        if (threadIdx.x == 0) {
+            atomicAdd(&dev->count_c, a);
+            atomicAdd(&dev->count_d, b);
+        }
     }
 }
 
@@ -708,17 +714,34 @@ constexpr int kFinBlocks = 64;
 // Two-level fixed-order reduction: block b sums rows [b·R, (b+1)·R) of the per-CTA partials
 // into partials2[b]; the last block to finish (ticket) sums partials2[0 .. kFinBlocks) in index
 // order — deterministic, and the row loads of the 64 blocks run in parallel.
+// Fixed-order block sum of 13 values: butterfly within each warp, then warp 0 over the warps'
+// sums; the result lands in red[0][0..12].
 __device__ __forceinline__ void block_sum13(double acc[13], double (*red)[13]) {
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 #pragma unroll
-    for (int q = 0; q < 13; ++q) red[tid][q] = acc[q];
-    __syncthreads();
-    for (int s = kFinThreads / 2; s > 0; s >>= 1) {
-        if (tid < s)
+    for (int q = 0; q < 13; ++q) {
 #pragma unroll
-            for (int q = 0; q < 13; ++q) red[tid][q] += red[tid + s][q];
-        __syncthreads();
+        for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(kFull, acc[q], o);
     }
+    __syncthreads();   // red may still be read by the caller's previous use
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 13; ++q) red[w][q] = acc[q];
+    __syncthreads();
+    if (w == 0) {
+#pragma unroll
+        for (int q = 0; q < 13; ++q) {
+            double v = lane < kFinThreads / 32 ? red[lane][q] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            acc[q] = v;
+        }
+        __syncwarp();
+        if (lane == 0)
+#pragma unroll
+            for (int q = 0; q < 13; ++q) red[0][q] = acc[q];
+    }
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(kFinThreads) k_pose_finalize(const double *__restrict__ partials, int T,
@@ -727,7 +750,7 @@ __global__ void __launch_bounds__(kFinThreads) k_pose_finalize(const double *__r
                                                                float *__restrict__ loss_out,
                                                                double *__restrict__ partials2,
                                                                unsigned int *__restrict__ ticket) {
-    __shared__ double red[kFinThreads][13];
+    __shared__ double red[kFinThreads / 32][13];
     __shared__ bool last;
     const int tid = threadIdx.x;
     const int R = (T + kFinBlocks - 1) / kFinBlocks;
@@ -803,8 +826,18 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_finalize(const double *__
                                                                 float *__restrict__ loss_out) {
     __shared__ double red[kLossThreads / 32];
     const int tid = threadIdx.x;
+    // all of a thread's loads in flight together, summed in row order
+    constexpr int kU = 16;
+    double x[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        const int t = tid + u * kLossThreads;
+        x[u] = t < T ? __ldg(partials + (size_t)t * 16 + 12) : 0.0;
+    }
     double acc = 0.0;
-    for (int t = tid; t < T; t += kLossThreads) acc += __ldg(partials + (size_t)t * 16 + 12);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) acc += x[u];
+    for (int t = tid + kU * kLossThreads; t < T; t += kLossThreads) acc += __ldg(partials + (size_t)t * 16 + 12);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
     if ((tid & 31) == 0) red[tid >> 5] = acc;
@@ -876,7 +909,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
         if (a.normalize) {
             if ((err = cudaMemsetAsync(&c.dev->count_c, 0, 2 * sizeof(unsigned int), s))) return err;
             int g = (W * H + 255) / 256;
-            if (g > c.num_sms * 8) g = c.num_sms * 8;
+            if (g > c.num_sms * 2) g = c.num_sms * 2;
             LaunchScope ls(&c, kL1Count, s);
             k_l1_count<<<g, 256, 0, s>>>(c.sil, a.tD, a.vis, W * H, a.cmode, a.dmode, c.dev);
             if ((err = cudaGetLastError())) return err;
