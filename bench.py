@@ -34,6 +34,7 @@ METRIC = "fwd+bwd render Mpix/s & Gaussians/s at 1/2/4/8 B200; fraction of roofl
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0        # B200_PROFILING.md fallback
 SM_COUNT = 148
+PROFILE_EVERY = 10   # per-kernel CUDA events ride on every 10th timed step (each event pair costs ≈ 2.7 µs of stream time)
 FP32_LANES_PER_SM = 128
 # Algorithmic work per unit: FP32 flops per (pixel, Gaussian)
 # evaluation in the forward and per composited pair in the backward (an FMA counts 2).
@@ -385,6 +386,7 @@ def main():
         clocks.start()
     for i in range(args.steps):
         flush.fill_(float(i))                               # evict L2 between steps (not timed)
+        R.set_profiling(i % PROFILE_EVERY == 0)             # per-kernel events on every 10th step
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)
@@ -498,6 +500,7 @@ def main():
             "gaussians_per_s": gps,
             "roofline": roofline,
             "stages": stage_json,
+            "stage_timing": f"CUDA events around every kernel on every {PROFILE_EVERY}th timed step ({(args.steps + PROFILE_EVERY - 1) // PROFILE_EVERY} of {args.steps}), on the launching stream",
             "work": {"n_pairs": P, "e_eval": stats["e_eval"], "e_comp": stats["e_comp"], "max_tile": stats["max_tile"]},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -251,8 +251,9 @@ VTGS_API vtgs_status vtgs_set_work_counters(vtgs_ctx *ctx, int32_t enable);
  *   12 densify, 13 visibility. */
 #define VTGS_NUM_STAGES 14
 VTGS_API vtgs_status vtgs_set_profiling(vtgs_ctx *ctx, int32_t enable);
-/* Synchronous: sum of event-timed milliseconds (ms[VTGS_NUM_STAGES], host) and launch counts
- * (counts[VTGS_NUM_STAGES], host, may be NULL) per stage since the previous call; resets. */
+/* Synchronous: sum of event-timed milliseconds (ms[VTGS_NUM_STAGES], host) and the number of
+ * event-timed launch scopes (counts[VTGS_NUM_STAGES], host, may be NULL; launches made while
+ * profiling was off are not counted) per stage since the previous call; resets. */
 VTGS_API vtgs_status vtgs_get_profile(vtgs_ctx *ctx, double *ms, int64_t *counts, void *stream);
 
 /* Synchronise `stream` and report a deferred device-side error (VTGS_ERR_CAPACITY) or a CUDA

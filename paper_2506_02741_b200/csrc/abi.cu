@@ -377,16 +377,20 @@ vtgs_status vtgs_get_profile(vtgs_ctx *ctx, double *ms, int64_t *counts, void *s
     cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
     if (!e) e = cudaDeviceSynchronize();
     if (e) return cuda_fail(ctx, e, "vtgs_get_profile");
+    int64_t timed[VTGS_NUM_STAGES] = {0};
     for (int i = 0; i < VTGS_NUM_STAGES; ++i) ms[i] = 0.0;
     for (auto &ev : c.prof) {
         float t = 0.f;
-        if (cudaEventElapsedTime(&t, ev.a, ev.b) == cudaSuccess) ms[ev.stage] += t;
+        if (cudaEventElapsedTime(&t, ev.a, ev.b) == cudaSuccess) {
+            ms[ev.stage] += t;
+            ++timed[ev.stage];
+        }
         c.prof_free.push_back(ev);
     }
     cudaGetLastError();
     c.prof.clear();
     for (int i = 0; i < VTGS_NUM_STAGES; ++i) {
-        if (counts) counts[i] = c.prof_counts[i];
+        if (counts) counts[i] = timed[i];
         c.prof_counts[i] = 0;
     }
     return VTGS_OK;
