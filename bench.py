@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--profile-run", action="store_true", help="short run for ncu (no clocks / cpu baseline)")
     ap.add_argument("--ssim", type=float, default=0.0,
                     help="add Eq. 2's SSIM term with this weight tau (0.2 in the paper) to the mapping step")
+    ap.add_argument("--no-graph", action="store_true", help="run every timed step eagerly (no CUDA graph)")
     return ap.parse_args()
 
 
@@ -373,6 +374,26 @@ def main():
     assert st["overflow"] == 0, "tile-pair capacity exceeded"
     R.set_work_counters(False)                             # diagnostics only: off in the timed region
 
+    # one CUDA graph of the whole step (launch-only: no host sync inside), replayed in the timed
+    # region; the every-10th profiled steps run eagerly (per-kernel events).  N > 1 steps stay
+    # eager (the NCCL all-reduce is not captured).
+    graph, per_step_launches = None, 0
+    if ws == 1 and not args.no_graph:
+        R.set_profiling(False)
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        with torch.cuda.stream(gs):
+            step()
+        torch.cuda.synchronize()
+        l0 = R.stats()["launches"]
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            step()
+        per_step_launches = R.stats()["launches"] - l0
+        torch.cuda.synchronize()
+        graph.replay()
+        torch.cuda.synchronize()
+
     # ---------------- timed region
     R.set_profiling(True)
     R.profile()                                            # reset
@@ -384,17 +405,23 @@ def main():
     torch.cuda.synchronize()
     if clocks:
         clocks.start()
+    replays = 0
     for i in range(args.steps):
         flush.fill_(float(i))                               # evict L2 between steps (not timed)
-        R.set_profiling(i % PROFILE_EVERY == 0)             # per-kernel events on every 10th step
+        prof_i = i % PROFILE_EVERY == 0
+        R.set_profiling(prof_i)                             # per-kernel events on every 10th step
         ev[i][0].record(stream)
-        step()
+        if graph is not None and not prof_i:
+            graph.replay()
+            replays += 1
+        else:
+            step()
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     clk = clocks.stop() if clocks else None
-    launches = R.stats()["launches"] - launches0
+    launches = R.stats()["launches"] - launches0 + replays * per_step_launches
     prof = R.profile()
     R.set_profiling(False)
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -500,7 +527,9 @@ def main():
             "gaussians_per_s": gps,
             "roofline": roofline,
             "stages": stage_json,
-            "stage_timing": f"CUDA events around every kernel on every {PROFILE_EVERY}th timed step ({(args.steps + PROFILE_EVERY - 1) // PROFILE_EVERY} of {args.steps}), on the launching stream",
+            "stage_timing": f"CUDA events around every kernel on every {PROFILE_EVERY}th timed step ({(args.steps + PROFILE_EVERY - 1) // PROFILE_EVERY} of {args.steps}, run eagerly), on the launching stream",
+            "graph": (f"the other {replays} timed steps replay one captured CUDA graph of the step ({per_step_launches} launches)"
+                      if graph is not None else "eager"),
             "work": {"n_pairs": P, "e_eval": stats["e_eval"], "e_comp": stats["e_comp"], "max_tile": stats["max_tile"]},
             "cpu_baseline": cpu,
             "e2e": e2e,
