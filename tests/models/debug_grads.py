@@ -1,8 +1,9 @@
 """Ad-hoc GPU diagnostic (not collected by pytest): gradient error vs conditioning."""
+import os
 import sys
 import numpy as np
 import torch
-sys.path.insert(0, "."); sys.path.insert(0, "tests")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))); sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle
 from synth.scenes import cached_config
 from vtgs_testlib import gpu_instantiate, oracle_instantiate, view32

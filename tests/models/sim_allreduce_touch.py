@@ -2,8 +2,9 @@
 each of the 16 mapping views touches (any slot visible, oracle projection), and the union over each
 rank's view shard at N = 2, 4, 8 -- the chunks no rank touches are the only ones the sparse
 all-reduce could skip."""
-import sys, numpy as np, time
-sys.path.insert(0, "/root/repo")
+import os, sys, time
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle
 from synth.scenes import make_config
 from paper_2506_02741_b200.mapping import shard_views

@@ -3,9 +3,10 @@
 batches — per 32-entry batch of a region's list, the region's pixels (with their candidate
 counts in the batch) are split into 32 contiguous lane ranges by prefix sums; the warp runs
 max-over-lanes(Σ candidates) iterations plus one state swap per (lane, pixel)."""
+import os
 import sys
 import numpy as np
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle  # noqa: E402
 from synth.scenes import cached_config  # noqa: E402
 

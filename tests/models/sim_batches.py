@@ -6,11 +6,12 @@ entries (rect ∋ pixel ∧ d² ≤ 9σ²) and its termination position, then re
 batch-window sizes W, the warp iterations Σ_windows max_lanes(#candidates in window) against
 the ideal Σ_lanes #candidates / 32.
 """
+import os
 import sys
 
 import numpy as np
 
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle  # noqa: E402
 from synth.scenes import cached_config  # noqa: E402
 

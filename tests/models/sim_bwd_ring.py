@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Offline model of the backward's phase-1 lane utilisation (design tool, uses the oracle).
 
-Same sample of 8×4 sub-tiles of config 2 as tools/sim_batches.py.  Per pixel the phase-1
+Same sample of 8×4 sub-tiles of config 2 as tests/models/sim_batches.py.  Per pixel the phase-1
 candidates are the entries at sub-list positions < its `last` whose rect and 3σ disc contain it,
 walked back to front.  Compared: the lock-step walk per 32-entry batch (today's k_composite_bwd)
 and a ring of 32-entry batches whose (pixel, entry) pair storage is a circular buffer of C pairs
@@ -9,11 +9,12 @@ and a ring of 32-entry batches whose (pixel, entry) pair storage is a circular b
 released (its phase 2 run) once every live lane has passed it.  Reported: warp steps of phase 1,
 lane efficiency = Σ candidates / 32 / steps, and the pair count per batch (phase-2 work).
 """
+import os
 import sys
 
 import numpy as np
 
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import oracle  # noqa: E402
 from synth.scenes import cached_config  # noqa: E402
 
