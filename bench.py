@@ -510,11 +510,11 @@ def main():
     # ---------------- cpu baseline (oracle as it stands, bounded sample, rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_run:
-        rows = (H // 2 - 8, H // 2 + 8)
+        rows = (0, H)   # the whole view: ≈ 15–25 s of single-threaded oracle work (one step)
         dt, px = time_oracle(cfg, 1, 0, rows)
         cpu = {"value": px / dt / 1e6, "unit": "Mpix/s", "cores": 1, "kind": "oracle",
-               "sample": f"rows {rows[0]}-{rows[1] - 1} ({px} px) of the same view; projection + tile lists of all "
-                         f"{N} slots, render, L1, backward; single-threaded C (oracle/vtgs_oracle.c)",
+               "sample": f"one whole step of the same view ({px} px): projection + tile lists of all {N} slots, "
+                         f"render, L1, backward; single-threaded C (oracle/vtgs_oracle.c)",
                "seconds": dt}
 
     if rank == 0:
