@@ -515,6 +515,35 @@ def test_tracking_loop_graph_matches_eager_and_converges(vt):
     assert np.linalg.norm(pe[4:] - gt[4:]) < np.linalg.norm(init[4:] - gt[4:])
 
 
+def test_mapping_step_graph_matches_eager(vt):
+    """The bench replays the mapping step (zero grads + fwd + fused L1 + bwd) from one CUDA graph:
+    the graph gives the same images and loss bit for bit and the same gradients (float atomics:
+    equal up to summation order) as eager launches."""
+    from paper_2506_02741_b200.mapping import BatchedMapper
+    cfg = cached_config(2)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    kf = cfg.keyframes[2]
+    m = BatchedMapper(R, pr, co, cfg.intr, [vt.pose_tensor(np.asarray(kf.pose, dtype=np.float32), "cuda")],
+                      [dict(rgb=torch.from_numpy(kf.rgb).cuda(), depth=torch.from_numpy(kf.depth).cuda())], 0.8, 1.0)
+    m.step(allreduce=False)
+    torch.cuda.synchronize()
+    eager = [t.clone() for t in m.out] + [m.loss.clone(), m.grads.flat.clone()]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        m.step(allreduce=False)
+    m.grads.flat.fill_(123.0)
+    for t in m.out:
+        t.fill_(-1.0)
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager[:4], list(m.out) + [m.loss]):
+        assert torch.equal(a, b)
+    assert torch.allclose(eager[4], m.grads.flat, rtol=1e-5, atol=1e-6)
+
+
 def test_step_host_matches_device_path(vt):
     cfg = cached_config(2)
     R = _renderer(vt, cfg)
