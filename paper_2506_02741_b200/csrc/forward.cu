@@ -154,7 +154,6 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t *__restrict__ tile
         tile_start[i] = overflow ? 0u : (uint32_t)run;
         cursor[i] = overflow ? 0u : (uint32_t)run;
         if (overflow) tile_count[i] = 0;
-        else if (c > (uint32_t)kSortCap) radix_list[T + atomicAdd(&dev->big_count, 1u)] = (uint32_t)i;
         run += c;
     }
     if (tid == 0) tile_start[T] = overflow ? 0u : (uint32_t)total_s;
@@ -500,163 +499,9 @@ __device__ __forceinline__ void sublists_from_bits(const uint32_t *V, const uint
 // A tile whose largest bucket exceeds kMaxBucket (many equal or nearly equal depths) is flagged
 // and left to the radix sort kernel.  Lists in (LO, CAP] are handled; others return at once.
 // ------------------------------------------------------------------------------------------
-// CHUNKED = false: one CTA per tile, lists in (LO, CAP].  CHUNKED = true: a grid walks the chunk
-// work list of k_chunk_plan (parts of long tiles, each ≤ CAP entries, already bucketed by depth
-// into keys2 / vals2 / bits2) and writes each part at its place in the tile's list and sub-lists.
-template <int LO, int CAP, int NB, int NT, bool CHUNKED = false>
-__global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restrict__ tile_count,
-                                                         const uint32_t *__restrict__ tile_start,
-                                                         const uint32_t *__restrict__ keys,
-                                                         uint32_t *__restrict__ vals,
-                                                         const uint8_t *__restrict__ pbits,
-                                                         uint32_t *__restrict__ sub_lists,
-                                                         uint32_t *__restrict__ sub_count,
-                                                         uint32_t *__restrict__ radix_list,
-                                                         DevScalars *__restrict__ dev, int T,
-                                                         const uint32_t *__restrict__ chunk_list = nullptr,
-                                                         const uint32_t *__restrict__ ckeys = nullptr,
-                                                         const uint32_t *__restrict__ cvals = nullptr,
-                                                         const uint32_t *__restrict__ cbits = nullptr) {
-    constexpr int NW = NT / 32;
-    constexpr int PT = NB / NT;
-    static_assert(PT >= 1 && PT * NT == NB, "NB must be a multiple of NT");
-    extern __shared__ uint32_t sm[];
-    __shared__ uint32_t red[4][32];
-    __shared__ unsigned long long red64[2][33];
-    __shared__ uint32_t s_desc[12];
-    for (int it = 0;; ++it) {
-    int tile, n, off = 0, ntile;
-    if (CHUNKED) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const unsigned w = atomicAdd(&dev->chunk_next, 1u);
-            s_desc[0] = w < dev->chunk_count ? 1u : 0u;
-            if (w < dev->chunk_count)
-                for (int q = 0; q < 11; ++q) s_desc[1 + q] = chunk_list[(size_t)12 * w + q];
-        }
-        __syncthreads();
-        if (!s_desc[0]) return;
-        tile = (int)s_desc[1];
-        off = (int)s_desc[2];
-        n = (int)s_desc[3];
-        ntile = (int)tile_count[tile];
-    } else {
-        if (it > 0) return;
-        tile = blockIdx.x;
-        n = ntile = (int)tile_count[tile];
-        if (n <= LO || n > CAP) continue;
-    }
-    constexpr int kLogNB = NB == 8192 ? 13 : (NB == 4096 ? 12 : (NB == 2048 ? 11 : 10));
-    static_assert((1 << kLogNB) == NB, "NB must be 1024 … 8192");
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const uint32_t base = tile_start[tile];
-    uint32_t *K = sm, *V = sm + CAP, *K2 = sm + 2 * CAP, *V2 = sm + 3 * CAP, *H = sm + 4 * CAP;
-    uint8_t *B = reinterpret_cast<uint8_t *>(sm + 4 * CAP + NB), *B2 = B + CAP;
-    uint32_t kmin = 0xffffffffu, kmax = 0u;
-    for (int i = tid; i < n; i += NT) {
-        const uint32_t k = CHUNKED ? __ldg(ckeys + base + off + i) : __ldg(keys + base + i);
-        K[i] = k;
-        V[i] = CHUNKED ? __ldg(cvals + base + off + i) : __ldg(vals + base + i);
-        B[i] = CHUNKED ? (uint8_t)__ldg(cbits + base + off + i) : __ldg(pbits + base + i);
-        kmin = min(kmin, k);
-        kmax = max(kmax, k);
-    }
-    for (int i = tid; i < NB; i += NT) H[i] = 0u;
-    kmin = __reduce_min_sync(kFull, kmin);
-    kmax = __reduce_max_sync(kFull, kmax);
-    if (lane == 0) { red[0][w] = kmin; red[1][w] = kmax; }
-    __syncthreads();
-    if (w == 0) {
-        const uint32_t a = __reduce_min_sync(kFull, lane < NW ? red[0][lane] : 0xffffffffu);
-        const uint32_t b = __reduce_max_sync(kFull, lane < NW ? red[1][lane] : 0u);
-        __syncwarp();
-        if (lane == 0) { red[0][0] = a; red[1][0] = b; }
-    }
-    __syncthreads();
-    kmin = red[0][0];
-    kmax = red[1][0];
-    const uint32_t range = kmax - kmin;
-    const int nbits = range ? 32 - __clz(range) : 0;
-    const int shift = nbits > kLogNB ? nbits - kLogNB : 0;
-    for (int i = tid; i < n; i += NT) atomicAdd(&H[(K[i] - kmin) >> shift], 1u);
-    __syncthreads();
-    uint32_t cmax = 0;
-    {   // exclusive scan of the NB counts: PT per thread, then a block scan of the sums
-        uint32_t c[PT], tot = 0;
-#pragma unroll
-        for (int j = 0; j < PT; ++j) {
-            c[j] = H[tid * PT + j];
-            tot += c[j];
-            cmax = max(cmax, c[j]);
-        }
-        uint32_t incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += y;
-        }
-        cmax = __reduce_max_sync(kFull, cmax);
-        if (lane == 31) red[2][w] = incl;
-        if (lane == 0) red[3][w] = cmax;
-        __syncthreads();
-        if (w == 0) {   // exclusive scan of the warps' sums, max of their largest buckets
-            const uint32_t a = lane < NW ? red[2][lane] : 0u;
-            uint32_t ia = a;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(kFull, ia, o);
-                if (lane >= o) ia += y;
-            }
-            const uint32_t m = __reduce_max_sync(kFull, lane < NW ? red[3][lane] : 0u);
-            __syncwarp();
-            red[2][lane] = ia - a;
-            red[3][lane] = m;
-        }
-        __syncthreads();
-        uint32_t run = incl - tot + red[2][w];
-        cmax = red[3][0];
-#pragma unroll
-        for (int j = 0; j < PT; ++j) {
-            H[tid * PT + j] = run;
-            run += c[j];
-        }
-    }
-    if (!CHUNKED && cmax > (uint32_t)kMaxBucket) {   // degenerate depth distribution → the radix kernel's list
-        if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;
-        continue;
-    }
-    __syncthreads();
-    for (int i = tid; i < n; i += NT) {
-        const uint32_t k = K[i];
-        const uint32_t pos = atomicAdd(&H[(k - kmin) >> shift], 1u);  // H[b] becomes the segment end
-        K2[pos] = k;
-        V2[pos] = V[i];
-        B2[pos] = B[i];
-    }
-    __syncthreads();
-    for (int p = tid; p < n; p += NT) {
-        const uint32_t k = K2[p], v = V2[p];
-        const uint32_t b = (k - kmin) >> shift;
-        const int s0 = b ? (int)H[b - 1] : 0, s1 = (int)H[b];
-        int rank = 0;
-        for (int j = s0; j < s1; ++j) {
-            const uint32_t kj = K2[j];
-            rank += (kj < k || (kj == k && V2[j] < v)) ? 1 : 0;
-        }
-        V[s0 + rank] = v;
-        B[s0 + rank] = B2[p];
-    }
-    __syncthreads();
-    for (int i = tid; i < n; i += NT) vals[base + off + i] = V[i];
-    sublists_from_bits<NT>(V, B, n, sub_lists + (size_t)8 * base, sub_count + 8 * tile, red64, ntile,
-                           CHUNKED ? s_desc + 4 : nullptr);
-    }
-}
-
-
-// ------------------------------------------------------------------------------------------
 // K5, long lists (> kSortCap entries, configs 4 / 5): instead of one CTA sorting the whole list
-// on global scratch, one CTA per long tile buckets it by depth — block min / max of the z bits,
+// on global scratch, the long tile's CTA of the bucket-sort launch (k_tile_sort_bucket, which
+// would otherwise skip it) buckets it by depth — block min / max of the z bits,
 // NB buckets over that range (4,096 / 16,384 by length), segment starts s_b — and cuts it into CHUNKS:
 // chunk(b) = ⌊s_b / tgt⌋ with tgt = kSortCap − max(largest bucket, kMaxBucket), so a chunk holds
 // ≤ kSortCap entries and chunks are depth-ordered.  The pairs are scattered into bucket order (keys2 /
@@ -665,6 +510,8 @@ __global__ void __launch_bounds__(NT) k_tile_sort_bucket(const uint32_t *__restr
 // chip (many CTAs per long tile).  A tile with a bucket > kSortCap / 2 (near-equal depths) or
 // more than kMaxChunks chunks goes to the radix kernel as before.
 // ------------------------------------------------------------------------------------------
+// dynamic shared memory of the on-chip bucket sort of lists ≤ cap with nb buckets
+__host__ __device__ constexpr size_t bucket_smem(int cap, int nb) { return (4 * (size_t)cap + nb) * sizeof(uint32_t) + 2 * (size_t)cap; }
 constexpr int kMaxChunks = 64;
 constexpr int kPlanBuckets = 16384;   // fine enough that config 5's densest wall stays ≤ 2048 per bucket
 constexpr size_t kPlanSmem = (size_t)kPlanBuckets * (sizeof(uint32_t) + sizeof(uint8_t));
@@ -799,52 +646,185 @@ __device__ __forceinline__ void plan_tile(int tile, int n, uint32_t base, const 
     }
 }
 
-template <int NT>
-__global__ void __launch_bounds__(NT) k_chunk_plan(const uint32_t *__restrict__ tile_count,
-                                                   const uint32_t *__restrict__ tile_start,
-                                                   const uint32_t *__restrict__ keys,
-                                                   const uint32_t *__restrict__ vals,
-                                                   const uint8_t *__restrict__ pbits,
-                                                   uint32_t *__restrict__ keys2, uint32_t *__restrict__ vals2,
-                                                   uint32_t *__restrict__ bits2, uint32_t *__restrict__ sub_count,
-                                                   uint32_t *__restrict__ radix_list, uint32_t *__restrict__ chunk_list,
-                                                   DevScalars *__restrict__ dev, int T) {
-    extern __shared__ uint32_t plan_smem[];
-    uint32_t *H = plan_smem;                                                  // [kPlanBuckets]
-    uint8_t *CH = reinterpret_cast<uint8_t *>(plan_smem + kPlanBuckets);     // [kPlanBuckets]
-    __shared__ uint32_t csub[kMaxChunks][8];   // per chunk, per sub-tile counts
-    __shared__ uint32_t ccnt[kMaxChunks], cbeg[kMaxChunks];
+// ------------------------------------------------------------------------------------------
+// CHUNKED = false: one CTA per tile, lists in (LO, CAP].  CHUNKED = true: a grid walks the chunk
+// work list of the long-tile plans (parts of long tiles, each ≤ CAP entries, already bucketed by depth
+// into keys2 / vals2 / bits2) and writes each part at its place in the tile's list and sub-lists.
+template <int LO, int CAP, int NB, int NT, bool CHUNKED = false>
+__global__ void __launch_bounds__(NT, 2048 / NT) k_tile_sort_bucket(const uint32_t *__restrict__ tile_count,
+                                                         const uint32_t *__restrict__ tile_start,
+                                                         const uint32_t *__restrict__ keys,
+                                                         uint32_t *__restrict__ vals,
+                                                         const uint8_t *__restrict__ pbits,
+                                                         uint32_t *__restrict__ sub_lists,
+                                                         uint32_t *__restrict__ sub_count,
+                                                         uint32_t *__restrict__ radix_list,
+                                                         DevScalars *__restrict__ dev, int T,
+                                                         uint32_t *__restrict__ chunk_list,
+                                                         uint32_t *__restrict__ ckeys,
+                                                         uint32_t *__restrict__ cvals,
+                                                         uint32_t *__restrict__ cbits) {
+    constexpr int NW = NT / 32;
+    constexpr int PT = NB / NT;
+    static_assert(PT >= 1 && PT * NT == NB, "NB must be a multiple of NT");
+    extern __shared__ uint32_t sm[];
     __shared__ uint32_t red[4][32];
-    __shared__ int s_tile;
-    const int tid = threadIdx.x;
-    for (;;) {
+    __shared__ unsigned long long red64[2][33];
+    __shared__ uint32_t s_desc[12];
+    __shared__ uint32_t csub[CHUNKED ? 1 : kMaxChunks][8];   // the long-tile plan (plan_tile)
+    __shared__ uint32_t ccnt[CHUNKED ? 1 : kMaxChunks], cbeg[CHUNKED ? 1 : kMaxChunks];
+    for (int it = 0;; ++it) {
+    int tile, n, off = 0, ntile;
+    if (CHUNKED) {
         __syncthreads();
-        if (tid == 0) {
-            const unsigned x = atomicAdd(&dev->big_next, 1u);
-            s_tile = x < dev->big_count ? (int)radix_list[T + x] : -1;
+        if (threadIdx.x == 0) {
+            const unsigned w = atomicAdd(&dev->chunk_next, 1u);
+            s_desc[0] = w < dev->chunk_count ? 1u : 0u;
+            if (w < dev->chunk_count)
+                for (int q = 0; q < 11; ++q) s_desc[1 + q] = chunk_list[(size_t)12 * w + q];
         }
         __syncthreads();
-        const int tile = s_tile;
-        if (tile < 0) return;
-        const int n = (int)tile_count[tile];
-        const uint32_t base = tile_start[tile];
-        if (n > kMaxChunks * (kSortCap / 2)) {   // beyond the plan's capacity: radix sort
-            if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;
+        if (!s_desc[0]) return;
+        tile = (int)s_desc[1];
+        off = (int)s_desc[2];
+        n = (int)s_desc[3];
+        ntile = (int)tile_count[tile];
+    } else {
+        if (it > 0) return;
+        tile = blockIdx.x;
+        n = ntile = (int)tile_count[tile];
+        if (n > CAP) {   // a long list: this CTA plans its chunks (k_tile_sort_bucket<…, CHUNKED> sorts them)
+            if constexpr (!CHUNKED) {
+                static_assert(bucket_smem(CAP, NB) >= kPlanSmem, "the plan reuses the bucket sort's shared memory");
+                const uint32_t b0 = tile_start[tile];
+                if (n > kMaxChunks * (kSortCap / 2)) {   // beyond the plan's capacity: radix sort
+                    if (threadIdx.x == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;
+                } else if (n <= 16384) {
+                    plan_tile<4096, NT>(tile, n, b0, keys, vals, pbits, ckeys, cvals, cbits, sub_count, radix_list,
+                                        chunk_list, dev, sm, reinterpret_cast<uint8_t *>(sm + kPlanBuckets), csub,
+                                        ccnt, cbeg, red);
+                } else {
+                    plan_tile<kPlanBuckets, NT>(tile, n, b0, keys, vals, pbits, ckeys, cvals, cbits, sub_count,
+                                                radix_list, chunk_list, dev, sm,
+                                                reinterpret_cast<uint8_t *>(sm + kPlanBuckets), csub, ccnt, cbeg, red);
+                }
+            }
             continue;
         }
-        if (n <= 16384)
-            plan_tile<4096, NT>(tile, n, base, keys, vals, pbits, keys2, vals2, bits2, sub_count, radix_list,
-                                chunk_list, dev, H, CH, csub, ccnt, cbeg, red);
-        else
-            plan_tile<kPlanBuckets, NT>(tile, n, base, keys, vals, pbits, keys2, vals2, bits2, sub_count,
-                                        radix_list, chunk_list, dev, H, CH, csub, ccnt, cbeg, red);
+        if (n <= LO) continue;
+    }
+    constexpr int kLogNB = NB == 8192 ? 13 : (NB == 4096 ? 12 : (NB == 2048 ? 11 : 10));
+    static_assert((1 << kLogNB) == NB, "NB must be 1024 … 8192");
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t base = tile_start[tile];
+    uint32_t *K = sm, *V = sm + CAP, *K2 = sm + 2 * CAP, *V2 = sm + 3 * CAP, *H = sm + 4 * CAP;
+    uint8_t *B = reinterpret_cast<uint8_t *>(sm + 4 * CAP + NB), *B2 = B + CAP;
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    for (int i = tid; i < n; i += NT) {
+        const uint32_t k = CHUNKED ? __ldg(ckeys + base + off + i) : __ldg(keys + base + i);
+        K[i] = k;
+        V[i] = CHUNKED ? __ldg(cvals + base + off + i) : __ldg(vals + base + i);
+        B[i] = CHUNKED ? (uint8_t)__ldg(cbits + base + off + i) : __ldg(pbits + base + i);
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
+    }
+    for (int i = tid; i < NB; i += NT) H[i] = 0u;
+    kmin = __reduce_min_sync(kFull, kmin);
+    kmax = __reduce_max_sync(kFull, kmax);
+    if (lane == 0) { red[0][w] = kmin; red[1][w] = kmax; }
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t a = __reduce_min_sync(kFull, lane < NW ? red[0][lane] : 0xffffffffu);
+        const uint32_t b = __reduce_max_sync(kFull, lane < NW ? red[1][lane] : 0u);
+        __syncwarp();
+        if (lane == 0) { red[0][0] = a; red[1][0] = b; }
+    }
+    __syncthreads();
+    kmin = red[0][0];
+    kmax = red[1][0];
+    const uint32_t range = kmax - kmin;
+    const int nbits = range ? 32 - __clz(range) : 0;
+    const int shift = nbits > kLogNB ? nbits - kLogNB : 0;
+    for (int i = tid; i < n; i += NT) atomicAdd(&H[(K[i] - kmin) >> shift], 1u);
+    __syncthreads();
+    uint32_t cmax = 0;
+    {   // exclusive scan of the NB counts: PT per thread, then a block scan of the sums
+        uint32_t c[PT], tot = 0;
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+            c[j] = H[tid * PT + j];
+            tot += c[j];
+            cmax = max(cmax, c[j]);
+        }
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        cmax = __reduce_max_sync(kFull, cmax);
+        if (lane == 31) red[2][w] = incl;
+        if (lane == 0) red[3][w] = cmax;
+        __syncthreads();
+        if (w == 0) {   // exclusive scan of the warps' sums, max of their largest buckets
+            const uint32_t a = lane < NW ? red[2][lane] : 0u;
+            uint32_t ia = a;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, ia, o);
+                if (lane >= o) ia += y;
+            }
+            const uint32_t m = __reduce_max_sync(kFull, lane < NW ? red[3][lane] : 0u);
+            __syncwarp();
+            red[2][lane] = ia - a;
+            red[3][lane] = m;
+        }
+        __syncthreads();
+        uint32_t run = incl - tot + red[2][w];
+        cmax = red[3][0];
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+            H[tid * PT + j] = run;
+            run += c[j];
+        }
+    }
+    if (!CHUNKED && cmax > (uint32_t)kMaxBucket) {   // degenerate depth distribution → the radix kernel's list
+        if (tid == 0) radix_list[atomicAdd(&dev->radix_count, 1u)] = (uint32_t)tile;
+        continue;
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) {
+        const uint32_t k = K[i];
+        const uint32_t pos = atomicAdd(&H[(k - kmin) >> shift], 1u);  // H[b] becomes the segment end
+        K2[pos] = k;
+        V2[pos] = V[i];
+        B2[pos] = B[i];
+    }
+    __syncthreads();
+    for (int p = tid; p < n; p += NT) {
+        const uint32_t k = K2[p], v = V2[p];
+        const uint32_t b = (k - kmin) >> shift;
+        const int s0 = b ? (int)H[b - 1] : 0, s1 = (int)H[b];
+        int rank = 0;
+        for (int j = s0; j < s1; ++j) {
+            const uint32_t kj = K2[j];
+            rank += (kj < k || (kj == k && V2[j] < v)) ? 1 : 0;
+        }
+        V[s0 + rank] = v;
+        B[s0 + rank] = B2[p];
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) vals[base + off + i] = V[i];
+    sublists_from_bits<NT>(V, B, n, sub_lists + (size_t)8 * base, sub_count + 8 * tile, red64, ntile,
+                           CHUNKED ? s_desc + 4 : nullptr);
     }
 }
+
+
 
 constexpr int kSortCapBig = 8192;
 constexpr size_t kSortSmem = 4 * kSortCap * sizeof(uint32_t) + kSortCap * sizeof(uint16_t);
 constexpr size_t kSortSmemBig = 4 * kSortCapBig * sizeof(uint32_t) + kSortCapBig * sizeof(uint16_t);
-constexpr size_t bucket_smem(int cap, int nb) { return (4 * (size_t)cap + nb) * sizeof(uint32_t) + 2 * (size_t)cap; }
 
 static int sort_variant() {
     static int v = -1;
@@ -888,19 +868,18 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
         LaunchScope ls(&c, kSort, s);
         // every launch exits at once for the tiles it does not own
         if (sort_variant()) {
-            // longer lists: chunked (k_chunk_plan); flagged (degenerate) tiles: the radix kernel.
+            // longer lists: chunked (plan_tile); flagged (degenerate) tiles: the radix kernel.
             // One launch for every list ≤ kSortCap (short and long tiles' CTAs interleave; two
             // launches split at 2,048 left each one's tail exposed: 0.143 → 0.136 ms at config 2)
+            // (its CTAs of longer lists plan their depth chunks of ≤ kSortCap entries instead)
             k_tile_sort_bucket<-1, kSortCap, 4096, 1024><<<T, 1024, bucket_smem(kSortCap, 4096), s>>>(
-                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T);
-            // lists > kSortCap: depth-bucketed into chunks of ≤ kSortCap entries, chunks sorted on chip
-            k_chunk_plan<1024><<<c.num_sms, 1024, kPlanSmem, s>>>(
-                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.keys2, c.vals2, c.offs, c.sub_count,
-                c.tile_flag, c.chunk_list, c.dev, T);
+                c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T,
+                c.chunk_list, c.keys2, c.vals2, c.offs);
+            // the chunks of the long lists, sorted on chip
             k_tile_sort_bucket<0, kSortCap, 4096, 1024, true><<<2 * c.num_sms, 1024, bucket_smem(kSortCap, 4096), s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T,
                 c.chunk_list, c.keys2, c.vals2, c.offs);
-            c.launches += 2;
+            ++c.launches;
             k_tile_sort<kSortCap, kSortCapBig, true><<<c.num_sms, kBlock, kSortSmemBig, s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.keys2, c.vals2, c.offs, c.rect, ntx, c.sub_lists,
                 c.sub_count, c.tile_flag, c.dev);
@@ -928,9 +907,6 @@ cudaError_t forward_set_attributes() {
         e = cudaFuncSetAttribute(k_tile_sort_bucket<-1, kSortCap, 4096, 1024>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, 4096));
 
-    if (!e)
-        e = cudaFuncSetAttribute(k_chunk_plan<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kPlanSmem);
     if (!e)
         e = cudaFuncSetAttribute(k_tile_sort_bucket<0, kSortCap, 4096, 1024, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, 4096));

@@ -38,9 +38,7 @@ struct DevScalars {
     unsigned int count_d;
     unsigned int fin_ticket;  // k_pose_finalize last-block ticket (self-resetting)
     unsigned int radix_count; // entries in the radix-sort work list (Ctx::tile_flag)
-    unsigned int big_count;   // entries in the long-list (> kSortCap) work list (Ctx::tile_flag + max_tiles)
-    unsigned int big_next;    // its dynamic fetch cursor
-    unsigned int chunk_count; // chunks of long tiles planned by k_chunk_plan (Ctx::chunk_list)
+    unsigned int chunk_count; // chunks of long tiles planned by plan_tile (Ctx::chunk_list)
     unsigned int chunk_next;  // their dynamic fetch cursor
 };
 
@@ -73,7 +71,7 @@ struct Ctx {
     uint32_t *keys2 = nullptr;       // fallback sort scratch [max_pairs]
     uint32_t *vals2 = nullptr;
     uint32_t *offs = nullptr;        // fallback sort ranks [max_pairs]
-    uint32_t *chunk_list = nullptr;  // k_chunk_plan's chunk descriptors, 12 u32 each [12·(max_pairs/2048 + max_tiles + 1)]
+    uint32_t *chunk_list = nullptr;  // the long-tile plans' chunk descriptors, 12 u32 each [12·(max_pairs/2048 + max_tiles + 1)]
     uint32_t *sub_masks = nullptr;   // per sub-list entry: its 32-pixel mask (forward → backward) [8·max_pairs]
     uint32_t *sub_lists = nullptr;   // per tile 8 sub-lists (8×4 sub-tiles), capacity 8·n_tile [8·max_pairs]
     uint32_t *sub_count = nullptr;   // [8·max_tiles]
