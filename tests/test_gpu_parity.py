@@ -566,6 +566,17 @@ def test_step_host_matches_device_path(vt):
     torch.cuda.synchronize()
     assert loss_h == pytest.approx(lo.item(), rel=1e-6)
     assert torch.allclose(d1, d2, rtol=1e-5, atol=1e-6)
+    # repeated calls with all-pinned host buffers (the way the bench's e2e leg calls it)
+    hv = torch.from_numpy(view32(cfg.views[0]).astype(np.float32)).pin_memory()
+    hr, hd = torch.from_numpy(tg.rgb).pin_memory(), torch.from_numpy(tg.depth).pin_memory()
+    for _ in range(3):
+        d3 = torch.zeros_like(d1)
+        r3 = torch.zeros_like(r1)
+        loss_g = R.step_host(pr, co, hv, cfg.intr, hr, hd, 0.8, 1.0, 0, 0, 0, vt.VTGS_GRAD_ATTR, (0, cfg.n_slots),
+                             out, d3, r3)
+        assert loss_g == loss_h
+        assert torch.allclose(d3, d2, rtol=1e-5, atol=1e-6)
+        assert torch.allclose(r3, r2, rtol=1e-5, atol=1e-6)
 
 
 # ------------------------------------------------------------------------------ f1 (head-frame BA)
