@@ -518,7 +518,7 @@ struct PoseRing {
 };
 
 constexpr int kPoseRingWarps = 2;
-constexpr int kPoseInner = 4;
+constexpr int kPoseInner = 8;   // lane-independent steps between warp checks (4 → 8: tracking backward 14.5 → 14.0 ms per frame)
 constexpr float kExpScale9P = -4.5f * kLog2e;   // −log2(e)/(2σ²) = kExpScale9P / (9σ²), as the forward
 
 template <int R, bool LOSS>
