@@ -481,7 +481,7 @@ def main():
     if not args.profile_run:
         h_tg = [(torch.from_numpy(t.rgb).pin_memory(), torch.from_numpy(t.depth).pin_memory()) for t in tgts]
         h_views = [torch.from_numpy(v.reshape(7).copy()).pin_memory() for v in views_np]
-        for _ in range(2):
+        for _ in range(max(args.warmup, 20)):   # fresh pinned buffers and an idle host: let them settle
             grads.zero_()
             for hv, (hr, hd) in zip(h_views, h_tg):
                 R.step_host(pr, co, hv, cfg.intr, hr, hd, wc, wd, 0, 0, 0, want, (0, N), out, d_co, d_r)
