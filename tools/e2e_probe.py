@@ -35,3 +35,14 @@ print(f"per-call wall median {1e3 * np.median(ts):.3f} ms")
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record(); step(); ev[1].record(); torch.cuda.synchronize()
 print(f"device time of one call {ev[0].elapsed_time(ev[1]):.3f} ms")
+grads = torch.zeros(5 * N, device=dev)
+d_co2, d_r2 = grads[:4 * N].view(N, 4), grads[4 * N:]
+def step2():
+    grads.zero_()
+    return R.step_host(pr, co, hv, cfg.intr, hr, hd, 0.8, 1.0, 0, 0, 0, want, (0, N), out, d_co2, d_r2)
+for _ in range(5): step2()
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(n): step2()
+torch.cuda.synchronize()
+print(f"zero + step_host wall {1e3 * (time.perf_counter() - t0) / n:.3f} ms/step")
