@@ -17,6 +17,7 @@ this tier) on a bounded row band of the same workload.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -68,8 +69,11 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region.  The sampler process
+    starts before the warm-up (nvidia-smi needs ~0.1-0.3 s to produce its first line); mark()
+    brackets the timed region on the host clock and only samples stamped inside it (±25 ms) are
+    kept; a region shorter than the sampling period keeps the sample nearest to it instead."""
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -78,6 +82,7 @@ class ClockSampler:
         self.proc = None
         self.lines = []
         self.t = None
+        self.region = None
 
     def start(self):
         try:
@@ -93,9 +98,18 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def mark_start(self):
+        self.region = [time.time(), None]
+
+    def mark_stop(self):
+        if self.region:
+            self.region[1] = time.time()
+
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if self.region and self.region[1] is not None:
+            time.sleep(0.12)   # let the sample after the region arrive
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -103,22 +117,37 @@ class ClockSampler:
             self.proc.kill()
         if self.t:
             self.t.join(timeout=2)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
+            if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[1]), float(parts[2]), parts[5:9]))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[4:8]):
+        note = None
+        if self.region and self.region[1] is not None and rows:
+            t0, t1 = self.region
+            inside = [r for r in rows if t0 - 0.025 <= r[0] <= t1 + 0.025]
+            if not inside:
+                mid = 0.5 * (t0 + t1)
+                inside = [min(rows, key=lambda r: abs(r[0] - mid))]
+                note = f"timed region {1e3 * (t1 - t0):.0f} ms < sampling period: nearest sample"
+            rows = inside
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for n, v in zip(names, r[3]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median([r[1] for r in rows]) if rows else None,
+               "sm_max_mhz": max(r[2] for r in rows) if rows else None,
+               "reasons": sorted(reasons), "samples": len(rows)}
+        if note:
+            out["note"] = note
+        return out
 
 
 def dist_env():
@@ -255,15 +284,16 @@ def run_tracking(args):
     with torch.cuda.graph(g, stream=s):
         body(s)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    clocks = ClockSampler(local)
+    clocks.start()                        # before the warm-up: nvidia-smi's first line takes a while
     for _ in range(max(args.warmup, 1)):
         pose.copy_(init); state.zero_(); g.replay()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clocks = ClockSampler(local)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark_start()
     cur = torch.cuda.current_stream()
     for i in range(args.steps):
         flush.fill_(float(i))
@@ -273,6 +303,7 @@ def run_tracking(args):
         g.replay()
         ev[i][1].record(cur)
     torch.cuda.synchronize()
+    clocks.mark_stop()
     if ws > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -367,6 +398,9 @@ def main():
     def step():
         mapper.step(allreduce=ws > 1)
 
+    clocks = ClockSampler(local) if not args.profile_run else None
+    if clocks:
+        clocks.start()                    # before the warm-up: nvidia-smi's first line takes a while
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
@@ -399,12 +433,11 @@ def main():
     R.profile()                                            # reset
     launches0 = R.stats()["launches"]
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clocks = ClockSampler(local) if not args.profile_run else None
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     if clocks:
-        clocks.start()
+        clocks.mark_start()
     replays = 0
     for i in range(args.steps):
         flush.fill_(float(i))                               # evict L2 between steps (not timed)
@@ -418,6 +451,8 @@ def main():
             step()
         ev[i][1].record(stream)
     torch.cuda.synchronize()
+    if clocks:
+        clocks.mark_stop()
     if ws > 1:
         dist.barrier()
     clk = clocks.stop() if clocks else None
