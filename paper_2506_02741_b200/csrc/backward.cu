@@ -562,8 +562,7 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
     EntryStream st;
     stream_start<false>(st, list, bb_top + (int)lane, bb_top - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
     uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
-    float4 posn = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (bb_top + (int)lane >= 0 && bb_top + (int)lane < cnt) posn = __ldg(p.pos_rad + st.e.g);
+    const float ifx = 1.0f / fx, ify = 1.0f / fy;
     int built = 0;
     auto build = [&]() {
         const int bb = bb_top - 32 * built;
@@ -576,10 +575,10 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
             const float4 A = make_float4(e.pr.x, e.pr.y, __fmul_rn(9.0f, s2), e.co.w);
             ring.A[slot + lane] = A;
             ring.B[slot + lane] = make_float4(e.co.x, e.co.y, e.co.z, e.pr.z);
-            float xc[3];
-            view_transform(P.R, P.t, posn, xc);
+            // X_c from the projection itself (x = (u − cx)·z / fx, …): no gather of the world centre
             const float iz = 1.0f / e.pr.z;
-            ring.Xq[slot + lane] = make_float4(xc[0], xc[1], xc[2], e.co.w / s2);
+            ring.Xq[slot + lane] = make_float4((e.pr.x - cxp) * e.pr.z * ifx, (e.pr.y - cyp) * e.pr.z * ify, e.pr.z,
+                                               e.co.w / s2);
             ring.iz[slot + lane] = e.pr.w > 0.f ? iz : -iz;
             mj = mnx & onmask;
         }
@@ -591,7 +590,6 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
         const int nidx = bb - 32 + (int)lane;
         stream_next<false>(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
         mnx = load_mask(mlist, nidx, wmax);
-        if (nidx >= 0 && nidx < cnt) posn = __ldg(p.pos_rad + st.e.g);
     };
     while (built < nb && built < R) build();
     __syncwarp();
