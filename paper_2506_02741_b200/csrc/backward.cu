@@ -192,11 +192,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             sA[wl_][lane] = Aj;
             sB[wl_][lane] = cur.co;
             sZ[wl_][lane] = cur.pr.z;
-            if (POSE) {
-                float xc[3];
-                view_transform(P.R, P.t, __ldg(p.pos_rad + cur.g), xc);
-                sX[wl_][lane] = make_float4(xc[0], xc[1], xc[2], cur.pr.w);
-            }
+            if (POSE)   // camera-space centre from the projection (x = (u − cx)·z / fx, …)
+                sX[wl_][lane] = make_float4((cur.pr.x - p.in.cx) * cur.pr.z / p.in.fx,
+                                            (cur.pr.y - p.in.cy) * cur.pr.z / p.in.fy, cur.pr.z, cur.pr.w);
             mj = mcur & onmask;
         }
         __syncwarp();
@@ -379,9 +377,6 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p
     const int n = (int)p.tile_count[tile];
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
-    PoseR P;
-    pose_rotation(*p.view, P);
-
     const PixelUp up = pixel_upstream<LOSS>(p, px, py, inside);
     const float g0 = up.g0, g1 = up.g1, g2 = up.g2, gD = up.gD, gS = up.gS;
     const float r0 = up.r0, r1 = up.r1, r2 = up.r2, rz = up.rz;
@@ -410,11 +405,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p
             sA[wl_][lane] = Aj;
             sB[wl_][lane] = cur.co;
             sZ[wl_][lane] = cur.pr.z;
-            float xc[3];
-            view_transform(P.R, P.t, __ldg(p.pos_rad + cur.g), xc);
             const float z = cur.pr.z, s = fabsf(cur.pr.w), iz = 1.0f / z;
             sP1[wl_][lane] = make_float4(p.in.fx * iz, p.in.fy * iz, (Aj.x - p.in.cx) * iz, (Aj.y - p.in.cy) * iz);
-            sP2[wl_][lane] = make_float4(xc[0], xc[1], xc[2], cur.co.w / (s * s));
+            sP2[wl_][lane] = make_float4((Aj.x - p.in.cx) * z / p.in.fx, (Aj.y - p.in.cy) * z / p.in.fy, z,
+                                         cur.co.w / (s * s));   // X_c from the projection
             sP3[wl_][lane] = cur.pr.w > 0.f ? iz : 0.f;   // ∂σ/∂z = −σ/z only when σ is unclamped
             mj = mcur & onmask;
         }
@@ -540,9 +534,6 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const int cnt = (int)p.sub_count[tile * 8 + sub];
-    PoseR P;
-    pose_rotation(*p.view, P);
-
     const PixelUp up = pixel_upstream<LOSS>(p, px, py, inside);
     const float g0 = up.g0, g1 = up.g1, g2 = up.g2, gD = up.gD, gS = up.gS;
     const float r0 = up.r0, r1 = up.r1, r2 = up.r2, rz = up.rz;
