@@ -110,6 +110,18 @@ __device__ __forceinline__ unsigned lane_mask(const float4 A, const uint2 r, int
     return m;
 }
 
+// The entry's ±3σ pixel rect recomputed from its projection with exactly k_project_count's fp32
+// operations (|proj.w| is the clamped σ it used), so the compositing kernels need not gather it.
+__device__ __forceinline__ uint2 rect_from_proj(const float4 pr, int W, int H) {
+    const float e = __fmul_rn(3.0f, fabsf(pr.w));
+    const float Wm1 = (float)(W - 1), Hm1 = (float)(H - 1);
+    const float cx0 = ceilf(__fsub_rn(pr.x, e)), cx1 = floorf(__fadd_rn(pr.x, e));
+    const float cy0 = ceilf(__fsub_rn(pr.y, e)), cy1 = floorf(__fadd_rn(pr.y, e));
+    const int x0 = cx0 < 0.0f ? 0 : (int)cx0, x1 = cx1 > Wm1 ? (int)Wm1 : (int)cx1;
+    const int y0 = cy0 < 0.0f ? 0 : (int)cy0, y1 = cy1 > Hm1 ? (int)Hm1 : (int)cy1;
+    return make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
+}
+
 // 32×32 bit-matrix transpose across the warp: lane j holds row j on entry, lane i holds
 // column i on exit (bit j of the result = bit i of lane j's input).
 __device__ __forceinline__ unsigned transpose32(unsigned x, unsigned lane) {

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     const unsigned inmask = __ballot_sync(kFullMask, inside);
 
     EntryStream st;
-    stream_start(st, list, (int)lane, 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    stream_start<false>(st, list, (int)lane, 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
     const EntryRegs &nxt = st.e;
     int built = 0;
     // build batch `built` from the prefetched registers, prefetch the one after it
@@ -175,13 +175,13 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
             const float4 A = make_float4(nxt.pr.x, nxt.pr.y, s9, nxt.co.w);
             ring.A[slot + lane] = A;
             ring.B[slot + lane] = make_float4(nxt.co.x, nxt.co.y, nxt.co.z, nxt.pr.z);
-            const unsigned m0 = lane_mask(A, nxt.r, sx, sy);
+            const unsigned m0 = lane_mask(A, rect_from_proj(nxt.pr, p.W, p.H), sx, sy);
             mout[idx] = m0;
             mj = m0 & inmask;
         }
         ring.bits[slot + lane] = __brev(transpose32(mj, lane));  // bit 31 − j = entry j
         ++built;
-        stream_next(st, list, (built + 1) * 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        stream_next<false>(st, list, (built + 1) * 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
     };
     while (built < nb && built < R) build();
     __syncwarp();
