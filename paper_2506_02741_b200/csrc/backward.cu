@@ -296,14 +296,14 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             // dL/dw·w = dL/dα·o·w;  ∂w/∂σ = w d²/σ³, ∂w/∂u = w (x−u)/σ², ∂w/∂v = w (y−v)/σ²
             const float s = fabsf(cur.pr.w);
             const float inv_s2 = __fdividef(1.0f, s * s);
-            const float dsg = B.w * sw2 * inv_s2 / s;
+            const float dsg = B.w * sw2 * inv_s2 * rcp_approx(s);
             if (ATTR && (int64_t)cur.g >= p.learn_begin && (int64_t)cur.g < p.learn_end) {
                 const bool wc = p.want & VTGS_GRAD_COLOR, wo = p.want & VTGS_GRAD_OPACITY;
                 if ((wc && (dc0 != 0.f || dc1 != 0.f || dc2 != 0.f)) || (wo && dop != 0.f))
                     atomicAdd(&p.d_col_opa[cur.g],
                               make_float4(wc ? dc0 : 0.f, wc ? dc1 : 0.f, wc ? dc2 : 0.f, wo ? dop : 0.f));
                 if ((p.want & VTGS_GRAD_RADIUS) && cur.pr.w > 0.f && dsg != 0.f)
-                    atomicAdd(&p.d_radius[cur.g], dsg * fmean / z);  // ∂σ/∂r = f/z
+                    atomicAdd(&p.d_radius[cur.g], dsg * fmean * rcp_approx(z));  // ∂σ/∂r = f/z
             }
             if (POSE) {
                 const float4 X = sX[wl_][lane];
