@@ -193,8 +193,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             sB[wl_][lane] = cur.co;
             sZ[wl_][lane] = cur.pr.z;
             if (POSE)   // camera-space centre from the projection (x = (u − cx)·z / fx, …)
-                sX[wl_][lane] = make_float4((cur.pr.x - p.in.cx) * cur.pr.z / p.in.fx,
-                                            (cur.pr.y - p.in.cy) * cur.pr.z / p.in.fy, cur.pr.z, cur.pr.w);
+                sX[wl_][lane] = make_float4((cur.pr.x - p.in.cx) * cur.pr.z * rcp_approx(p.in.fx),
+                                            (cur.pr.y - p.in.cy) * cur.pr.z * rcp_approx(p.in.fy), cur.pr.z, cur.pr.w);
             mj = mcur & onmask;
         }
         __syncwarp();
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             if (POSE) {
                 const float4 X = sX[wl_][lane];
                 const float du = B.w * swx * inv_s2, dv = B.w * swy * inv_s2;
-                const float iz = 1.0f / z;
+                const float iz = rcp_approx(z);
                 float dzt = dzd - (du * (Aj.x - p.in.cx) + dv * (Aj.y - p.in.cy)) * iz;
                 if (X.w > 0.f) dzt -= dsg * s * iz;  // ∂σ/∂z = −σ/z (unclamped)
                 const float gx = du * p.in.fx * iz, gy = dv * p.in.fy * iz, gz = dzt;
@@ -405,10 +405,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p
             sA[wl_][lane] = Aj;
             sB[wl_][lane] = cur.co;
             sZ[wl_][lane] = cur.pr.z;
-            const float z = cur.pr.z, s = fabsf(cur.pr.w), iz = 1.0f / z;
+            const float z = cur.pr.z, s = fabsf(cur.pr.w), iz = rcp_approx(z);
             sP1[wl_][lane] = make_float4(p.in.fx * iz, p.in.fy * iz, (Aj.x - p.in.cx) * iz, (Aj.y - p.in.cy) * iz);
-            sP2[wl_][lane] = make_float4((Aj.x - p.in.cx) * z / p.in.fx, (Aj.y - p.in.cy) * z / p.in.fy, z,
-                                         cur.co.w / (s * s));   // X_c from the projection
+            sP2[wl_][lane] = make_float4((Aj.x - p.in.cx) * z * rcp_approx(p.in.fx), (Aj.y - p.in.cy) * z * rcp_approx(p.in.fy),
+                                         z, cur.co.w * rcp_approx(s * s));   // X_c from the projection
             sP3[wl_][lane] = cur.pr.w > 0.f ? iz : 0.f;   // ∂σ/∂z = −σ/z only when σ is unclamped
             mj = mcur & onmask;
         }
@@ -567,9 +567,9 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
             ring.A[slot + lane] = A;
             ring.B[slot + lane] = make_float4(e.co.x, e.co.y, e.co.z, e.pr.z);
             // X_c from the projection itself (x = (u − cx)·z / fx, …): no gather of the world centre
-            const float iz = 1.0f / e.pr.z;
+            const float iz = rcp_approx(e.pr.z);
             ring.Xq[slot + lane] = make_float4((e.pr.x - cxp) * e.pr.z * ifx, (e.pr.y - cyp) * e.pr.z * ify, e.pr.z,
-                                               e.co.w / s2);
+                                               e.co.w * rcp_approx(s2));
             ring.iz[slot + lane] = e.pr.w > 0.f ? iz : -iz;
             mj = mnx & onmask;
         }
