@@ -98,13 +98,15 @@ __global__ void __launch_bounds__(kSsThreads) k_ssim_moments(const float *__rest
                 const float mx = acc[0][o], my = acc[1][o], exx = acc[2][o], eyy = acc[3][o], exy = acc[4][o];
                 const float A1 = 2.f * mx * my + kC1, A2 = 2.f * (exy - mx * my) + kC2;
                 const float B1 = mx * mx + my * my + kC1, B2 = (exx - mx * mx) + (eyy - my * my) + kC2;
-                const float S = (A1 * A2) / (B1 * B2);
+                // one approximate reciprocal per factor instead of seven IEEE divisions per pixel
+                const float iA1 = rcp_approx(A1), iA2 = rcp_approx(A2), iB1 = rcp_approx(B1), iB2 = rcp_approx(B2);
+                const float S = (A1 * A2) * (iB1 * iB2);
                 ssum += (double)S;
                 const float k = dLdS * S;
                 const size_t p = (size_t)py * W + px;
-                abc[(0 * 3 + c) * npx + p] = k * (2.f * my / A1 - 2.f * my / A2 - 2.f * mx / B1 + 2.f * mx / B2);
-                abc[(1 * 3 + c) * npx + p] = -k / B2;
-                abc[(2 * 3 + c) * npx + p] = 2.f * k / A2;
+                abc[(0 * 3 + c) * npx + p] = k * (2.f * my * (iA1 - iA2) + 2.f * mx * (iB2 - iB1));
+                abc[(1 * 3 + c) * npx + p] = -k * iB2;
+                abc[(2 * 3 + c) * npx + p] = 2.f * k * iA2;
             }
         }
         __syncthreads();
