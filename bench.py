@@ -510,6 +510,15 @@ def main():
                 "peak_source": (f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
                                 f"FP32 {SM_COUNT} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz "
                                 f"(B200_PROFILING.md unit counts, max clock)")}
+    # the whole step against SURVEY §8(d)'s floors, per view: bytes 32 N (state) + 20 N (gradients)
+    # + 24 P (pairs written and read) + 68 HW (images, targets, saved T / last, re-reads); flops
+    # 20 E_eval + 60 E_comp; t_floor = max(bytes / HBM peak, flops / FP32 peak)
+    n_views_rank = len(views_np)
+    path_bytes = n_views_rank * (52.0 * N + 24.0 * P + 68.0 * HW)
+    path_flops = n_views_rank * (FLOPS_PER_EVAL_FWD * stats["e_eval"] + FLOPS_PER_COMP_BWD * stats["e_comp"])
+    t_floor_ms = max(path_bytes / (hbm_peak * 1e9), path_flops / (fp32_peak * 1e12)) * 1e3
+    path_floor = {"bytes": path_bytes, "flops": path_flops, "t_floor_ms": t_floor_ms,
+                  "frac": t_floor_ms / ms_max}
 
     # ---------------- e2e: the same step through the C-ABI with HOST buffers
     e2e = None
@@ -561,6 +570,7 @@ def main():
             "config": workload_config(cfg, args, n_views_total, len(views_np)),
             "gaussians_per_s": gps,
             "roofline": roofline,
+            "path_floor": path_floor,
             "stages": stage_json,
             "stage_timing": f"CUDA events around every kernel on every {PROFILE_EVERY}th timed step ({(args.steps + PROFILE_EVERY - 1) // PROFILE_EVERY} of {args.steps}, run eagerly), on the launching stream",
             "graph": (f"the other {replays} timed steps replay one captured CUDA graph of the step ({per_step_launches} launches)"
