@@ -375,8 +375,9 @@ __global__ void __launch_bounds__(kBlock) k_tile_sort(const uint32_t *__restrict
     // without a work list: one CTA per tile, tiles in (LO, CAP]; with one (the bucket-sort path):
     // a small grid walks the list of long / degenerate tiles that k_scan_tiles and
     // k_tile_sort_bucket appended (no wave of empty CTAs over every tile)
-    const int nwork = work_list ? (int)dev->radix_count : 1;
-    for (int w = blockIdx.x; w < (work_list ? nwork : 1); w += gridDim.x) {
+    // with a work list: w walks it; without one: a single pass, tile = blockIdx.x
+    const int nwork = work_list ? (int)dev->radix_count : (int)blockIdx.x + 1;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
     const int tile = work_list ? (int)work_list[w] : (int)blockIdx.x;
     const int n = (int)tile_count[tile];
     if (!work_list && (n <= LO || (!GLOBAL && n > CAP))) return;
