@@ -95,7 +95,7 @@ def test_tile_lists_micro_scenes(vt):
         assert np.array_equal(start, ostart) and np.array_equal(gid.astype(np.int64), ogid)
 
 
-@pytest.mark.parametrize("case", ["equal_depth", "two_depths", "long_lists", "very_long_lists"])
+@pytest.mark.parametrize("case", ["equal_depth", "two_depths", "long_lists", "very_long_lists", "equal_depth_long"])
 def test_tile_lists_sort_paths(vt, case):
     """The per-tile sort's paths, bit-exact against the oracle: equal or nearly equal depths (a
     bucket larger than the bucket sort takes → radix hand-off, ties broken by gid), and lists
@@ -103,11 +103,11 @@ def test_tile_lists_sort_paths(vt, case):
     are sorted on chip, several chunks per tile for the very long lists).  The sub-lists of the
     long tiles are checked through the forward render against the oracle's."""
     rng = np.random.Generator(np.random.PCG64([7, {"equal_depth": 0, "two_depths": 1, "long_lists": 2,
-                                                   "very_long_lists": 3}[case]]))
+                                                   "very_long_lists": 3, "equal_depth_long": 4}[case]]))
     W, H = 40, 36
     intr = Intrinsics(30.0, 30.0, (W - 1) / 2, (H - 1) / 2, W, H)
-    n = {"long_lists": 20000, "very_long_lists": 60000}.get(case, 6000)
-    if case == "equal_depth":
+    n = {"long_lists": 20000, "very_long_lists": 60000, "equal_depth_long": 30000}.get(case, 6000)
+    if case in ("equal_depth", "equal_depth_long"):   # the long one: radix sort on global scratch
         z = np.full(n, 2.0)
     elif case == "two_depths":
         z = np.where(rng.random(n) < 0.5, 2.0, np.nextafter(np.float32(2.0), np.float32(3.0)))
@@ -133,6 +133,8 @@ def test_tile_lists_sort_paths(vt, case):
         assert np.diff(ostart).max() > 4096
     if case == "very_long_lists":
         assert np.diff(ostart).max() > 3 * 4096
+    if case == "equal_depth_long":
+        assert np.diff(ostart).max() > 8192
     ref = oracle.render(pos_rad, col_opa, view32(view), intr)
     _check_images(out, ref, ref["flags"], max_flagged=2e-2)
 
