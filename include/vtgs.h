@@ -133,6 +133,23 @@ VTGS_API vtgs_status vtgs_visibility_mask(vtgs_ctx *ctx, const float *depth, con
                                  vtgs_intrinsics intr, float tol, uint8_t *mask, int64_t *n_visible,
                                  void *stream);
 
+/* Per-candidate visible-point counts for selecting the overlapping section of a head frame —
+ * PAPER.md:180 (§3.3 "Selecting Overlapping Section S^o": "we project the depth D_i from the
+ * initialized pose to each one frame in the overlap candidate view list. We count the number of
+ * visible points to each candidate view, and select the candidate views that have more visible
+ * points than a threshold γ"), SPEC.md:382-386 steps (1)-(3).  Same per-point test as
+ * vtgs_visibility_mask, but each candidate r is counted alone (no union):
+ *   depth [H×W] (the head frame, at device `pose` = its initialised pose), ref_depth [R×H×W] and
+ *   ref_poses[R] (device) the candidate views, 1 ≤ R ≤ 65535;
+ *   counts: device int64[R], OVERWRITTEN with the visible valid pixels per candidate;
+ *   n_valid: device int64 or NULL, OVERWRITTEN with the frame's valid pixels (the fraction's
+ *   denominator, PAPER.md:700 γ = 0.26 / 0.24 is a fraction).  Asynchronous on `stream`.
+ * Errors: NULL argument → VTGS_ERR_INVALID_ARG; R out of range → VTGS_ERR_SHAPE. */
+VTGS_API vtgs_status vtgs_visibility_counts(vtgs_ctx *ctx, const float *depth, const vtgs_pose *pose,
+                                   const float *ref_depth, const vtgs_pose *ref_poses, int32_t R,
+                                   vtgs_intrinsics intr, float tol, int64_t *counts, int64_t *n_valid,
+                                   void *stream);
+
 /* (2)–(4) Forward render of N Gaussians from `view` — PAPER.md:146 (Eq. 1 `splat`),
  * PAPER.md:192 (Eq. 2 multi-set render: concatenate the sets, pass the union).
  *   projection: X_c = Rᵀ(X_w − t), culled if r ≤ 0 or z ≤ 0.01 m; σ = max(f_mean·r/z, 0.3) px;

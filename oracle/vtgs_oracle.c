@@ -25,11 +25,22 @@
  * invariants, brute-force tile lists, central finite differences in fp64
  * for colour, opacity, radius and the 7 pose parameters.
  *
- * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -shared -fPIC (no FMA contraction,
- * so every fp32 decision quantity is rounded exactly as DESIGN.md §3 states).
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC (no FMA
+ * contraction, so every fp32 decision quantity is rounded exactly as DESIGN.md §3 states).
+ * OpenMP: the forward render runs its pixel rows in parallel (results independent of the thread
+ * count); the backward splits the pixels into row bands with private accumulators merged in
+ * band order.  OMP_NUM_THREADS=1 gives the single-core oracle.
  */
 #include <math.h>
 #include <stdint.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* memory budget of the backward's per-thread accumulator copies (bytes; env OR_BWD_MEM overrides) */
+#ifndef OR_BWD_MEM
+#define OR_BWD_MEM 16.0e9
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -38,7 +49,8 @@
 #include "oracle_impl.inc"
 #undef DEC
 #undef FN
-#undef OR_EPS_A
+#undef OR_EPS_DEC
+#undef OR_EPS_VAL
 #undef OR_ALPHA_MIN
 #undef OR_ALPHA_MAX
 #undef OR_T_MIN
@@ -62,16 +74,21 @@
  * normalize 0: sum over pixels (‖·‖₁ sums the 3 channels); 1: divided by the mask's pixel
  * count ("mean absolute difference over masked pixels"; empty mask → 0).
  * Upstream gradients are the subgradient with sgn(0) = 0.
- * Returns the loss value; writes gC (H×W×3), gD, gS (gS ≡ 0).  `flag` (H×W, may be NULL) is
- * set where a residual is nonzero but within 5e-5 of 0, or S within 1e-5 of 0.99, i.e. where
- * the kernel's fp32 render could take the other branch of sgn or of the mask.  (A residual
- * that is exactly 0 — e.g. a clipped black target rendered from black Gaussians — is exactly 0
- * in fp32 too.)
+ * Returns the loss value; writes gC (H×W×3), gD, gS (gS ≡ 0).
+ * Near-tie flags (the kernel renders in fp32, so its residual can take the other side of
+ * sgn): a (pixel, component) is flagged when its residual is nonzero but within `band` of 0
+ * (DESIGN.md §3 derives `band` from the measured GPU-vs-oracle render difference), and a whole
+ * pixel when S lies within 1e-5 of 0.99 under a W-mask.  `flag` (H×W, may be NULL) marks
+ * flagged pixels; `flip` (H×W×4, may be NULL) gets, per flagged component (3 colour channels,
+ * depth), the largest change of its upstream gradient the other branch could cause, 2·w·s
+ * (0 elsewhere) — the tests turn it into a per-Gaussian allowance by running or_render_bwd
+ * on it.  (A residual that is exactly 0 — e.g. a clipped black target rendered from black
+ * Gaussians — is exactly 0 in fp32 too.)
  * ------------------------------------------------------------------------------------- */
 double or_l1_upstream(const double *C, const double *D, const double *S, const double *tC,
                       const double *tD, const unsigned char *vis, int64_t npx, double w_color,
                       double w_depth, int color_mask_mode, int depth_mask_mode, int normalize,
-                      double *gC, double *gD, double *gS, int32_t *flag)
+                      double *gC, double *gD, double *gS, int32_t *flag, double band, double *flip)
 {
     int64_t nc = 0, nd = 0;
     for (int64_t p = 0; p < npx; ++p) {
@@ -88,19 +105,25 @@ double or_l1_upstream(const double *C, const double *D, const double *S, const d
         const int Wm = U && S[p] > 0.99 && (vis ? vis[p] != 0 : 1);
         const int mc = color_mask_mode ? Wm : 1;
         const int md = depth_mask_mode ? Wm : U;
-        int fl = (color_mask_mode || depth_mask_mode) && U && fabs(S[p] - 0.99) < 1e-5;
+        const int mflip = (color_mask_mode || depth_mask_mode) && U && fabs(S[p] - 0.99) < 1e-5;
+        int fl = mflip;
+        double fw[4] = {0.0, 0.0, 0.0, 0.0};
         for (int c = 0; c < 3; ++c) {
             const double r = C[3 * p + c] - tC[3 * p + c];
-            if (mc && r != 0.0 && fabs(r) < 5e-5) fl = 1;
+            const int near = mc && r != 0.0 && fabs(r) < band;
+            if (near || (mflip && color_mask_mode)) { fl = 1; fw[c] = 2.0 * fabs(w_color * sc); }
             gC[3 * p + c] = mc ? w_color * sc * (double)((r > 0) - (r < 0)) : 0.0;
             loss += mc ? w_color * sc * fabs(r) : 0.0;
         }
         const double r = D[p] - tD[p];
-        if (md && r != 0.0 && fabs(r) < 5e-5) fl = 1;
+        const int near = md && r != 0.0 && fabs(r) < band;
+        if (near || (mflip && depth_mask_mode)) { fl = 1; fw[3] = 2.0 * fabs(w_depth * sd); }
         gD[p] = md ? w_depth * sd * (double)((r > 0) - (r < 0)) : 0.0;
         loss += md ? w_depth * sd * fabs(r) : 0.0;
         gS[p] = 0.0;
         if (flag) flag[p] = fl;
+        if (flip)
+            for (int c = 0; c < 4; ++c) flip[4 * p + c] = fw[c];
     }
     return loss;
 }
@@ -216,4 +239,28 @@ int64_t or_densify_f32(const double *depth, const double *rgb, const double *pos
     free(pr);
     free(co);
     return n;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * One Adam step on a camera pose (S:207-215 adam_step: "standard first/second-moment update,
+ * β1=0.9, β2=0.999, ε=1e-8 ... quaternion renormalized after step"; learning rates per group —
+ * rotation lr_rot for q, translation lr_trans for t, "lr_rot, lr_trans").  fp64:
+ *   t ← t + 1;  m ← β1 m + (1−β1) g;  v ← β2 v + (1−β2) g²;
+ *   p ← p − lr · (m / (1 − β1^t)) / (√(v / (1 − β2^t)) + ε);  q ← q / |q|.
+ * pose[7] = (q w,x,y,z, t x,y,z) and state[15] = m[7], v[7], step are updated in place.
+ * ------------------------------------------------------------------------------------- */
+void or_pose_adam(double *pose, const double *g, double *state, double lr_rot, double lr_trans)
+{
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+    const double t = state[14] + 1.0;
+    state[14] = t;
+    const double c1 = 1.0 - pow(b1, t), c2 = 1.0 - pow(b2, t);
+    for (int i = 0; i < 7; ++i) {
+        state[i] = b1 * state[i] + (1.0 - b1) * g[i];
+        state[7 + i] = b2 * state[7 + i] + (1.0 - b2) * g[i] * g[i];
+        const double lr = i < 4 ? lr_rot : lr_trans;
+        pose[i] -= lr * (state[i] / c1) / (sqrt(state[7 + i] / c2) + eps);
+    }
+    const double n = sqrt(pose[0] * pose[0] + pose[1] * pose[1] + pose[2] * pose[2] + pose[3] * pose[3]);
+    for (int i = 0; i < 4; ++i) pose[i] /= n;
 }

@@ -292,6 +292,23 @@ vtgs_status vtgs_visibility_mask(vtgs_ctx *ctx, const float *depth, const vtgs_p
     return e ? cuda_fail(ctx, e, "vtgs_visibility_mask") : VTGS_OK;
 }
 
+vtgs_status vtgs_visibility_counts(vtgs_ctx *ctx, const float *depth, const vtgs_pose *pose, const float *ref_depth,
+                                   const vtgs_pose *ref_poses, int32_t R, vtgs_intrinsics intr, float tol,
+                                   int64_t *counts, int64_t *n_valid, void *stream) {
+    if (!ctx) return VTGS_ERR_INVALID_ARG;
+    Ctx &c = ctx->c;
+    c.last_error[0] = 0;
+    if (!depth || !pose || !ref_depth || !ref_poses || !counts)
+        return fail(ctx, VTGS_ERR_INVALID_ARG, "NULL argument to vtgs_visibility_counts");
+    if (R < 1 || R > 65535) return fail(ctx, VTGS_ERR_SHAPE, "R = %d candidate views (1..65535)", R);
+    vtgs_status st = check_intr(ctx, intr);
+    if (st) return st;
+    cudaSetDevice(c.device);
+    cudaError_t e = vtgs::launch_visibility_counts(c, depth, pose, ref_depth, ref_poses, R, intr, tol, counts,
+                                                   n_valid, (cudaStream_t)stream);
+    return e ? cuda_fail(ctx, e, "vtgs_visibility_counts") : VTGS_OK;
+}
+
 vtgs_status vtgs_densify(vtgs_ctx *ctx, const float *depth, const float *rgb, const vtgs_pose *pose,
                          vtgs_intrinsics intr, const float *silhouette, float threshold, const float *opacity,
                          float opacity_default, float *pos_rad_out, float *col_opa_out, int64_t *n_new,

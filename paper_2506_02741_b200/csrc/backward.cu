@@ -21,14 +21,13 @@ constexpr unsigned kFull = kFullMask;
 
 struct BwdArgs {
     const float4 *proj;
-    const uint2 *rect;
     const float4 *col_opa;
     const float4 *pos_rad;
     const uint32_t *tile_count;
     const uint32_t *tile_start;
     const uint32_t *sub_lists;
     const uint32_t *sub_count;
-    const uint32_t *sub_masks;   // the forward's per-entry pixel masks
+    const uint32_t *sub_masks;   // the forward's per-entry EXACT composited pixel masks
     int W, H, ntx;
     const float *color, *depth, *sil, *T_final;
     const uint32_t *last;
@@ -177,67 +176,56 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
 
     const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
     EntryRegs nxt;
-    fetch_entry<false>(nxt, list, bb_top + (int)lane, wmax, p.proj, p.col_opa, p.rect);
+    fetch_entry<false>(nxt, list, bb_top + (int)lane, wmax, p.proj, p.col_opa, nullptr);
     uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
     for (int bb = bb_top; bb >= 0; bb -= 32) {
         const EntryRegs cur = nxt;
         const uint32_t mcur = mnx;
-        fetch_entry<false>(nxt, list, bb - 32 + (int)lane, wmax, p.proj, p.col_opa, p.rect);
+        fetch_entry<false>(nxt, list, bb - 32 + (int)lane, wmax, p.proj, p.col_opa, nullptr);
         mnx = load_mask(mlist, bb - 32 + (int)lane, wmax);  // next (lower) batch
         const int jj = bb + (int)lane;
         unsigned mj = 0u;
-        float4 Aj = make_float4(0.f, 0.f, 0.f, 0.f);
+        float s2j = 1.0f;
         if (jj < wmax) {   // wmax ≤ the sub-list length
-            Aj = entry_geom(cur.pr);
-            sA[wl_][lane] = Aj;
+            const float s = fabsf(cur.pr.w);
+            s2j = __fmul_rn(s, s);
+            sA[wl_][lane] = make_float4(cur.pr.x, cur.pr.y, s2j, exp_scale(s2j));
             sB[wl_][lane] = cur.co;
             sZ[wl_][lane] = cur.pr.z;
             if (POSE)   // camera-space centre from the projection (x = (u − cx)·z / fx, …)
                 sX[wl_][lane] = make_float4((cur.pr.x - p.in.cx) * cur.pr.z * rcp_approx(p.in.fx),
                                             (cur.pr.y - p.in.cy) * cur.pr.z * rcp_approx(p.in.fy), cur.pr.z, cur.pr.w);
-            mj = mcur & onmask;
+            mj = mcur & onmask;   // the forward's exact composited pixels with a nonzero upstream
         }
         __syncwarp();
-        // candidates at positions ≥ the pixel's `last` were not composited: drop them from the
-        // lane's column (phase 1) and, through the transposed threshold masks, from each entry's
-        // pixel set (phase 2), so no zero pair is ever written or read for them
-        const int rem = (int)L - bb;
-        const unsigned alive = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-        unsigned bits = transpose32(mj, lane) & alive;
-        mj &= transpose32(alive, lane);
-        // ---- phase 1: lane = pixel, back to front, two candidates per iteration: both
-        // candidates' loads, footprint, α, 1/(1−α) and f carry no loop state and are computed
+        unsigned bits = transpose32(mj, lane);   // lane = pixel: the entries it composited
+        // ---- phase 1: lane = pixel, back to front, two pairs per iteration: both pairs' loads,
+        // α (the forward's exact bits), 1/(1−α) and f carry no loop state and are computed
         // together; the recursion (T, Fb, Tb) then runs over the two in order ----
-        auto stage_a = [&](int k, bool v, float &a, float &rc, float &wgt, float &fi, bool &comp, bool &aclamp) {
+        auto stage_a = [&](int k, bool v, float &a, float &rc, float &wgt, float &fi, bool &aclamp) {
             float4 A, B;
             float zk;
-            if (v) {   // predicated loads: lanes without a candidate add no shared-memory traffic
+            if (v) {   // predicated loads: lanes without a pair add no shared-memory traffic
                 A = sA[wl_][k];
                 B = sB[wl_][k];
                 zk = sZ[wl_][k];
             }
-            const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
-            const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-            wgt = fast_exp2(d2 * A.w);
-            const float raw = __fmul_rn(B.w, wgt);
+            const float d2 = pair_d2(pxf, pyf, A.x, A.y);
+            const float raw = raw_alpha(d2, A.z, A.w, B.w, v, wgt);
             aclamp = raw > kAlphaMax;
             a = aclamp ? kAlphaMax : raw;
-            comp = v && d2 <= A.z && a >= 1.0f / 255.0f;
             rc = rcp_approx(1.0f - a);
             fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (zk - rz);
         };
-        auto stage_b = [&](int k, bool comp, bool aclamp, float a, float rc, float wgt, float fi) {
-            float om = 0.f, dAe = 0.f;
-            if (comp) {
-                const float oma = 1.0f - a;
-                const float Ti = T * rc;
-                om = a * Ti;
-                // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
-                dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
-                Fb = a * fi + oma * Fb;
-                Tb = oma * Tb;
-                T = Ti;
-            }
+        auto stage_b = [&](int k, bool aclamp, float a, float rc, float wgt, float fi) {
+            const float oma = 1.0f - a;
+            const float Ti = T * rc;
+            const float om = a * Ti;
+            // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
+            const float dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
+            Fb = a * fi + oma * Fb;
+            Tb = oma * Tb;
+            T = Ti;
             M[k][lane] = make_float2(om, dAe);
         };
         while (bits) {
@@ -247,14 +235,14 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             const int k1 = (31 - __clz(bits)) & 31;
             if (v1) bits &= ~(1u << k1);
             float a0, rc0, w0, f0, a1, rc1, w1, f1;
-            bool c0, cl0, c1, cl1;
-            stage_a(k0, true, a0, rc0, w0, f0, c0, cl0);
-            stage_a(k1, v1, a1, rc1, w1, f1, c1, cl1);
-            stage_b(k0, c0, cl0, a0, rc0, w0, f0);
-            if (v1) stage_b(k1, c1, cl1, a1, rc1, w1, f1);
+            bool cl0, cl1;
+            stage_a(k0, true, a0, rc0, w0, f0, cl0);
+            stage_a(k1, v1, a1, rc1, w1, f1, cl1);
+            stage_b(k0, cl0, a0, rc0, w0, f0);
+            if (v1) stage_b(k1, cl1, a1, rc1, w1, f1);
         }
         __syncwarp();
-        // ---- phase 2: lane = entry, over the pixels its footprint covers, two pixels per
+        // ---- phase 2: lane = entry, over the pixels that composited it, two pixels per
         // iteration (both pixels' M and upstream loads issued before either is accumulated) ----
         if (mj) {
             const float4 B = cur.co;
@@ -262,19 +250,17 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, sw2 = 0.f, swx = 0.f, swy = 0.f, dzd = 0.f;
             unsigned mm = __funnelshift_r(mj, mj, lane);  // rotate right by lane
             auto accum = [&](int i, float2 md, float4 gp) {
-                if (md.x != 0.f) {   // composited (ω > 0 for every composited pair)
-                    dc0 = fmaf(gp.x, md.x, dc0);
-                    dc1 = fmaf(gp.y, md.x, dc1);
-                    dc2 = fmaf(gp.z, md.x, dc2);
-                    dzd = fmaf(gp.w, md.x, dzd);
-                    const float dx = (float)(sx + (i & 7)) - Aj.x, dy = (float)(sy + (i >> 3)) - Aj.y;
-                    const float d2 = dx * dx + dy * dy;
-                    const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution; 0 when α clamped)
-                    dop += dw;
-                    sw2 = fmaf(dw, d2, sw2);
-                    swx = fmaf(dw, dx, swx);
-                    swy = fmaf(dw, dy, swy);
-                }
+                dc0 = fmaf(gp.x, md.x, dc0);
+                dc1 = fmaf(gp.y, md.x, dc1);
+                dc2 = fmaf(gp.z, md.x, dc2);
+                dzd = fmaf(gp.w, md.x, dzd);
+                const float dx = (float)(sx + (i & 7)) - cur.pr.x, dy = (float)(sy + (i >> 3)) - cur.pr.y;
+                const float d2 = dx * dx + dy * dy;
+                const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution; 0 when α clamped)
+                dop += dw;
+                sw2 = fmaf(dw, d2, sw2);
+                swx = fmaf(dw, dx, swx);
+                swy = fmaf(dw, dy, swy);
             };
             while (mm) {
                 const int i0 = ((__ffs(mm) - 1) + (int)lane) & 31;
@@ -285,17 +271,17 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
                 const float2 md0 = M[lane][i0];
                 const float4 gp0 = sG[wl_][i0];
                 float2 md1 = make_float2(0.f, 0.f);
-                float4 gp1;
+                float4 gp1 = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (v1) {
                     md1 = M[lane][i1];
                     gp1 = sG[wl_][i1];
                 }
                 accum(i0, md0, gp0);
-                accum(i1, md1, gp1);   // md1.x == 0 when there is no second pixel
+                if (v1) accum(i1, md1, gp1);
             }
             // dL/dw·w = dL/dα·o·w;  ∂w/∂σ = w d²/σ³, ∂w/∂u = w (x−u)/σ², ∂w/∂v = w (y−v)/σ²
             const float s = fabsf(cur.pr.w);
-            const float inv_s2 = __fdividef(1.0f, s * s);
+            const float inv_s2 = rcp_approx(s2j);
             const float dsg = B.w * sw2 * inv_s2 * rcp_approx(s);
             if (ATTR && (int64_t)cur.g >= p.learn_begin && (int64_t)cur.g < p.learn_end) {
                 const bool wc = p.want & VTGS_GRAD_COLOR, wo = p.want & VTGS_GRAD_OPACITY;
@@ -309,7 +295,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
                 const float4 X = sX[wl_][lane];
                 const float du = B.w * swx * inv_s2, dv = B.w * swy * inv_s2;
                 const float iz = rcp_approx(z);
-                float dzt = dzd - (du * (Aj.x - p.in.cx) + dv * (Aj.y - p.in.cy)) * iz;
+                float dzt = dzd - (du * (cur.pr.x - p.in.cx) + dv * (cur.pr.y - p.in.cy)) * iz;
                 if (X.w > 0.f) dzt -= dsg * s * iz;  // ∂σ/∂z = −σ/z (unclamped)
                 const float gx = du * p.in.fx * iz, gy = dv * p.in.fy * iz, gz = dzt;
                 if ((p.want & VTGS_GRAD_POSITION) && (gx != 0.f || gy != 0.f || gz != 0.f))   // dL/dX_w = R g
@@ -348,159 +334,15 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
 
 // ------------------------------------------------------------------------------------------
 // Pose-only backward (tracking, Eq. 1: "keep all Gaussians in the scene fixed, and merely
-// optimize the pose").  The pose gradient is linear in the per-pair terms, so
-// each composited pair's dL/dX_c contribution goes straight into the lane's 12 accumulators
-// (Σ g, Σ X_c gᵀ) from the recursion of phase 1: no per-Gaussian reduction, no M matrix, no
-// phase 2, and a third of the shared memory (occupancy).  Per entry the build stores the
-// chain's constants: fx/z, fy/z, (u − cx)/z, (v − cy)/z, o/σ², [σ unclamped]/z and X_c; per pair
+// optimize the pose"), ring walk.  The pose gradient is linear in the per-pair
+// terms, so each composited pair's dL/dX_c goes straight into the lane's 12 accumulators
+// (Σ g, Σ X_c gᵀ): no per-Gaussian reduction, so the lanes walk back to front ACROSS batch
+// boundaries at their own pace over a ring of R resident batches, like the forward's ring
+// (k_composite_fwd_ring): a lane only waits when it needs a batch not yet built and the ring is
+// R batches ahead of the slowest lane.  The lane's candidates are the forward's EXACT composited
+// pairs (no compositing test is re-done).  Per entry the slot keeps A = (u, v, s2, escale),
+// B = (c, z), Xq = (X_c.x, X_c.y, o, o/σ²) and ±1/z (−: σ clamped, ∂σ/∂z = 0); per pair
 //   q = (o/σ²)·dL/dα·w,  g = (q·dx·fx/z, q·dy·fy/z, g_D·ω − q·dx·(u−cx)/z − q·dy·(v−cy)/z − q·d²·[1/z])
-// (the same chain k_composite_bwd applies per (Gaussian, sub-tile) after summing the pairs).
-// ------------------------------------------------------------------------------------------
-template <bool LOSS>
-__global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_pose(BwdArgs p) {
-    __shared__ float4 sA[kBwdWarps][32];   // u, v, 9σ², −log2(e)/(2σ²)
-    __shared__ float4 sB[kBwdWarps][32];   // c, o
-    __shared__ float sZ[kBwdWarps][32];
-    __shared__ float4 sP1[kBwdWarps][32];  // fx/z, fy/z, (u − cx)/z, (v − cy)/z
-    __shared__ float4 sP2[kBwdWarps][32];  // X_c (x, y, z), o/σ²
-    __shared__ float sP3[kBwdWarps][32];   // 1/z if σ unclamped else 0
-    const int wl_ = threadIdx.x >> 5;
-    const int gsub = blockIdx.x * kBwdWarps + wl_;
-    const int tile = gsub >> 3;
-    const int sub = gsub & 7;
-    const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
-    const unsigned lane = lane_id();
-    const int sx = tx * kTile + (sub & 1) * 8, sy = ty * kTile + (sub >> 1) * 4;
-    const int px = sx + (lane & 7), py = sy + (lane >> 3);
-    const bool inside = px < p.W && py < p.H;
-    const float pxf = (float)px, pyf = (float)py;
-    const int n = (int)p.tile_count[tile];
-    const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
-    const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
-    const PixelUp up = pixel_upstream<LOSS>(p, px, py, inside);
-    const float g0 = up.g0, g1 = up.g1, g2 = up.g2, gD = up.gD, gS = up.gS;
-    const float r0 = up.r0, r1 = up.r1, r2 = up.r2, rz = up.rz;
-    float T = up.T;
-    const bool on = inside && up.L > 0 && (g0 != 0.f || g1 != 0.f || g2 != 0.f || gD != 0.f || gS != 0.f);
-    const uint32_t L = on ? up.L : 0u;
-    const unsigned onmask = __ballot_sync(kFullMask, on);
-    const int wmax = (int)__reduce_max_sync(kFullMask, L);
-    float Fb = 0.f, Tb = 1.0f;
-    const float Kr = g0 * r0 + g1 * r1 + g2 * r2 + gD * rz + gS;
-    float h0 = 0.f, h1 = 0.f, h2 = 0.f;
-    float K00 = 0.f, K01 = 0.f, K02 = 0.f, K10 = 0.f, K11 = 0.f, K12 = 0.f, K20 = 0.f, K21 = 0.f, K22 = 0.f;
-
-    const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
-    EntryRegs nxt;
-    fetch_entry<false>(nxt, list, bb_top + (int)lane, wmax, p.proj, p.col_opa, p.rect);
-    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
-    for (int bb = bb_top; bb >= 0; bb -= 32) {
-        const EntryRegs cur = nxt;
-        const uint32_t mcur = mnx;
-        fetch_entry<false>(nxt, list, bb - 32 + (int)lane, wmax, p.proj, p.col_opa, p.rect);
-        mnx = load_mask(mlist, bb - 32 + (int)lane, wmax);
-        unsigned mj = 0u;
-        if (bb + (int)lane < wmax) {
-            const float4 Aj = entry_geom(cur.pr);
-            sA[wl_][lane] = Aj;
-            sB[wl_][lane] = cur.co;
-            sZ[wl_][lane] = cur.pr.z;
-            const float z = cur.pr.z, s = fabsf(cur.pr.w), iz = rcp_approx(z);
-            sP1[wl_][lane] = make_float4(p.in.fx * iz, p.in.fy * iz, (Aj.x - p.in.cx) * iz, (Aj.y - p.in.cy) * iz);
-            sP2[wl_][lane] = make_float4((Aj.x - p.in.cx) * z * rcp_approx(p.in.fx), (Aj.y - p.in.cy) * z * rcp_approx(p.in.fy),
-                                         z, cur.co.w * rcp_approx(s * s));   // X_c from the projection
-            sP3[wl_][lane] = cur.pr.w > 0.f ? iz : 0.f;   // ∂σ/∂z = −σ/z only when σ is unclamped
-            mj = mcur & onmask;
-        }
-        __syncwarp();
-        const int rem = (int)L - bb;
-        const unsigned alive = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-        unsigned bits = transpose32(mj, lane) & alive;
-        // software-pipelined as k_composite_bwd's phase 1
-        struct StA {
-            float a, rc, wgt, fi, dx, dy, d2;
-            int k;
-            bool v, comp, aclamp;
-        };
-        auto stage_a = [&](StA &st) {
-            st.v = bits != 0u;
-            st.k = 31 - __clz(bits);
-            bits &= ~(1u << (st.k & 31));
-            float4 A, B;
-            float zk;
-            if (st.v) {
-                A = sA[wl_][st.k];
-                B = sB[wl_][st.k];
-                zk = sZ[wl_][st.k];
-            }
-            st.dx = __fsub_rn(pxf, A.x);
-            st.dy = __fsub_rn(pyf, A.y);
-            st.d2 = __fadd_rn(__fmul_rn(st.dx, st.dx), __fmul_rn(st.dy, st.dy));
-            st.wgt = fast_exp2(st.d2 * A.w);
-            const float raw = __fmul_rn(B.w, st.wgt);
-            st.aclamp = raw > kAlphaMax;
-            st.a = st.aclamp ? kAlphaMax : raw;
-            st.comp = st.v && st.d2 <= A.z && st.a >= 1.0f / 255.0f;
-            st.rc = rcp_approx(1.0f - st.a);
-            st.fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (zk - rz);
-        };
-        StA cs;
-        stage_a(cs);
-        while (cs.v) {
-            StA ns;
-            stage_a(ns);
-            if (cs.comp) {
-                const float oma = 1.0f - cs.a;
-                const float Ti = T * cs.rc;
-                const float om = cs.a * Ti;
-                const float dAe = cs.aclamp ? 0.f : Ti * (cs.fi - Fb + Kr * Tb) * cs.wgt;
-                Fb = cs.a * cs.fi + oma * Fb;
-                Tb = oma * Tb;
-                T = Ti;
-                const float4 c1 = sP1[wl_][cs.k], c2 = sP2[wl_][cs.k];
-                const float kz = sP3[wl_][cs.k];
-                const float q = c2.w * dAe;
-                const float du = q * cs.dx, dv = q * cs.dy;
-                const float gx = du * c1.x, gy = dv * c1.y;
-                const float gz = gD * om - du * c1.z - dv * c1.w - q * cs.d2 * kz;
-                h0 += gx; h1 += gy; h2 += gz;
-                K00 = fmaf(c2.x, gx, K00); K01 = fmaf(c2.x, gy, K01); K02 = fmaf(c2.x, gz, K02);
-                K10 = fmaf(c2.y, gx, K10); K11 = fmaf(c2.y, gy, K11); K12 = fmaf(c2.y, gz, K12);
-                K20 = fmaf(c2.z, gx, K20); K21 = fmaf(c2.z, gy, K21); K22 = fmaf(c2.z, gz, K22);
-            }
-            cs = ns;
-        }
-        __syncwarp();
-    }
-
-    __shared__ double sRed[kBwdWarps][13];   // fixed-order reduction: lanes → warp → CTA
-    double v[13] = {h0, h1, h2, K00, K01, K02, K10, K11, K12, K20, K21, K22, up.lossv};
-#pragma unroll
-    for (int q = 0; q < 13; ++q) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(kFullMask, v[q], o);
-    }
-    if (lane == 0)
-#pragma unroll
-        for (int q = 0; q < 13; ++q) sRed[wl_][q] = v[q];
-    __syncthreads();
-    if (threadIdx.x < 13) {
-        double s = 0.0;
-#pragma unroll
-        for (int i = 0; i < kBwdWarps; ++i) s += sRed[i][threadIdx.x];
-        p.partials[(size_t)blockIdx.x * 16 + threadIdx.x] = s;
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// Pose-only backward, ring walk.  k_composite_bwd_pose walks each 32-entry batch in lock step,
-// so the warp runs max-over-lanes candidates per batch (depth-sorted batches are spatially
-// coherent: a batch loads a few pixels).  With no per-Gaussian reduction there is no phase 2 to
-// synchronise on, so the lanes can walk back to front ACROSS batch boundaries at their own pace
-// over a ring of R resident batches, exactly like the forward's ring (k_composite_fwd_ring):
-// a lane only waits when it needs a batch not yet built and the ring is R batches ahead of the
-// slowest lane.  Per entry the slot keeps A = (u, v, 9σ², o), B = (c, z), Xq = (X_c, o/σ²) and
-// ±1/z (−: σ clamped, ∂σ/∂z = 0).  α is computed exactly as the forward ring computes it.
 // ------------------------------------------------------------------------------------------
 template <int R>
 struct PoseRing {
@@ -508,12 +350,11 @@ struct PoseRing {
     float4 B[R * 32];
     float4 Xq[R * 32];
     float iz[R * 32];
-    uint32_t bits[R * 32];   // per lane: its candidates of the batch (bit k = entry k)
+    uint32_t bits[R * 32];   // per lane: its composited entries of the batch (bit k = entry k)
 };
 
 constexpr int kPoseRingWarps = 2;
 constexpr int kPoseInner = 8;   // lane-independent steps between warp checks (4 → 8: tracking backward 14.5 → 14.0 ms per frame)
-constexpr float kExpScale9P = -4.5f * kLog2e;   // −log2(e)/(2σ²) = kExpScale9P / (9σ²), as the forward
 
 template <int R, bool LOSS>
 __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring(BwdArgs p) {
@@ -551,7 +392,7 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
     const float fx = p.in.fx, fy = p.in.fy, cxp = p.in.cx, cyp = p.in.cy;
 
     EntryStream st;
-    stream_start<false>(st, list, bb_top + (int)lane, bb_top - 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    stream_start<false>(st, list, bb_top + (int)lane, bb_top - 32 + (int)lane, cnt, p.proj, p.col_opa, nullptr);
     uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
     const float ifx = 1.0f / fx, ify = 1.0f / fy;
     int built = 0;
@@ -563,23 +404,19 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
             const EntryRegs &e = st.e;
             const float s = fabsf(e.pr.w);
             const float s2 = __fmul_rn(s, s);
-            const float4 A = make_float4(e.pr.x, e.pr.y, __fmul_rn(9.0f, s2), e.co.w);
-            ring.A[slot + lane] = A;
+            ring.A[slot + lane] = make_float4(e.pr.x, e.pr.y, s2, exp_scale(s2));
             ring.B[slot + lane] = make_float4(e.co.x, e.co.y, e.co.z, e.pr.z);
             // X_c from the projection itself (x = (u − cx)·z / fx, …): no gather of the world centre
             const float iz = rcp_approx(e.pr.z);
-            ring.Xq[slot + lane] = make_float4((e.pr.x - cxp) * e.pr.z * ifx, (e.pr.y - cyp) * e.pr.z * ify, e.pr.z,
+            ring.Xq[slot + lane] = make_float4((e.pr.x - cxp) * e.pr.z * ifx, (e.pr.y - cyp) * e.pr.z * ify, e.co.w,
                                                e.co.w * rcp_approx(s2));
             ring.iz[slot + lane] = e.pr.w > 0.f ? iz : -iz;
-            mj = mnx & onmask;
+            mj = mnx & onmask;   // the forward's exact composited pixels with a nonzero upstream
         }
-        // positions ≥ the pixel's `last` were not composited
-        const int rem = L - bb;
-        const unsigned alive = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-        ring.bits[slot + lane] = transpose32(mj, lane) & alive;
+        ring.bits[slot + lane] = transpose32(mj, lane);
         ++built;
         const int nidx = bb - 32 + (int)lane;
-        stream_next<false>(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        stream_next<false>(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, nullptr);
         mnx = load_mask(mlist, nidx, wmax);
     };
     while (built < nb && built < R) build();
@@ -605,16 +442,15 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
                 A = ring.A[soff + k];
                 B = ring.B[soff + k];
             }
-            const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
-            const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-            const float wgt = fast_exp2(d2 * (kExpScale9P * rcp_approx(A.z)));
-            const float raw = __fmul_rn(A.w, wgt);
-            const bool aclamp = raw > kAlphaMax;
-            const float a = aclamp ? kAlphaMax : raw;
-            const bool comp = has && d2 <= A.z && a >= 1.0f / 255.0f;
-            if (comp) {
+            if (has) {   // every candidate is a composited pair
                 const float4 Xq = ring.Xq[soff + k];
                 const float izs = ring.iz[soff + k];
+                const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
+                const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+                float wgt;
+                const float raw = raw_alpha(d2, A.z, A.w, Xq.z, true, wgt);
+                const bool aclamp = raw > kAlphaMax;
+                const float a = aclamp ? kAlphaMax : raw;
                 const float oma = 1.0f - a;
                 const float Ti = T * rcp_approx(oma);
                 const float om = a * Ti;
@@ -628,10 +464,11 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
                 const float du = q * dx, dv = q * dy;
                 const float gx = du * fx * iz, gy = dv * fy * iz;
                 const float gz = gD * om - (du * (A.x - cxp) + dv * (A.y - cyp)) * iz - q * d2 * kz;
+                const float X0 = Xq.x, X1 = Xq.y, X2 = B.w;
                 h0 += gx; h1 += gy; h2 += gz;
-                K00 = fmaf(Xq.x, gx, K00); K01 = fmaf(Xq.x, gy, K01); K02 = fmaf(Xq.x, gz, K02);
-                K10 = fmaf(Xq.y, gx, K10); K11 = fmaf(Xq.y, gy, K11); K12 = fmaf(Xq.y, gz, K12);
-                K20 = fmaf(Xq.z, gx, K20); K21 = fmaf(Xq.z, gy, K21); K22 = fmaf(Xq.z, gz, K22);
+                K00 = fmaf(X0, gx, K00); K01 = fmaf(X0, gy, K01); K02 = fmaf(X0, gz, K02);
+                K10 = fmaf(X1, gx, K10); K11 = fmaf(X1, gy, K11); K12 = fmaf(X1, gz, K12);
+                K20 = fmaf(X2, gx, K20); K21 = fmaf(X2, gy, K21); K22 = fmaf(X2, gz, K22);
             }
         }
         while (cur == 0u && b + 1 < built) advance();
@@ -845,7 +682,7 @@ static int pose_direct() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("VTGS_BWD_POSE");
-        v = e ? atoi(e) : 2;   // 2: pose-only ring kernel, 1: pose-only lock-step kernel, 0: the general two-phase kernel
+        v = e ? atoi(e) : 1;   // 1: pose-only ring kernel, 0: the general two-phase kernel
     }
     return v;
 }
@@ -881,7 +718,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile, T = ntx * nty;
     cudaError_t err;
     BwdArgs a{};
-    a.proj = c.proj; a.rect = c.rect; a.col_opa = c.col_opa; a.pos_rad = c.pos_rad;
+    a.proj = c.proj; a.col_opa = c.col_opa; a.pos_rad = c.pos_rad;
     a.tile_count = c.tile_count; a.tile_start = c.tile_start; a.sub_lists = c.sub_lists; a.sub_count = c.sub_count;
     a.sub_masks = c.sub_masks;
     a.W = W; a.H = H; a.ntx = ntx;
@@ -911,17 +748,11 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     const int sel = (A ? 4 : 0) | ((P || X) ? 2 : 0) | (L ? 1 : 0);
     if (P && !A && !X && pose_direct()) {   // tracking: pose-only backward without the per-Gaussian reduction
         LaunchScope ls(&c, kCompBwd, s);
-        if (pose_direct() == 2) {
-            constexpr int R = 4;
-            const size_t sm = sizeof(PoseRing<R>) * kPoseRingWarps;
-            static_assert(kPoseRingWarps == kBwdWarps, "k_pose_finalize rows: one partial per CTA of kBwdWarps warps");
-            if (L) k_composite_bwd_pose_ring<R, true><<<T * (8 / kPoseRingWarps), kPoseRingWarps * 32, sm, s>>>(a);
-            else k_composite_bwd_pose_ring<R, false><<<T * (8 / kPoseRingWarps), kPoseRingWarps * 32, sm, s>>>(a);
-        } else if (L) {
-            k_composite_bwd_pose<true><<<T * (8 / kBwdWarps), kBwdWarps * 32, 0, s>>>(a);
-        } else {
-            k_composite_bwd_pose<false><<<T * (8 / kBwdWarps), kBwdWarps * 32, 0, s>>>(a);
-        }
+        constexpr int R = 4;
+        const size_t sm = sizeof(PoseRing<R>) * kPoseRingWarps;
+        static_assert(kPoseRingWarps == kBwdWarps, "k_pose_finalize rows: one partial per CTA of kBwdWarps warps");
+        if (L) k_composite_bwd_pose_ring<R, true><<<T * (8 / kPoseRingWarps), kPoseRingWarps * 32, sm, s>>>(a);
+        else k_composite_bwd_pose_ring<R, false><<<T * (8 / kPoseRingWarps), kPoseRingWarps * 32, sm, s>>>(a);
     } else {
     {
     LaunchScope ls(&c, kCompBwd, s);

@@ -79,11 +79,43 @@ __device__ __forceinline__ uint32_t load_mask(const uint32_t *__restrict__ mlist
     return (idx >= 0 && idx < n) ? __ldg(mlist + idx) : 0u;
 }
 
-// (u, v, 9σ² exact fp32 — the truncation threshold, −log2(e)/(2σ²))
-__device__ __forceinline__ float4 entry_geom(const float4 pr) {
-    const float s = fabsf(pr.w);
-    const float s2 = __fmul_rn(s, s);
-    return make_float4(pr.x, pr.y, __fmul_rn(9.0f, s2), __fdividef(-0.5f * kLog2e, s2));
+// ---- α of a (pixel, Gaussian) pair: ONE definition for every compositing kernel -----------
+// DESIGN.md §3 step 7: w = exp((−0.5·d²)/σ²), α = min(o·w, 0.999), skipped iff α < 1/255.
+// Per entry the kernels keep s2 = fl(σ·σ) and the IEEE exponent scale escale = fl(−½log2(e)/s2)
+// (exp_scale, computed once per entry, identical bits in every kernel).  Fast path:
+// w = ex2.approx(fl(d²·escale)), relative error ≤ ~7e-7 against the correctly rounded fp32 exp
+// of the fp32 argument fl(fl(−0.5·d²)/s2) — the oracle's w.  When the raw α = fl(o·w) lies within
+// kNearRel (1.5e-5, ≥ 20× that error) of 1/255 or 0.999 the decision could depend on it, so w is
+// recomputed as that correctly rounded exp (fp64 exp, rounded once): every α decision is then
+// taken on the oracle's bits.  The forward and the backward call the same function on the same
+// stored entry data, so they see the same α bits (no fwd/bwd decision mismatch).
+constexpr float kAlphaMin = 1.0f / 255.0f;
+constexpr float kNearRel = 1.0f / 65536.0f;
+constexpr float kNegHalfLog2e = -0.5f * kLog2e;
+
+__device__ __forceinline__ float exp_scale(float s2) { return __fdiv_rn(kNegHalfLog2e, s2); }
+
+__device__ __forceinline__ float exact_w(float d2, float s2) {
+    return __double2float_rn(exp((double)__fdiv_rn(__fmul_rn(-0.5f, d2), s2)));
+}
+
+// raw α = fl(o·w) before the 0.999 clamp (α = min(raw, 0.999); clamped ⇔ raw > 0.999); w is
+// returned for the backward's chain.  `elig` = the pair passed the 3σ test (only those decide).
+__device__ __forceinline__ float raw_alpha(float d2, float s2, float escale, float o, bool elig, float &w) {
+    w = fast_exp2(__fmul_rn(d2, escale));
+    float raw = __fmul_rn(o, w);
+    const bool near = fabsf(raw - kAlphaMax) <= kAlphaMax * kNearRel || fabsf(raw - kAlphaMin) <= kAlphaMin * kNearRel;
+    if (elig && near) {
+        w = exact_w(d2, s2);
+        raw = __fmul_rn(o, w);
+    }
+    return raw;
+}
+
+// d² of pixel (xf, yf) to centre (u, v), DESIGN.md §3 step 7 (no FMA contraction)
+__device__ __forceinline__ float pair_d2(float xf, float yf, float u, float v) {
+    const float dx = __fsub_rn(xf, u), dy = __fsub_rn(yf, v);
+    return __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
 }
 
 // Mask of the warp's 32 pixels (bit = (y−sy)·8 + (x−sx)) inside the entry's rect and,
@@ -100,7 +132,9 @@ __device__ __forceinline__ unsigned lane_mask(const float4 A, const uint2 r, int
         const float dy = __fsub_rn((float)y, A.y);
         const float dy2 = __fmul_rn(dy, dy);
         if (!(dy2 <= A.z)) continue;
-        const float r2 = A.z - dy2;                                  // ≥ 0
+        // the exact test accepts |dx| up to √(r2 + ½ulp(9σ²)) (dx² + dy² rounds down onto 9σ²):
+        // widen by A.z·2⁻²³ ≥ ½ulp before the root, then by 0.01 px for the approximate rsqrt
+        const float r2 = A.z - dy2 + A.z * 1.1920929e-7f;           // ≥ 0
         const float hw = r2 * rsqrt_approx(fmaxf(r2, 1e-30f)) + 0.01f; // √r2 (+ ≤ 2⁻²² rel.) + margin
         const int xa = max(x0, (int)ceilf(A.x - hw)), xb = min(x1, (int)floorf(A.x + hw));
         if (xa > xb) continue;

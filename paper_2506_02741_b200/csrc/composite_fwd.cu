@@ -10,13 +10,12 @@ namespace vtgs {
 
 struct FwdArgs {
     const float4 *proj;
-    const uint2 *rect;
     const float4 *col_opa;
     const uint32_t *tile_count;
     const uint32_t *tile_start;
     const uint32_t *sub_lists;
     const uint32_t *sub_count;
-    uint32_t *sub_masks;   // per sub-list entry: its 32-pixel lane_mask (read by the backward)
+    uint32_t *sub_masks;   // per sub-list entry: the EXACT set of its sub-tile's pixels that composited it
     int W, H, ntx;
     float *color, *depth, *sil, *T_final;
     uint32_t *last;
@@ -24,102 +23,6 @@ struct FwdArgs {
 };
 
 constexpr int kFwdWarps = 2;  // warps (8×4 sub-tiles) per CTA: small CTAs retire independently
-
-__global__ void __launch_bounds__(kFwdWarps * 32, 16) k_composite_fwd(FwdArgs p) {
-    __shared__ float4 sA[kFwdWarps][32];  // u, v, 9σ², −log2(e)/(2σ²) of the warp's current batch
-    __shared__ float4 sB[kFwdWarps][32];  // colour, opacity
-    __shared__ float sZ[kFwdWarps][32];
-
-    const int wl = threadIdx.x >> 5;
-    const int gsub = blockIdx.x * kFwdWarps + wl;
-    const int tile = gsub >> 3;
-    const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
-    const int w = gsub & 7;
-    const unsigned lane = lane_id();
-    const int sx = tx * kTile + (w & 1) * 8, sy = ty * kTile + (w >> 1) * 4;
-    const int px = sx + (lane & 7), py = sy + (lane >> 3);
-    const bool inside = px < p.W && py < p.H;
-    const float pxf = (float)px, pyf = (float)py;
-    const int n = (int)p.tile_count[tile];
-    const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)w * n;
-    uint32_t *mout = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)w * n;
-    const int cnt = (int)p.sub_count[tile * 8 + w];
-
-    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f, Sl = 0.f;
-    uint32_t lastc = 0, ne = 0, nc = 0;
-    bool done = !inside;
-    unsigned active = __ballot_sync(kFullMask, !done);
-
-    EntryRegs nxt;
-    fetch_entry(nxt, list, (int)lane, cnt, p.proj, p.col_opa, p.rect);
-    for (int bb = 0; bb < cnt && active; bb += 32) {
-        const EntryRegs cur = nxt;
-        fetch_entry(nxt, list, bb + 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);  // next batch
-        unsigned mj = 0u;
-        if (bb + (int)lane < cnt) {
-            const float4 A = entry_geom(cur.pr);
-            sA[wl][lane] = A;
-            sB[wl][lane] = cur.co;
-            sZ[wl][lane] = cur.pr.z;
-            const unsigned m0 = lane_mask(A, cur.r, sx, sy);
-            mout[bb + lane] = m0;
-            mj = m0 & active;
-        }
-        __syncwarp();
-        unsigned bits = transpose32(mj, lane);
-        while (bits) {
-            const int k = __ffs(bits) - 1;
-            bits &= bits - 1u;
-            const float4 A = sA[wl][k];
-            const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
-            const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-            if (d2 <= A.z) {
-                ++ne;
-                const float4 B = sB[wl][k];
-                const float a = fminf(__fmul_rn(B.w, fast_exp2(d2 * A.w)), kAlphaMax);
-                if (a >= 1.0f / 255.0f) {
-                    const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
-                    if (Tn < kTMin) {
-                        done = true;
-                        bits = 0u;
-                    } else {
-                        const float om = a * T;
-                        C0 = fmaf(B.x, om, C0);
-                        C1 = fmaf(B.y, om, C1);
-                        C2 = fmaf(B.z, om, C2);
-                        D = fmaf(sZ[wl][k], om, D);
-                        Sl += om;
-                        T = Tn;
-                        lastc = (uint32_t)(bb + k + 1);
-                        ++nc;
-                    }
-                }
-            }
-        }
-        active = __ballot_sync(kFullMask, !done);
-        __syncwarp();
-    }
-    if (inside) {
-        const int pix = py * p.W + px;
-        p.color[3 * pix + 0] = C0;
-        p.color[3 * pix + 1] = C1;
-        p.color[3 * pix + 2] = C2;
-        p.depth[pix] = D;
-        p.sil[pix] = Sl;
-        p.T_final[pix] = T;
-        p.last[pix] = lastc;
-    }
-    unsigned long long a = ne, b = nc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(kFullMask, a, o);
-        b += __shfl_xor_sync(kFullMask, b, o);
-    }
-    if (lane == 0 && (a | b)) {
-        atomicAdd(&p.dev->e_eval, a);
-        atomicAdd(&p.dev->e_comp, b);
-    }
-}
 
 // Ring walk.  The warp builds 32-entry batches of its sub-list into a ring of R slots (entry
 // data A = (u, v, 9σ², o), B = (c_r, c_g, c_b, z), and per lane the bit column of the entries
@@ -129,13 +32,14 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 16) k_composite_fwd(FwdArgs p)
 // step (the warp runs max-over-lanes candidates per batch), the warp runs ≈ max-over-lanes of
 // the whole-list candidate count — tools/sim_batches.py: lane efficiency 0.27 → 0.87 at R = 16.
 constexpr int kInner = 6;                      // lane-independent steps between warp checks
-constexpr float kExpScale9 = -4.5f * kLog2e;  // −log2(e)/(2σ²) = kExpScale9 / (9σ²)
 
 template <int R>
 struct FwdRing {
-    float4 A[R * 32];
-    float4 B[R * 32];
-    uint32_t bits[R * 32];
+    float4 A[R * 32];        // u, v, s2 = σ², escale = −½log2(e)/s2
+    float4 B[R * 32];        // c_r, c_g, c_b, o
+    float Z[R * 32];         // z
+    uint32_t bits[R * 32];   // per lane: its candidate entries of the batch (bit 31 − j = entry j)
+    uint32_t cbits[R * 32];  // per lane: the entries it composited (same orientation)
 };
 
 template <int R, bool STATS>
@@ -161,27 +65,39 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     const unsigned inmask = __ballot_sync(kFullMask, inside);
 
     EntryStream st;
-    stream_start<false>(st, list, (int)lane, 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+    stream_start<false>(st, list, (int)lane, 32 + (int)lane, cnt, p.proj, p.col_opa, nullptr);
     const EntryRegs &nxt = st.e;
     int built = 0;
+    // Exact composited masks (forward → backward): each lane ORs the entries it composites into
+    // its column word of the batch (ring.cbits, stored when it leaves the batch).  When a slot
+    // is rebuilt every lane has left its old batch; the 32 column words are bit-transposed so
+    // lane j holds entry j's pixel set, which is stored next to the sub-list.  The backward
+    // walks exactly these pairs and never re-decides a compositing test.
+    auto emit = [&](int t) {
+        const int slot = (t & (R - 1)) * 32;
+        const unsigned m = transpose32(__brev(ring.cbits[slot + lane]), lane);
+        if (t * 32 + (int)lane < cnt) mout[t * 32 + lane] = m;
+    };
     // build batch `built` from the prefetched registers, prefetch the one after it
     auto build = [&]() {
         const int slot = (built & (R - 1)) * 32;
+        if (built >= R) emit(built - R);
         const int idx = built * 32 + (int)lane;
         unsigned mj = 0u;
         if (idx < cnt) {
             const float s = fabsf(nxt.pr.w);
-            const float s9 = __fmul_rn(9.0f, __fmul_rn(s, s));
-            const float4 A = make_float4(nxt.pr.x, nxt.pr.y, s9, nxt.co.w);
-            ring.A[slot + lane] = A;
-            ring.B[slot + lane] = make_float4(nxt.co.x, nxt.co.y, nxt.co.z, nxt.pr.z);
-            const unsigned m0 = lane_mask(A, rect_from_proj(nxt.pr, p.W, p.H), sx, sy);
-            mout[idx] = m0;
+            const float s2 = __fmul_rn(s, s);
+            ring.A[slot + lane] = make_float4(nxt.pr.x, nxt.pr.y, s2, exp_scale(s2));
+            ring.B[slot + lane] = nxt.co;
+            ring.Z[slot + lane] = nxt.pr.z;
+            const unsigned m0 =
+                lane_mask(make_float4(nxt.pr.x, nxt.pr.y, __fmul_rn(9.0f, s2), 0.f), rect_from_proj(nxt.pr, p.W, p.H), sx, sy);
             mj = m0 & inmask;
         }
         ring.bits[slot + lane] = __brev(transpose32(mj, lane));  // bit 31 − j = entry j
+        ring.cbits[slot + lane] = 0u;
         ++built;
-        stream_next<false>(st, list, (built + 1) * 32 + (int)lane, cnt, p.proj, p.col_opa, p.rect);
+        stream_next<false>(st, list, (built + 1) * 32 + (int)lane, cnt, p.proj, p.col_opa, nullptr);
     };
     while (built < nb && built < R) build();
     __syncwarp();
@@ -189,17 +105,22 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f, Sl = 0.f;
     uint32_t lastc = 0, ne = 0, nc = 0;
     // lane state: batch b, its remaining candidate bits cur (bit 31 − j = entry j, so the lowest
-    // remaining entry is the highest set bit, one FLO), the address of the batch's entry 31 and
-    // 1 + the sub-list position of its entry 31.  Finished (terminated, walked the whole list,
-    // or outside the image) ⇔ cur == 0 && b + 1 ≥ nb.
+    // remaining entry is the highest set bit, one FLO), the address of the batch's entry 31,
+    // 1 + the sub-list position of its entry 31, and cw = the entries of batch b it composited.
+    // Finished (terminated, walked the whole list, or outside the image) ⇔ cur == 0 && b + 1 ≥ nb.
     int b = inside ? -1 : nb;
-    unsigned cur = 0u;
-    const float4 *abase = ring.A;
+    unsigned cur = 0u, cw = 0u;
+    int soff = 0;
     int lbase = 0;
+    auto flush = [&]() {   // store the lane's composited bits of batch b (before leaving it)
+        if (cw) ring.cbits[soff + lane] = cw;
+        cw = 0u;
+    };
     auto advance = [&]() {
+        flush();
         ++b;
-        cur = ring.bits[(b & (R - 1)) * 32 + lane];
-        abase = ring.A + (b & (R - 1)) * 32 + 31;
+        soff = (b & (R - 1)) * 32;
+        cur = ring.bits[soff + lane];
         lbase = b * 32 + 32;
     };
     for (;;) {
@@ -210,36 +131,41 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
             if (cur == 0u && b + 1 < built) advance();
             const bool has = cur != 0u;
             const int hb = 31 - __clz(cur);                // highest set bit = lowest remaining entry
-            cur &= ~(1u << (hb & 31));
-            const float4 *ap = abase - hb;                 // entry 31 − hb
+            const unsigned bit = 1u << (hb & 31);
+            cur &= ~bit;
+            const int k = soff + 31 - hb;                  // ring index of entry 31 − hb
             float4 A, Bc;                                  // unused unless `has` (elig includes it)
             if (has) {   // predicated loads: idle lanes add no shared-memory traffic
-                A = ap[0];
-                Bc = ap[R * 32];
+                A = ring.A[k];
+                Bc = ring.B[k];
             }
-            const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
-            const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-            const bool elig = has && d2 <= A.z;
-            const float a = fminf(__fmul_rn(A.w, fast_exp2(d2 * (kExpScale9 * rcp_approx(A.z)))), kAlphaMax);
-            const bool comp = elig && a >= 1.0f / 255.0f;
+            const float d2 = pair_d2(pxf, pyf, A.x, A.y);
+            const bool elig = has && d2 <= __fmul_rn(9.0f, A.z);
+            float w;
+            const float raw = raw_alpha(d2, A.z, A.w, Bc.w, elig, w);
+            const float a = fminf(raw, kAlphaMax);
+            const bool comp = elig && a >= kAlphaMin;
             const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
             const bool term = comp && Tn < kTMin;
             const bool acc = comp && !term;
             const float om = a * T;
             if (acc) {   // predicated: Bc is garbage for lanes without a candidate
+                const float zk = ring.Z[k];
                 C0 = fmaf(Bc.x, om, C0);
                 C1 = fmaf(Bc.y, om, C1);
                 C2 = fmaf(Bc.z, om, C2);
-                D = fmaf(Bc.w, om, D);
+                D = fmaf(zk, om, D);
                 Sl += om;
                 T = Tn;
                 lastc = (uint32_t)(lbase - hb);
+                cw |= bit;
             }
             if (STATS) {
                 ne += elig ? 1u : 0u;
                 nc += acc ? 1u : 0u;
             }
             if (term) {
+                flush();
                 cur = 0u;
                 b = nb;
             }
@@ -253,11 +179,14 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
             const int need = !live ? 0x7fffffff : (cur ? b : b + 1);  // earliest batch still needed
             const int lo = __reduce_min_sync(kFullMask, need);
             if (built < nb && built < lo + R) {
+                if (cur == 0u && b >= 0 && b < nb) flush();   // batch b is done for this lane: it may be emitted now
                 while (built < nb && built < lo + R) build();
                 __syncwarp();
             }
         }
     }
+    if (b >= 0 && b < nb) flush();
+    for (int t = built > R ? built - R : 0; t < built; ++t) emit(t);
     if (inside) {
         const int pix = py * p.W + px;
         p.color[3 * pix + 0] = C0;
@@ -286,7 +215,7 @@ static int fwd_variant() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("VTGS_FWD");
-        v = e ? atoi(e) : 4;    // 0: batch lock-step walk; 4 / 8 / 16: ring depth
+        v = e ? atoi(e) : 4;    // ring depth 4 (default) or 8
     }
     return v;
 }
@@ -309,16 +238,10 @@ static cudaError_t launch_ring(const FwdArgs &a, int T, bool stats, cudaStream_t
 cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
     const int W = c.intr.width, H = c.intr.height;
     const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile;
-    FwdArgs a{c.proj, c.rect, c.col_opa, c.tile_count, c.tile_start, c.sub_lists, c.sub_count, c.sub_masks, W, H, ntx,
+    FwdArgs a{c.proj, c.col_opa, c.tile_count, c.tile_start, c.sub_lists, c.sub_count, c.sub_masks, W, H, ntx,
               c.color, c.depth, c.sil, c.T_final, c.last, c.dev};
-    switch (fwd_variant()) {
-        case 0:
-            k_composite_fwd<<<ntx * nty * 8 / kFwdWarps, kFwdWarps * 32, 0, s>>>(a);
-            return cudaGetLastError();
-        case 8: return launch_ring<8>(a, ntx * nty, c.count_work, s);
-        case 16: return launch_ring<16>(a, ntx * nty, c.count_work, s);
-        default: return launch_ring<4>(a, ntx * nty, c.count_work, s);
-    }
+    if (fwd_variant() == 8) return launch_ring<8>(a, ntx * nty, c.count_work, s);
+    return launch_ring<4>(a, ntx * nty, c.count_work, s);
 }
 
 }  // namespace vtgs

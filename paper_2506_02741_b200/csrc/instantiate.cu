@@ -147,6 +147,39 @@ cudaError_t launch_densify(Ctx &c, const float *depth, const float *rgb, const v
 // (R25).
 constexpr int kMaxVisRefs = 8;
 
+// Back-projection of pixel (x, y) at depth d from the frame's pose (DESIGN.md §3 step 2 order).
+__device__ __forceinline__ void vis_world_point(int x, int y, float d, const PoseR &P, const vtgs_intrinsics &in,
+                                                float Xw[3]) {
+    const float X0 = __fdiv_rn(__fmul_rn(__fsub_rn((float)x, in.cx), d), in.fx);
+    const float X1 = __fdiv_rn(__fmul_rn(__fsub_rn((float)y, in.cy), d), in.fy);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        Xw[a] = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(P.R[3 * a], X0), __fmul_rn(P.R[3 * a + 1], X1)),
+                                    __fmul_rn(P.R[3 * a + 2], d)),
+                          P.t[a]);
+}
+
+// The 1 % depth-band test of one world point against one reference view (R25).
+__device__ __forceinline__ bool vis_test(const float Xw[3], const PoseR &Pr, const float *__restrict__ D, int W,
+                                         int H, const vtgs_intrinsics &in, float tol) {
+    float X[3];
+    view_transform(Pr.R, Pr.t, make_float4(Xw[0], Xw[1], Xw[2], 0.f), X);
+    const float z = X[2];
+    if (!(z > kNearClip)) return false;
+    const float u = __fadd_rn(__fdiv_rn(__fmul_rn(in.fx, X[0]), z), in.cx);
+    const float v = __fadd_rn(__fdiv_rn(__fmul_rn(in.fy, X[1]), z), in.cy);
+    if (!(u >= 0.0f && u <= (float)(W - 1) && v >= 0.0f && v <= (float)(H - 1))) return false;
+    const int x0 = (int)floorf(u), y0 = (int)floorf(v);
+    const int x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
+    const float fa = __fsub_rn(u, (float)x0), fb = __fsub_rn(v, (float)y0);
+    const float d00 = D[y0 * W + x0], d10 = D[y0 * W + x1], d01 = D[y1 * W + x0], d11 = D[y1 * W + x1];
+    if (!(d00 > 0.0f && d10 > 0.0f && d01 > 0.0f && d11 > 0.0f)) return false;
+    const float ia = __fsub_rn(1.0f, fa), ib = __fsub_rn(1.0f, fb);
+    const float di = __fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(d00, ia), __fmul_rn(d10, fa)), ib),
+                               __fmul_rn(__fadd_rn(__fmul_rn(d01, ia), __fmul_rn(d11, fa)), fb));
+    return fabsf(__fsub_rn(z, di)) <= __fmul_rn(tol, di);
+}
+
 __global__ void __launch_bounds__(256) k_visibility(const float *__restrict__ depth, const vtgs_pose *__restrict__ pose,
                                                     const float *__restrict__ ref_depth,
                                                     const vtgs_pose *__restrict__ ref_poses, int R, int W, int H,
@@ -157,46 +190,76 @@ __global__ void __launch_bounds__(256) k_visibility(const float *__restrict__ de
     if (threadIdx.x < R) pose_rotation(ref_poses[threadIdx.x], Pr[threadIdx.x]);
     __syncthreads();
     const int HW = W * H;
-    const float Wm1 = (float)(W - 1), Hm1 = (float)(H - 1);
     unsigned cnt = 0;
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < HW; p += gridDim.x * blockDim.x) {
         uint8_t vis = 0;
         const float d = depth[p];
         if (d > 0.0f && isfinite(d)) {
             const int y = p / W, x = p - y * W;
-            const float X0 = __fdiv_rn(__fmul_rn(__fsub_rn((float)x, in.cx), d), in.fx);
-            const float X1 = __fdiv_rn(__fmul_rn(__fsub_rn((float)y, in.cy), d), in.fy);
             float Xw[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-                Xw[a] = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(P.R[3 * a], X0), __fmul_rn(P.R[3 * a + 1], X1)),
-                                            __fmul_rn(P.R[3 * a + 2], d)),
-                                  P.t[a]);
-            for (int r = 0; r < R && !vis; ++r) {
-                float X[3];
-                view_transform(Pr[r].R, Pr[r].t, make_float4(Xw[0], Xw[1], Xw[2], 0.f), X);
-                const float z = X[2];
-                if (!(z > kNearClip)) continue;
-                const float u = __fadd_rn(__fdiv_rn(__fmul_rn(in.fx, X[0]), z), in.cx);
-                const float v = __fadd_rn(__fdiv_rn(__fmul_rn(in.fy, X[1]), z), in.cy);
-                if (!(u >= 0.0f && u <= Wm1 && v >= 0.0f && v <= Hm1)) continue;
-                const int x0 = (int)floorf(u), y0 = (int)floorf(v);
-                const int x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
-                const float fa = __fsub_rn(u, (float)x0), fb = __fsub_rn(v, (float)y0);
-                const float *D = ref_depth + (size_t)r * HW;
-                const float d00 = D[y0 * W + x0], d10 = D[y0 * W + x1], d01 = D[y1 * W + x0], d11 = D[y1 * W + x1];
-                if (!(d00 > 0.0f && d10 > 0.0f && d01 > 0.0f && d11 > 0.0f)) continue;
-                const float ia = __fsub_rn(1.0f, fa), ib = __fsub_rn(1.0f, fb);
-                const float di = __fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(d00, ia), __fmul_rn(d10, fa)), ib),
-                                           __fmul_rn(__fadd_rn(__fmul_rn(d01, ia), __fmul_rn(d11, fa)), fb));
-                if (fabsf(__fsub_rn(z, di)) <= __fmul_rn(tol, di)) vis = 1;
-            }
+            vis_world_point(x, y, d, P, in, Xw);
+            for (int r = 0; r < R && !vis; ++r)
+                if (vis_test(Xw, Pr[r], ref_depth + (size_t)r * HW, W, H, in, tol)) vis = 1;
         }
         mask[p] = vis;
         cnt += vis;
     }
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if (n_vis && (threadIdx.x & 31) == 0 && cnt) atomicAdd(n_vis, (unsigned long long)cnt);
+}
+
+// Per-candidate visible-point counts for the overlapping-section selection ("we
+// project the depth D_i from the initialized pose to each one frame in the overlap candidate view
+// list. We count the number of visible points to each candidate view"): counts[r] = number of
+// valid pixels of the frame visible to candidate r alone (no union); n_valid = valid pixels.
+// grid.y = candidate; one thread per pixel; warp sums → one atomic per warp.
+__global__ void __launch_bounds__(256) k_visibility_counts(const float *__restrict__ depth,
+                                                           const vtgs_pose *__restrict__ pose,
+                                                           const float *__restrict__ ref_depth,
+                                                           const vtgs_pose *__restrict__ ref_poses, int W, int H,
+                                                           vtgs_intrinsics in, float tol,
+                                                           unsigned long long *__restrict__ counts,
+                                                           unsigned long long *__restrict__ n_valid) {
+    __shared__ PoseR P, Pr;
+    const int r = blockIdx.y;
+    if (threadIdx.x == 0) pose_rotation(*pose, P);
+    if (threadIdx.x == 32) pose_rotation(ref_poses[r], Pr);
+    __syncthreads();
+    const int HW = W * H;
+    const float *D = ref_depth + (size_t)r * HW;
+    unsigned cnt = 0, nv = 0;
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < HW; p += gridDim.x * blockDim.x) {
+        const float d = depth[p];
+        if (d > 0.0f && isfinite(d)) {
+            ++nv;
+            const int y = p / W, x = p - y * W;
+            float Xw[3];
+            vis_world_point(x, y, d, P, in, Xw);
+            cnt += vis_test(Xw, Pr, D, W, H, in, tol) ? 1u : 0u;
+        }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    nv = __reduce_add_sync(0xffffffffu, nv);
+    if ((threadIdx.x & 31) == 0) {
+        if (cnt) atomicAdd(counts + r, (unsigned long long)cnt);
+        if (n_valid && r == 0 && nv) atomicAdd(n_valid, (unsigned long long)nv);
+    }
+}
+
+cudaError_t launch_visibility_counts(Ctx &c, const float *depth, const vtgs_pose *pose, const float *ref_depth,
+                                     const vtgs_pose *ref_poses, int R, vtgs_intrinsics intr, float tol,
+                                     int64_t *counts, int64_t *n_valid, cudaStream_t s) {
+    const int HW = intr.width * intr.height;
+    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t)R, s);
+    if (!e && n_valid) e = cudaMemsetAsync(n_valid, 0, sizeof(int64_t), s);
+    if (e) return e;
+    int gx = (HW + 255) / 256;
+    const int cap = (c.num_sms * 8 + R - 1) / R;
+    if (gx > cap) gx = cap < 1 ? 1 : cap;
+    LaunchScope ls(&c, kVisibility, s);
+    k_visibility_counts<<<dim3(gx, R), 256, 0, s>>>(depth, pose, ref_depth, ref_poses, intr.width, intr.height, intr,
+                                                     tol, (unsigned long long *)counts, (unsigned long long *)n_valid);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_visibility(Ctx &c, const float *depth, const vtgs_pose *pose, const float *ref_depth,

@@ -228,6 +228,9 @@ cudaError_t ssim_set_constants();
 cudaError_t launch_visibility(Ctx &c, const float *depth, const vtgs_pose *pose, const float *ref_depth,
                               const vtgs_pose *ref_poses, int R, vtgs_intrinsics intr, float tol, uint8_t *mask,
                               int64_t *n_vis, cudaStream_t s);
+cudaError_t launch_visibility_counts(Ctx &c, const float *depth, const vtgs_pose *pose, const float *ref_depth,
+                                     const vtgs_pose *ref_poses, int R, vtgs_intrinsics intr, float tol,
+                                     int64_t *counts, int64_t *n_valid, cudaStream_t s);
 cudaError_t launch_densify(Ctx &c, const float *depth, const float *rgb, const vtgs_pose *pose, vtgs_intrinsics intr,
                            const float *sil, float thr, const float *opacity, float opacity_default,
                            float4 *pos_rad, float4 *col_opa, int64_t *n_new, cudaStream_t s);

@@ -11,6 +11,12 @@
   concurrently on one GPU (or one per GPU); the selection is the argmin of the final losses.
 * `section_visibility(...)` — W_i's visibility term: the union of the frame's visibility to the
   section's head, middle and last frames (vtgs_visibility_mask).
+* `overlap_candidates(...)` / `select_overlap_section(...)` — the whole head-frame selection of
+  PAPER.md:180-182: candidate views every N1 frames (N1 = 5),
+  per-candidate visible-point counts on the device (vtgs_visibility_counts), the candidates whose
+  visible fraction exceeds γ (0.26 / 0.24), the most-front (earliest) 3 sections
+  holding a kept candidate, then the pre-tracking argmin.  The filter and the ordering are a few
+  scalars per candidate: host logic; every per-pixel step runs in libvtgs.so.
 """
 from __future__ import annotations
 
@@ -99,3 +105,42 @@ def pretrack_select(renderers: Sequence, sections: Sequence[dict], intr, rgb: to
         r.final_loss = f
     best = min(range(len(finals)), key=lambda i: finals[i])
     return best, finals, results
+
+
+def candidate_view_list(n_previous: int, n1: int = 5) -> List[int]:
+    """The overlap candidate view list: every N1-th previous frame (N1 = 5 at
+    PAPER.md:260; SPEC.md:382 step (1))."""
+    return list(range(0, n_previous, n1))
+
+
+def overlap_candidates(renderer, depth: torch.Tensor, init_pose: torch.Tensor, cand_depth: torch.Tensor,
+                       cand_poses: torch.Tensor, cand_section: Sequence[int], intr, gamma: float,
+                       n_sections: int = 3, tol: float = 0.01):
+    """Steps (2)-(4) of SPEC.md:382-386: visible-point counts of the head frame (depth at its
+    initialised pose) to each candidate view, the candidates with visible fraction > γ, and the
+    most-front `n_sections` distinct sections containing a kept candidate (earliest section index
+    first; "the most front 3 sections").  No candidate kept → the most recent section
+    (SPEC.md:387).  Returns (sections, counts [R] (host int64), n_valid)."""
+    counts, n_valid = renderer.visibility_counts(depth, init_pose, cand_depth, cand_poses, intr, tol)
+    counts = counts.cpu().tolist()
+    nv = int(n_valid.item())
+    kept = [i for i, c in enumerate(counts) if nv > 0 and c / nv > gamma]
+    secs = sorted({int(cand_section[i]) for i in kept})[:n_sections]
+    if not secs:
+        secs = [max(int(s) for s in cand_section)]
+    return secs, counts, nv
+
+
+def select_overlap_section(renderers: Sequence, sections: Sequence[dict], depth: torch.Tensor, rgb: torch.Tensor,
+                           init_pose: torch.Tensor, cand_depth: torch.Tensor, cand_poses: torch.Tensor,
+                           cand_section: Sequence[int], intr, gamma: float, iterations: int, lr_rot: float,
+                           lr_trans: float, w_color: float = 0.5, w_depth: float = 1.0, concurrent: bool = True):
+    """The head frame's overlapping section S^o: candidates → ≤ 3 sections →
+    pre-track each (concurrently, one renderer context + stream each) → the section with the
+    minimum final Eq. 1 loss.  `sections[k]` = dict(pos_rad, col_opa[, vis_mask]) of section k.
+    Returns (chosen section index, candidate sections, their final losses, counts, n_valid)."""
+    secs, counts, nv = overlap_candidates(renderers[0], depth, init_pose, cand_depth, cand_poses, cand_section,
+                                          intr, gamma)
+    best, finals, _ = pretrack_select(list(renderers)[:len(secs)], [sections[k] for k in secs], intr, rgb, depth,
+                                      init_pose, iterations, lr_rot, lr_trans, w_color, w_depth, concurrent)
+    return secs[best], secs, finals, counts, nv

@@ -68,6 +68,7 @@ _SIGS = {
     "vtgs_render_bwd": (_c.c_int32, [_P, _P, _P, _P, _c.POINTER(vtgs_l1_loss), _c.c_uint32, _c.c_int64, _c.c_int64,
                                      _P, _P, _P, _P, _P, _P]),
     "vtgs_visibility_mask": (_c.c_int32, [_P, _P, _P, _P, _P, _c.c_int32, vtgs_intrinsics, _c.c_float, _P, _P, _P]),
+    "vtgs_visibility_counts": (_c.c_int32, [_P, _P, _P, _P, _P, _c.c_int32, vtgs_intrinsics, _c.c_float, _P, _P, _P]),
     "vtgs_densify": (_c.c_int32, [_P, _P, _P, _P, vtgs_intrinsics, _P, _c.c_float, _P, _c.c_float, _P, _P, _P, _P]),
     "vtgs_ssim_loss": (_c.c_int32, [_P, _P, _P, _c.c_int32, _c.c_int32, _c.c_float, _P, _P, _P]),
     "vtgs_keyframe_pose_grad": (_c.c_int32, [_P, _P, _P, _P, _c.c_int32, _c.c_int64, _P, _P]),
@@ -200,6 +201,17 @@ class Renderer:
         _ok(vtgs_visibility_mask(self.ctx, _ptr(depth), _ptr(pose), _ptr(ref_depth), _ptr(ref_poses), R,
                                  intrinsics(intr), float(tol), _ptr(mask), None, _stream(stream)), self.ctx)
         return mask
+
+    def visibility_counts(self, depth: torch.Tensor, pose: torch.Tensor, ref_depth: torch.Tensor,
+                          ref_poses: torch.Tensor, intr, tol: float = 0.01, stream=None):
+        """Per-candidate visible-point counts of a frame → (int64 [R] device, int64 [1]
+        device valid-pixel count)."""
+        R = ref_poses.reshape(-1, 7).shape[0]
+        counts = torch.empty(R, dtype=torch.int64, device=self.device)
+        n_valid = torch.empty(1, dtype=torch.int64, device=self.device)
+        _ok(vtgs_visibility_counts(self.ctx, _ptr(depth), _ptr(pose), _ptr(ref_depth), _ptr(ref_poses), R,
+                                   intrinsics(intr), float(tol), _ptr(counts), _ptr(n_valid), _stream(stream)), self.ctx)
+        return counts, n_valid
 
     def densify(self, depth: torch.Tensor, rgb: torch.Tensor, pose: torch.Tensor, intr, silhouette: torch.Tensor,
                 pos_rad_out: torch.Tensor, col_opa_out: torch.Tensor, threshold: float = 0.5, opacity=None,

@@ -557,3 +557,20 @@ def cached_config(which: int, seed: int = 0) -> Config:
     if key not in _CFG_CACHE:
         _CFG_CACHE[key] = make_config(which, seed)
     return _CFG_CACHE[key]
+
+
+def pretrack_scene(seed: int = 0) -> dict:
+    """A small head-frame selection scene: a 6×5×3 m room with
+    12 boxes seen at 96×72 (f = 80) along a 30-frame trajectory (10 cm / 5° steps).  Sections of 5
+    frames: section k holds frames [5k, 5k+5); its Gaussians tie frames 5k and 5k+2.  Candidate
+    views every N1 = 5 frames (frames 0, 5, …, 25; candidate i belongs to section i).  The head
+    frame to track is trajectory frame 29 (ray-cast at ground truth), initialised at GT ∘ (1°, 2 cm)."""
+    intr = Intrinsics(80.0, 80.0, 47.5, 35.5, 96, 72)
+    scene, poses, kfs, opacity, rng_img = _config_room("pretrack", seed, intr, (6.0, 5.0, 3.0), 12, 30)
+    head = kfs[29]
+    rng_p = np.random.Generator(np.random.PCG64([seed, 7]))
+    init = perturb_pose(head.pose, 1.0, 0.02, rng_p)
+    sections = [{"frames": [5 * k, 5 * k + 2], "vis_frames": [5 * k, 5 * k + 2, 5 * k + 4]} for k in range(6)]
+    return {"intr": intr, "frames": kfs, "opacity": opacity, "sections": sections, "candidates": list(range(0, 30, 5)),
+            "cand_section": [i // 5 for i in range(0, 30, 5)], "head": head, "init": init,
+            "gamma": 0.26, "iterations": 8, "lr": 0.002}

@@ -15,7 +15,7 @@ import pytest
 
 import oracle
 from synth.scenes import Intrinsics, cached_config, micro_scene
-from vtgs_testlib import close, gpu_instantiate, oracle_instantiate, report, view32
+from vtgs_testlib import check_grads, close, combine_allow, flip_allowance, gpu_instantiate, oracle_instantiate, report, view32
 
 pytestmark = pytest.mark.gpu
 
@@ -137,6 +137,25 @@ def test_tile_lists_sort_paths(vt, case):
         assert np.diff(ostart).max() > 8192
     ref = oracle.render(pos_rad, col_opa, view32(view), intr)
     _check_images(out, ref, ref["flags"], max_flagged=2e-2)
+    # gradients through the same (chunked / radix-sorted) sub-lists: the backward walks the long
+    # tiles' lists back to front from the forward's exact composited masks
+    rg = np.random.default_rng(5)
+    gC = rg.normal(size=(H, W, 3)).astype(np.float32)
+    gD = rg.normal(size=(H, W)).astype(np.float32)
+    gS = rg.normal(size=(H, W)).astype(np.float32)
+    R._keep = (pv, out, pr, co)
+    want = vt.VTGS_GRAD_ALL
+    dco = torch.zeros((n, 4), device="cuda")
+    drad = torch.zeros(n, device="cuda")
+    dpose = torch.zeros(7, device="cuda")
+    R.render_bwd(want, d_col_opa=dco, d_radius=drad, d_pose=dpose, dL_dcolor=torch.from_numpy(gC).cuda(),
+                 dL_ddepth=torch.from_numpy(gD).cuda(), dL_dsil=torch.from_numpy(gS).cuda())
+    torch.cuda.synchronize()
+    reft = oracle.render(pos_rad, col_opa, view32(view), intr, want_tainted=True)
+    g = oracle.render_bwd(pos_rad, col_opa, view32(view), intr, gC, gD, gS, want_allow=True)
+    check_grads(vt, want, dco.cpu().numpy().astype(np.float64), drad.cpu().numpy().astype(np.float64),
+                dpose.cpu().numpy().astype(np.float64), g, reft["tainted"], allow=combine_allow(g),
+                name=f"sort path {case}", cap=2e-2)
 
 
 # ------------------------------------------------------------------------------ (a4)
@@ -201,35 +220,17 @@ def test_forward_parity_micro_ragged(vt, seed):
 
 
 # ------------------------------------------------------------------------------ (a5)
-def _oracle_grads(cfg, opr, oco, v, gC, gD, gS, extra_flags=None):
-    ref = oracle.render(opr, oco, v, cfg.intr, want_tainted=True, extra_flags=extra_flags)
-    g = oracle.render_bwd(opr, oco, v, cfg.intr, gC, gD, gS)
-    return ref, g
+def _oracle_grads(cfg, opr, oco, v, gC, gD, gS, flip=None):
+    """Oracle gradients for the upstream (gC, gD, gS); the taint comes from the forward's decision
+    near-ties only; `flip` (L1 sgn near-ties) becomes a per-Gaussian allowance."""
+    ref = oracle.render(opr, oco, v, cfg.intr, want_tainted=True)
+    g = oracle.render_bwd(opr, oco, v, cfg.intr, gC, gD, gS, want_allow=True)
+    allow = combine_allow(g, None if flip is None else flip_allowance(opr, oco, v, cfg.intr, flip))
+    return ref, g, allow
 
 
-def _check_grads(want, dco, drad, dpose, g, tainted, vt, learn=None):
-    N = len(tainted)
-    keep = ~tainted
-    if learn is not None:
-        lo, hi = learn
-        idx = np.arange(N)
-        outside = (idx < lo) | (idx >= hi)
-        assert not dco[outside].any() and not drad[outside].any()
-        keep &= ~outside
-    if want & (vt.VTGS_GRAD_COLOR | vt.VTGS_GRAD_OPACITY):
-        st = {}
-        ok = close(dco[keep], g["d_col_opa"][keep], absum=g["d_abs"][keep, :4], stats=st)
-        assert ok.all(), report("d_col_opa", ok, dco[keep], g["d_col_opa"][keep])
-        assert st["floor_only"] <= 5 + 1e-5 * st["n"], st
-    if want & vt.VTGS_GRAD_RADIUS:
-        st = {}
-        ok = close(drad[keep], g["d_radius"][keep], absum=g["d_abs"][keep, 4], stats=st)
-        assert ok.all(), report("d_radius", ok, drad[keep], g["d_radius"][keep])
-        assert st["floor_only"] <= 5 + 1e-5 * st["n"], st
-    if want & vt.VTGS_GRAD_POSE:
-        ref = g["d_pose"]
-        err = np.linalg.norm(dpose - ref)
-        assert err <= 1e-3 * np.linalg.norm(ref), f"d_pose gpu={dpose} oracle={ref}"
+def _check_grads(want, dco, drad, dpose, g, tainted, vt, learn=None, allow=None, name=""):
+    return check_grads(vt, want, dco, drad, dpose, g, tainted, allow=allow, learn=learn, name=name)
 
 
 def _run_bwd(vt, R, cfg, want, n, **kw):
@@ -258,8 +259,8 @@ def test_backward_parity_upstream(vt, which):
     dco, drad, dpose = _run_bwd(vt, R, cfg, want, cfg.n_slots, dL_dcolor=torch.from_numpy(gC).cuda(),
                                 dL_ddepth=torch.from_numpy(gD).cuda(), dL_dsil=torch.from_numpy(gS).cuda())
     opr, oco = oracle_instantiate(cfg)
-    ref, g = _oracle_grads(cfg, opr, oco, _view(cfg), gC, gD, gS)
-    _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt)
+    ref, g, allow = _oracle_grads(cfg, opr, oco, _view(cfg), gC, gD, gS)
+    _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt, allow=allow, name=f"upstream config {which}")
 
 
 @pytest.mark.parametrize("which", [1, 2, 3])
@@ -279,8 +280,8 @@ def test_backward_pose_only_upstream(vt, which):
                                 dL_ddepth=torch.from_numpy(gD).cuda(), dL_dsil=torch.from_numpy(gS).cuda())
     assert not dco.any() and not drad.any()
     opr, oco = oracle_instantiate(cfg)
-    ref, g = _oracle_grads(cfg, opr, oco, _view(cfg), gC, gD, gS)
-    _check_grads(vt.VTGS_GRAD_POSE, dco, drad, dpose, g, ref["tainted"], vt)
+    ref, g, allow = _oracle_grads(cfg, opr, oco, _view(cfg), gC, gD, gS)
+    _check_grads(vt.VTGS_GRAD_POSE, dco, drad, dpose, g, ref["tainted"], vt, allow=allow, name=f"pose-only config {which}")
 
 
 @pytest.mark.parametrize("which", [1, 2, 3])
@@ -301,12 +302,41 @@ def test_backward_parity_fused_l1(vt, which):
     opr, oco = oracle_instantiate(cfg)
     v = _view(cfg)
     img = oracle.render(opr, oco, v, cfg.intr)
-    loss, gC, gD, gS, lflags = oracle.l1_upstream(img["color"], img["depth"], img["sil"], tg.rgb, tg.depth, None,
-                                                   L["w_color"], L["w_depth"], L["color_mask_mode"],
-                                                   L["depth_mask_mode"], 0)
+    loss, gC, gD, gS, lflags, flip = oracle.l1_upstream(img["color"], img["depth"], img["sil"], tg.rgb, tg.depth,
+                                                         None, L["w_color"], L["w_depth"], L["color_mask_mode"],
+                                                         L["depth_mask_mode"], 0, want_flip=True)
     assert abs(float(loss_out.item()) - loss) <= 1e-4 * abs(loss) + 1e-6
-    ref, g = _oracle_grads(cfg, opr, oco, v, gC, gD, gS, extra_flags=lflags)
-    _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt)
+    ref, g, allow = _oracle_grads(cfg, opr, oco, v, gC, gD, gS, flip=flip)
+    _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt, allow=allow, name=f"fused L1 config {which}")
+
+
+@pytest.mark.parametrize("which", [4, 5])
+def test_backward_parity_long_lists_full_size(vt, which):
+    """Gradient parity on the workloads whose tiles exceed the on-chip sort (configs 4 and 5: tile
+    lists up to ~7k and ~58k entries, chunked / radix sort paths) at full size, through the
+    config's own mapping objective (L1 terms of Eq. 2, sum form): one view of config 4
+    (16 keyframes 640×480, 4.9M slots) and one of config 5 (40 keyframes 1200×680, 32.6M slots)."""
+    cfg = cached_config(which)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    v = view32(cfg.views[0])
+    _render_gpu(vt, R, cfg, pr, co, v)
+    st = R.stats()
+    print(f"[long lists config {which}] P = {st['n_pairs']}, longest tile list {st['max_tile']}")
+    assert st["overflow"] == 0 and st["max_tile"] > 4096, st
+    tg = cfg.targets[0]
+    wc, wd = cfg.loss_weights
+    want = vt.VTGS_GRAD_ATTR
+    dco, drad, dpose = _run_bwd(vt, R, cfg, want, cfg.n_slots, loss=dict(
+        target_rgb=torch.from_numpy(tg.rgb).cuda(), target_depth=torch.from_numpy(tg.depth).cuda(), w_color=wc,
+        w_depth=wd))
+    del pr, co
+    opr, oco = oracle_instantiate(cfg)
+    img = oracle.render(opr, oco, v, cfg.intr)
+    _, gC, gD, gS, _, flip = oracle.l1_upstream(img["color"], img["depth"], img["sil"], tg.rgb, tg.depth, None,
+                                                wc, wd, 0, 0, 0, want_flip=True)
+    ref, g, allow = _oracle_grads(cfg, opr, oco, v, gC, gD, gS, flip=flip)
+    _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt, allow=allow, name=f"long lists config {which}")
 
 
 def test_backward_learn_range_and_accumulate(vt):
@@ -322,8 +352,9 @@ def test_backward_learn_range_and_accumulate(vt):
     lo, hi = 700, 2100
     dco, drad, _ = _run_bwd(vt, R, cfg, vt.VTGS_GRAD_ATTR, cfg.n_slots, dL_dcolor=gC, learn=(lo, hi))
     opr, oco = oracle_instantiate(cfg)
-    ref, g = _oracle_grads(cfg, opr, oco, _view(cfg), gC.cpu().numpy(), None, None)
-    _check_grads(vt.VTGS_GRAD_ATTR, dco, drad, None, g, ref["tainted"], vt, learn=(lo, hi))
+    ref, g, allow = _oracle_grads(cfg, opr, oco, _view(cfg), gC.cpu().numpy(), None, None)
+    _check_grads(vt.VTGS_GRAD_ATTR, dco, drad, None, g, ref["tainted"], vt, learn=(lo, hi), allow=allow,
+                 name="learn range")
     acc = torch.zeros((cfg.n_slots, 4), device="cuda")
     accr = torch.zeros(cfg.n_slots, device="cuda")
     R.render_bwd(vt.VTGS_GRAD_ATTR, d_col_opa=acc, d_radius=accr, dL_dcolor=gC)
@@ -598,12 +629,20 @@ def _ba_scene(seed=0, W=64, H=48, K=3):
     return intr, poses, depth.astype(np.float32), rgb.astype(np.float32), opa.astype(np.float32), view
 
 
-def test_position_and_keyframe_pose_gradient_parity(vt):
+@pytest.mark.parametrize("scene", ["ba_small", "config2"])
+def test_position_and_keyframe_pose_gradient_parity(vt, scene):
     """Head-frame bundle adjustment: dL/dX_w per Gaussian (VTGS_GRAD_POSITION)
-    within the gradient bar (1e-3 rel / 1e-5 abs, or the fp32 summation floor, R23) on
-    untainted Gaussians, and the per-keyframe pose gradients (vtgs_keyframe_pose_grad) within 1e-3
-    of their norm, against the oracle's or_render_bwd d_pos + or_keyframe_pose_grad."""
-    intr, poses, depth, rgb, opa, view = _ba_scene()
+    within the gradient bar (1e-3 rel / 1e-5 abs, or the fp32 summation floor, R23, or
+    a T cut-off near-tie's allowance) on Gaussians not tainted by an α near-tie, and the
+    per-keyframe pose gradients (vtgs_keyframe_pose_grad) within 1e-3 of their norm, against the
+    oracle's or_render_bwd d_pos + or_keyframe_pose_grad — on a small 3-keyframe scene and on
+    config 2 at full size (5 keyframes, 1200×680, 4.08M slots, the view = keyframe 2's pose)."""
+    if scene == "ba_small":
+        intr, poses, depth, rgb, opa, view = _ba_scene()
+    else:
+        cfg = cached_config(2)
+        intr, poses, depth, rgb, opa = cfg.intr, cfg.pose_stack(), cfg.depth_stack(), cfg.rgb_stack(), cfg.opacity
+        view = cfg.views[0]
     K, H, W = depth.shape
     N = K * H * W
     R = vt.Renderer(0, N, W, H)
@@ -626,13 +665,22 @@ def test_position_and_keyframe_pose_gradient_parity(vt):
     del out
     opr, oco, _ = oracle.instantiate(depth, rgb, poses.astype(np.float64), intr, opa)
     ref = oracle.render(opr, oco, view32(view), intr, want_tainted=True)
-    g = oracle.render_bwd(opr, oco, view32(view), intr, gC, gD, gS)
+    g = oracle.render_bwd(opr, oco, view32(view), intr, gC, gD, gS, want_allow=True)
     keep = ~ref["tainted"]
     d = dpos.cpu().numpy()[:, :3].astype(np.float64)
     st = {}
-    ok = close(d[keep], g["d_pos"][keep], absum=g["d_pos_abs"][keep], stats=st)
-    assert ok.all(), report("d_position", ok, d[keep], g["d_pos"][keep])
+    dk, rk = d[keep], g["d_pos"][keep]
+    ok = close(dk, rk, absum=g["d_pos_abs"][keep], stats=st)
+    a_ok = np.abs(dk - rk) <= g["d_allow"][keep, 5:8] + np.maximum(1e-5, 1e-3 * np.abs(rk))
+    n_allow = int((a_ok & ~ok).any(1).sum())
+    ok |= a_ok
+    assert ok.all(), report("d_position", ok, dk, rk)
     assert st["floor_only"] <= 5 + 1e-5 * st["n"], st
+    touched = g["d_pos_abs"].sum(1) > 0
+    frac = (int((~keep & touched).sum()) + n_allow) / max(int(touched.sum()), 1)
+    print(f"[parity BA {scene}] tainted {int((~keep & touched).sum())}, allowance-only {n_allow}, "
+          f"excluded fraction {frac:.2e}")
+    assert frac <= 5e-3
     assert np.linalg.norm(dpose.cpu().numpy() - g["d_pose"]) <= 1e-3 * np.linalg.norm(g["d_pose"])
     kf_ref = oracle.keyframe_pose_grad(depth, poses.astype(np.float64), intr, g["d_pos"])
     for k in range(K):
@@ -665,11 +713,12 @@ def test_view_tied_pose_invariance_gpu(vt):
 
 
 # ------------------------------------------------------------------------------ f2 (SSIM of Eq. 2)
-@pytest.mark.parametrize("size", [(64, 48), (37, 29), (11, 11)])
+@pytest.mark.parametrize("size", [(64, 48), (37, 29), (11, 11), (200, 50), (1200, 680)])
 def test_ssim_loss_parity(vt, size):
     """τ·L_S of Eq. 2 (R24) and its gradient against the oracle's plain
     121-tap window definition: loss within 1e-5 relative; gradient within 1e-3 relative or 1e-5
-    absolute (the north_star gradient bar) elementwise, including the ragged borders."""
+    absolute (the north_star gradient bar) elementwise, including the ragged borders, the halos
+    between CTA columns / rows (200×50: 4 tile columns; 1200×680: the mapping view)."""
     W, H = size
     rng = np.random.default_rng(W * H)
     x = rng.uniform(size=(H, W, 3)).astype(np.float32)
@@ -721,11 +770,11 @@ def test_mapping_objective_with_ssim_parity(vt):
     opr, oco = oracle_instantiate(cfg)
     v = _view(cfg)
     img = oracle.render(opr, oco, v, cfg.intr)
-    _, gC, gD, gS, lflags = oracle.l1_upstream(img["color"], img["depth"], img["sil"], tg.rgb, tg.depth, None,
-                                               0.8, 1.0, 0, 0, 0)
+    _, gC, gD, gS, lflags, flip = oracle.l1_upstream(img["color"], img["depth"], img["sil"], tg.rgb, tg.depth,
+                                                     None, 0.8, 1.0, 0, 0, 0, want_flip=True)
     _, gss = oracle.ssim_loss(img["color"], tg.rgb, 0.2)
-    ref, g = _oracle_grads(cfg, opr, oco, v, gC + gss, gD, gS, extra_flags=lflags)
-    _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt)
+    ref, g, allow = _oracle_grads(cfg, opr, oco, v, gC + gss, gD, gS, flip=flip)
+    _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt, allow=allow, name="mapping objective + SSIM")
 
 
 # ------------------------------------------------------------------------------ f4 (densification)
@@ -835,3 +884,69 @@ def test_pretrack_select_concurrent_matches_sequential(vt):
     assert finals == finals2 and best == best2 == int(np.argmin(finals))
     ls = res[best].losses.cpu().numpy()
     assert ls[-1] < ls[0]                      # the selected section's pre-tracking reduces the error
+
+
+# ------------------------------------------------------------------------------ f3 (head-frame selection)
+def test_select_overlap_section_matches_oracle(vt):
+    """The whole head-frame selection of PAPER.md:180-182 / SPEC.md:382-390 against an independent
+    oracle recomputation: per-candidate visible-point counts (vtgs_visibility_counts) bit-exact
+    with the oracle's, the same γ-filtered most-front sections, per-section visibility masks
+    bit-exact, the pre-track final Eq. 1 losses of each section within 2e-3 relative of the
+    oracle's own tracking loop (its own renders, Adam steps and masks), and the same argmin
+    (SPEC.md:389 "chosen section = argmin of independently recomputed pre-track losses")."""
+    from paper_2506_02741_b200 import tracking
+    from synth.scenes import pretrack_scene
+    sc = pretrack_scene(0)
+    intr = sc["intr"]
+    H, W = intr.height, intr.width
+    dev = "cuda"
+    frames = sc["frames"]
+    head = sc["head"]
+    cand = sc["candidates"]
+    cand_depth = np.stack([frames[i].depth for i in cand])
+    cand_poses = np.stack([frames[i].pose for i in cand]).astype(np.float32)
+    init = view32(sc["init"])
+    renderers = [vt.Renderer(0, 2 * H * W, W, H) for _ in range(3)]
+    sections_gpu, sections_or = [], []
+    hd, hr = torch.from_numpy(head.depth).to(dev), torch.from_numpy(head.rgb).to(dev)
+    init_t = vt.pose_tensor(init, dev)
+    for sec in sc["sections"]:
+        fr = sec["frames"]
+        depth = np.stack([frames[i].depth for i in fr])
+        rgb = np.stack([frames[i].rgb for i in fr])
+        poses = np.stack([frames[i].pose for i in fr]).astype(np.float32)
+        opa = sc["opacity"][fr]
+        pr, co = renderers[0].instantiate(torch.from_numpy(depth).to(dev), torch.from_numpy(rgb).to(dev),
+                                          vt.pose_tensor(poses, dev), intr, torch.from_numpy(opa).to(dev))
+        vf = sec["vis_frames"]
+        vdepth = np.stack([frames[i].depth for i in vf])
+        vposes = np.stack([frames[i].pose for i in vf]).astype(np.float32)
+        vis = tracking.section_visibility(renderers[0], hd, init_t, torch.from_numpy(vdepth).to(dev),
+                                          vt.pose_tensor(vposes, dev), intr)
+        sections_gpu.append({"pos_rad": pr.clone(), "col_opa": co.clone(), "vis_mask": vis.clone()})
+        opr, oco, _ = oracle.instantiate(depth, rgb, poses.astype(np.float64), intr, opa)
+        ovis = oracle.visibility(head.depth, init, vdepth, vposes.astype(np.float64), intr)
+        assert np.array_equal(vis.cpu().numpy().astype(bool), ovis)
+        sections_or.append((opr, oco, ovis))
+    torch.cuda.synchronize()
+    chosen, secs, finals, counts, nv = tracking.select_overlap_section(
+        renderers, sections_gpu, hd, hr, init_t, torch.from_numpy(cand_depth).to(dev),
+        vt.pose_tensor(cand_poses, dev), sc["cand_section"], intr, sc["gamma"], sc["iterations"], sc["lr"], sc["lr"])
+    ocounts, onv = oracle.visibility_counts(head.depth, init, cand_depth, cand_poses.astype(np.float64), intr)
+    assert counts == ocounts and nv == onv, (counts, ocounts, nv, onv)
+    osecs = oracle.select_sections(ocounts, onv, sc["cand_section"], sc["gamma"])
+    assert secs == osecs, (secs, osecs)
+    assert len(secs) >= 2, f"the scene should offer a choice: {secs} from counts {counts} / {nv}"
+    ofinals = []
+    for k in osecs:
+        opr, oco, ovis = sections_or[k]
+        _, losses = oracle.track(opr, oco, intr, head.rgb, head.depth, init, sc["iterations"], sc["lr"], sc["lr"],
+                                 vis=ovis)
+        ofinals.append(losses[-1])
+    for a, b in zip(finals, ofinals):
+        assert abs(a - b) <= 2e-3 * abs(b), (finals, ofinals)
+    ob = int(np.argmin(ofinals))
+    srt = sorted(ofinals)
+    assert srt[1] - srt[0] > 1e-2 * srt[0], f"near-tie in the oracle's losses {ofinals}"
+    assert chosen == osecs[ob], (chosen, osecs, finals, ofinals)
+    print(f"[f3] counts {counts} / {nv}; sections {secs}; final losses gpu {finals} oracle {ofinals}; chosen {chosen}")

@@ -692,3 +692,131 @@ def test_visibility_special_cases(mode):
     assert 0 < m_a.mean() < 1 and m_b.all() and not m_c.any() and np.array_equal(m_ab, m_a | m_c)
     loose = oracle.visibility(depth, pose, (depth / 1.015)[None], pose[None], intr, tol=0.02, mode=mode)
     assert loose.mean() > 0.99          # monotone in the tolerance
+
+
+# ------------------------------------------------------------------------------ round-2 pins
+def test_rotation_known_values():
+    """The pose convention pinned by known rotations, not by round trips (camera-to-world,
+    unit quaternion (w,x,y,z); 90° z-rotations compose to 180°).  With the Hamilton
+    convention q = (cos θ/2, 0, 0, sin θ/2) rotates by θ about +z, so for θ = 90° the camera's +x
+    axis maps to world +y (a transposed R would map it to −y); q = (cos 45°, sin 45°, 0, 0)
+    maps camera +y to world +z; q = (0, 0, 0, 1) (two 90° z-turns) maps +x to −x.  Pixel
+    (cx+fx, cy) at d = 2 is X_c = (2, 0, 2), pixel (cx, cy+fy) at d = 2 is X_c = (0, 2, 2)
+    (S:66); the world point is R·X_c + t with t = (1, 2, 3)."""
+    c, s = math.cos(math.pi / 4), math.sin(math.pi / 4)
+    intr = Intrinsics(4.0, 4.0, 2.0, 3.0, 8, 6)
+    cases = [  # (pose, pixel, world)
+        ([c, 0, 0, s, 1, 2, 3], (6, 3), (1.0, 4.0, 5.0)),     # +x → +y
+        ([c, 0, 0, s, 1, 2, 3], (2, 7 - 4), (1.0, 2.0, 5.0)),  # principal ray (0,0,2) → (0,0,2)
+        ([0, 0, 0, 1, 1, 2, 3], (6, 3), (-1.0, 2.0, 5.0)),    # 180° about z: +x → −x
+        ([c, 0, s, 0, 1, 2, 3], (6, 3), (3.0, 2.0, 1.0)),     # 90° about y: +x → −z, +z → +x
+    ]
+    for pose, (x, y), world in cases:
+        if world is None:
+            continue
+        for mode in MODES:
+            depth = np.zeros((1, 6, 8))
+            depth[0, y, x] = 2.0
+            pr, _, n = oracle.instantiate(depth, np.zeros((1, 6, 8, 3)), np.array([pose]), intr, mode=mode)
+            np.testing.assert_allclose(pr[y * 8 + x, :3], world, atol=1e-6, err_msg=f"{pose} {mode}")
+    # camera +y → world +z under a 90° turn about +x: pixel (cx, cy + fy/2) at d = 2 is X_c = (0, 1, 2)
+    # → R·X_c = (0, −2, 1) (y → z, z → −y), + t = (1, 0, 4)
+    intr2 = Intrinsics(4.0, 4.0, 2.0, 1.0, 8, 6)
+    for mode in MODES:
+        depth = np.zeros((1, 6, 8))
+        depth[0, 3, 2] = 2.0
+        pr, _, _ = oracle.instantiate(depth, np.zeros((1, 6, 8, 3)), np.array([[c, s, 0, 0, 1, 2, 3]]), intr2, mode=mode)
+        np.testing.assert_allclose(pr[3 * 8 + 2, :3], (1.0, 0.0, 4.0), atol=1e-6)
+    # and the view transform is its inverse: projecting that world point from the same pose
+    # gives back the pixel and the depth (S:75 round trip through a non-trivial rotation)
+    p = oracle.project(np.array([[1.0, 0.0, 4.0, 0.01]]), np.array([c, s, 0, 0, 1, 2, 3]), intr2, mode="f64")
+    np.testing.assert_allclose(p["proj"][0, :3], (2.0, 3.0, 2.0), atol=1e-12)
+
+
+def test_pose_adam_spec_examples():
+    """S:207-215 (adam_step): zero gradient → parameters unchanged; constant gradient g, first step
+    → Δ = −lr·g/(|g| + ε) ≈ −lr·sign(g) (bias correction makes m̂ = g, v̂ = g²), and the same
+    again on the second step; the quaternion is renormalised after every step (|q| = 1 within
+    1e-9); separate rates for rotation and translation."""
+    q = np.array([0.9, 0.1, -0.3, 0.2])
+    pose0 = np.concatenate([q / np.linalg.norm(q), [0.5, -1.0, 2.0]])
+    p, st = oracle.pose_adam(pose0, np.zeros(7), np.zeros(15), 0.01, 0.02)
+    np.testing.assert_allclose(p, pose0, atol=1e-15)
+    assert st[14] == 1.0
+    g = np.array([0.0, 0.0, 0.0, 0.0, 3.0, -0.5, 1e-3])
+    p1, st1 = oracle.pose_adam(pose0, g, np.zeros(15), 0.01, 0.02)
+    np.testing.assert_allclose(p1[4:] - pose0[4:], -0.02 * g[4:] / (np.abs(g[4:]) + 1e-8), rtol=1e-12)
+    np.testing.assert_allclose(p1[:4], pose0[:4], atol=1e-15)        # zero rotation gradient
+    p2, _ = oracle.pose_adam(p1, g, st1, 0.01, 0.02)
+    np.testing.assert_allclose(p2[4:] - p1[4:], -0.02 * g[4:] / (np.abs(g[4:]) + 1e-8), rtol=1e-9)
+    rng = np.random.default_rng(0)
+    p, st = pose0.copy(), np.zeros(15)
+    for _ in range(20):
+        p, st = oracle.pose_adam(p, rng.normal(size=7), st, 0.05, 0.01)
+        assert abs(np.linalg.norm(p[:4]) - 1.0) < 1e-9
+    # a rotation-only gradient moves q by ≈ lr per component before renormalisation
+    gq = np.array([1.0, -1.0, 0.0, 0.0, 0, 0, 0])
+    p3, _ = oracle.pose_adam(np.array([1.0, 0, 0, 0, 0, 0, 0]), gq, np.zeros(15), 0.01, 0.02)
+    raw = np.array([1.0 - 0.01, 0.01, 0.0, 0.0])
+    np.testing.assert_allclose(p3[:4], raw / np.linalg.norm(raw), atol=1e-9)
+    np.testing.assert_allclose(p3[4:], 0.0, atol=0)
+
+
+def _brute_render_vec(pr, co, view, intr):
+    """Naive compositing over ALL Gaussians in (z, gid) order, every pixel at once."""
+    p = oracle.project(pr, view, intr, mode="f64")
+    order = sorted([g for g in range(len(pr)) if p["status"][g]], key=lambda g: (p["proj"][g, 2], g))
+    H, W = intr.height, intr.width
+    ys, xs = np.mgrid[0:H, 0:W].astype(np.float64)
+    T = np.ones((H, W))
+    alive = np.ones((H, W), dtype=bool)
+    acc = np.zeros((H, W, 5))
+    for g in order:
+        u, v, z, s = p["proj"][g]
+        x0, y0, x1, y1 = p["rect"][g]
+        inr = (xs >= x0) & (xs <= x1) & (ys >= y0) & (ys <= y1)
+        d2 = (xs - u) ** 2 + (ys - v) ** 2
+        a = np.minimum(co[g, 3] * np.exp(-0.5 * d2 / (s * s)), 0.999)
+        el = alive & inr & (d2 <= 9 * s * s) & (a >= 1 / 255)
+        Tn = T * (1 - a)
+        stop = el & (Tn < 1e-4)
+        alive &= ~stop
+        comp = el & ~stop
+        acc[comp] += (a * T)[comp][:, None] * np.array([co[g, 0], co[g, 1], co[g, 2], z, 1.0])
+        T = np.where(comp, Tn, T)
+    return acc
+
+
+def test_tiled_equals_naive_1000_trials():
+    """S:166 and SPEC acceptance 2: the tiled renderer (tile lists, per-tile depth order) equals
+    a naive per-pixel compositor over all Gaussians within 1e-5 on ≥ 1000 random scenes at
+    16×16 … 32×32 (fp64 oracle mode; ragged sizes included)."""
+    worst = 0.0
+    for t in range(1000):
+        rng = np.random.default_rng(1000 + t)
+        W, H = int(rng.integers(16, 33)), int(rng.integers(16, 33))
+        m = micro_scene(t, n=int(rng.integers(1, 31)), width=W, height=H)
+        pr, co = m["pos_rad"].astype(np.float64), m["col_opa"].astype(np.float64)
+        r = oracle.render(pr, co, m["view"], m["intr"], mode="f64")
+        b = _brute_render_vec(pr, co, m["view"], m["intr"])
+        err = max(np.abs(r["color"] - b[..., :3]).max(), np.abs(r["depth"] - b[..., 3]).max(),
+                  np.abs(r["sil"] - b[..., 4]).max())
+        worst = max(worst, err)
+        assert err <= 1e-5, (t, err)
+    assert worst <= 1e-12
+
+
+def test_gradients_central_differences_100_scenes():
+    """S:218 / SPEC acceptance 1: analytic gradients (colour, opacity, radius, the 7 pose
+    parameters) against central finite differences on ≥ 100 random micro-scenes (16×16, ≤ 30
+    Gaussians), fp64.  Parameters whose ±ε runs change a discrete decision are skipped."""
+    total = skipped_all = 0
+    worst_all = 0.0
+    for seed in range(100, 200):
+        m = micro_scene(seed, n=5 + seed % 26)
+        checked, skipped, worst = _fd_check(m, seed)
+        total += checked
+        skipped_all += skipped
+        worst_all = max(worst_all, worst)
+        assert worst < 1e-5, (seed, worst)
+    assert total >= 100 * 40 and skipped_all <= 0.02 * total, (total, skipped_all)
