@@ -21,6 +21,7 @@ constexpr unsigned kFull = kFullMask;
 
 struct BwdArgs {
     const float4 *proj;
+    const float2 *thr;            // per Gaussian (D_c, D_clamp), k_project_count
     const float4 *col_opa;
     const float4 *pos_rad;
     const uint32_t *tile_count;
@@ -124,9 +125,9 @@ constexpr int kBwdWarps = 2;
 
 template <bool ATTR, bool POSE, bool LOSS>
 __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
-    __shared__ float4 sA[kBwdWarps][32];
-    __shared__ float4 sB[kBwdWarps][32];
-    __shared__ float sZ[kBwdWarps][32];
+    __shared__ float4 sA[kBwdWarps][32];             // u, v, 1/o, escale
+    __shared__ float4 sB[kBwdWarps][32];             // c, z
+    __shared__ float2 sL[kBwdWarps][32];             // log2 o, D_clamp
     __shared__ float4 sX[kBwdWarps][POSE ? 32 : 1];  // X_c and ±σ (−: σ clamped)
     __shared__ float4 sG[kBwdWarps][32];             // per pixel (g_C, g_D)
     // [kBwdWarps][32 entries][32 pixels]: phase 1 writes column = own lane (conflict-free per
@@ -176,12 +177,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
 
     const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
     EntryRegs nxt;
-    fetch_entry<false>(nxt, list, bb_top + (int)lane, wmax, p.proj, p.col_opa, nullptr);
+    fetch_entry(nxt, list, bb_top + (int)lane, wmax, p.proj, p.col_opa, p.thr);
     uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
     for (int bb = bb_top; bb >= 0; bb -= 32) {
         const EntryRegs cur = nxt;
         const uint32_t mcur = mnx;
-        fetch_entry<false>(nxt, list, bb - 32 + (int)lane, wmax, p.proj, p.col_opa, nullptr);
+        fetch_entry(nxt, list, bb - 32 + (int)lane, wmax, p.proj, p.col_opa, p.thr);
         mnx = load_mask(mlist, bb - 32 + (int)lane, wmax);  // next (lower) batch
         const int jj = bb + (int)lane;
         unsigned mj = 0u;
@@ -189,9 +190,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
         if (jj < wmax) {   // wmax ≤ the sub-list length
             const float s = fabsf(cur.pr.w);
             s2j = __fmul_rn(s, s);
-            sA[wl_][lane] = make_float4(cur.pr.x, cur.pr.y, s2j, exp_scale(s2j));
-            sB[wl_][lane] = cur.co;
-            sZ[wl_][lane] = cur.pr.z;
+            sA[wl_][lane] = make_float4(cur.pr.x, cur.pr.y, 1.0f / cur.co.w, exp_scale(s2j));
+            sB[wl_][lane] = make_float4(cur.co.x, cur.co.y, cur.co.z, cur.pr.z);
+            sL[wl_][lane] = entry_lo(cur.co.w, cur.th.y);
             if (POSE)   // camera-space centre from the projection (x = (u − cx)·z / fx, …)
                 sX[wl_][lane] = make_float4((cur.pr.x - p.in.cx) * cur.pr.z * rcp_approx(p.in.fx),
                                             (cur.pr.y - p.in.cy) * cur.pr.z * rcp_approx(p.in.fy), cur.pr.z, cur.pr.w);
@@ -204,18 +205,18 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
         // together; the recursion (T, Fb, Tb) then runs over the two in order ----
         auto stage_a = [&](int k, bool v, float &a, float &rc, float &wgt, float &fi, bool &aclamp) {
             float4 A, B;
-            float zk;
+            float2 lo;
             if (v) {   // predicated loads: lanes without a pair add no shared-memory traffic
                 A = sA[wl_][k];
                 B = sB[wl_][k];
-                zk = sZ[wl_][k];
+                lo = sL[wl_][k];
             }
             const float d2 = pair_d2(pxf, pyf, A.x, A.y);
-            const float raw = raw_alpha(d2, A.z, A.w, B.w, v, wgt);
-            aclamp = raw > kAlphaMax;
-            a = aclamp ? kAlphaMax : raw;
+            a = pair_alpha(d2, A.w, lo);   // the forward's α bits (same entry data, same thresholds)
+            aclamp = d2 <= lo.y;
+            wgt = a * A.z;                 // w = α / o (unclamped)
             rc = rcp_approx(1.0f - a);
-            fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (zk - rz);
+            fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (B.w - rz);
         };
         auto stage_b = [&](int k, bool aclamp, float a, float rc, float wgt, float fi) {
             const float oma = 1.0f - a;
@@ -340,16 +341,16 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
 // boundaries at their own pace over a ring of R resident batches, like the forward's ring
 // (k_composite_fwd_ring): a lane only waits when it needs a batch not yet built and the ring is
 // R batches ahead of the slowest lane.  The lane's candidates are the forward's EXACT composited
-// pairs (no compositing test is re-done).  Per entry the slot keeps A = (u, v, s2, escale),
-// B = (c, z), Xq = (X_c.x, X_c.y, o, o/σ²) and ±1/z (−: σ clamped, ∂σ/∂z = 0); per pair
+// pairs (no compositing test is re-done).  Per entry the slot keeps A = (u, v, 1/o, escale),
+// B = (c, z), Xq = (X_c.x, X_c.y, log2 o, o/σ²) and (±1/z (−: σ clamped, ∂σ/∂z = 0), D_clamp); per pair
 //   q = (o/σ²)·dL/dα·w,  g = (q·dx·fx/z, q·dy·fy/z, g_D·ω − q·dx·(u−cx)/z − q·dy·(v−cy)/z − q·d²·[1/z])
 // ------------------------------------------------------------------------------------------
 template <int R>
 struct PoseRing {
-    float4 A[R * 32];
-    float4 B[R * 32];
-    float4 Xq[R * 32];
-    float iz[R * 32];
+    float4 A[R * 32];        // u, v, 1/o, escale
+    float4 B[R * 32];        // c, z
+    float4 Xq[R * 32];       // X_c.x, X_c.y, log2 o, o/σ²
+    float2 iz[R * 32];       // ±1/z (−: σ clamped), D_clamp
     uint32_t bits[R * 32];   // per lane: its composited entries of the batch (bit k = entry k)
 };
 
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
     const float fx = p.in.fx, fy = p.in.fy, cxp = p.in.cx, cyp = p.in.cy;
 
     EntryStream st;
-    stream_start<false>(st, list, bb_top + (int)lane, bb_top - 32 + (int)lane, cnt, p.proj, p.col_opa, nullptr);
+    stream_start(st, list, bb_top + (int)lane, bb_top - 32 + (int)lane, cnt, p.proj, p.col_opa, p.thr);
     uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
     const float ifx = 1.0f / fx, ify = 1.0f / fy;
     int built = 0;
@@ -404,19 +405,20 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
             const EntryRegs &e = st.e;
             const float s = fabsf(e.pr.w);
             const float s2 = __fmul_rn(s, s);
-            ring.A[slot + lane] = make_float4(e.pr.x, e.pr.y, s2, exp_scale(s2));
+            ring.A[slot + lane] = make_float4(e.pr.x, e.pr.y, 1.0f / e.co.w, exp_scale(s2));
             ring.B[slot + lane] = make_float4(e.co.x, e.co.y, e.co.z, e.pr.z);
             // X_c from the projection itself (x = (u − cx)·z / fx, …): no gather of the world centre
             const float iz = rcp_approx(e.pr.z);
-            ring.Xq[slot + lane] = make_float4((e.pr.x - cxp) * e.pr.z * ifx, (e.pr.y - cyp) * e.pr.z * ify, e.co.w,
+            const float2 lo = entry_lo(e.co.w, e.th.y);
+            ring.Xq[slot + lane] = make_float4((e.pr.x - cxp) * e.pr.z * ifx, (e.pr.y - cyp) * e.pr.z * ify, lo.x,
                                                e.co.w * rcp_approx(s2));
-            ring.iz[slot + lane] = e.pr.w > 0.f ? iz : -iz;
+            ring.iz[slot + lane] = make_float2(e.pr.w > 0.f ? iz : -iz, lo.y);
             mj = mnx & onmask;   // the forward's exact composited pixels with a nonzero upstream
         }
         ring.bits[slot + lane] = transpose32(mj, lane);
         ++built;
         const int nidx = bb - 32 + (int)lane;
-        stream_next<false>(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, nullptr);
+        stream_next(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, p.thr);
         mnx = load_mask(mlist, nidx, wmax);
     };
     while (built < nb && built < R) build();
@@ -444,13 +446,13 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
             }
             if (has) {   // every candidate is a composited pair
                 const float4 Xq = ring.Xq[soff + k];
-                const float izs = ring.iz[soff + k];
+                const float2 izl = ring.iz[soff + k];
+                const float izs = izl.x;
                 const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
                 const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-                float wgt;
-                const float raw = raw_alpha(d2, A.z, A.w, Xq.z, true, wgt);
-                const bool aclamp = raw > kAlphaMax;
-                const float a = aclamp ? kAlphaMax : raw;
+                const float a = pair_alpha(d2, A.w, make_float2(Xq.z, izl.y));   // the forward's α bits
+                const bool aclamp = d2 <= izl.y;
+                const float wgt = a * A.z;   // w = α / o (unclamped)
                 const float oma = 1.0f - a;
                 const float Ti = T * rcp_approx(oma);
                 const float om = a * Ti;
@@ -718,7 +720,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile, T = ntx * nty;
     cudaError_t err;
     BwdArgs a{};
-    a.proj = c.proj; a.col_opa = c.col_opa; a.pos_rad = c.pos_rad;
+    a.proj = c.proj; a.thr = c.thr; a.col_opa = c.col_opa; a.pos_rad = c.pos_rad;
     a.tile_count = c.tile_count; a.tile_start = c.tile_start; a.sub_lists = c.sub_lists; a.sub_count = c.sub_count;
     a.sub_masks = c.sub_masks;
     a.W = W; a.H = H; a.ntx = ntx;

@@ -25,18 +25,17 @@ struct EntryRegs {
     uint32_t g;
     float4 pr;
     float4 co;
-    uint2 r;
+    float2 th;   // (D_c, D_clamp) of k_project_count
 };
 
-template <bool RECT = true>
 __device__ __forceinline__ void fetch_entry(EntryRegs &er, const uint32_t *__restrict__ list, int idx, int n,
                                             const float4 *__restrict__ proj, const float4 *__restrict__ col,
-                                            const uint2 *__restrict__ rect) {
+                                            const float2 *__restrict__ thr) {
     if (idx >= 0 && idx < n) {
         er.g = __ldg(list + idx);
         er.pr = __ldg(proj + er.g);
         er.co = __ldg(col + er.g);
-        if (RECT) er.r = __ldg(rect + er.g);
+        er.th = __ldg(thr + er.g);
     }
 }
 
@@ -49,25 +48,23 @@ struct EntryStream {
     bool gv;
 };
 
-template <bool RECT = true>
 __device__ __forceinline__ void stream_start(EntryStream &s, const uint32_t *__restrict__ list, int idx0, int idx1,
                                              int n, const float4 *__restrict__ proj, const float4 *__restrict__ col,
-                                             const uint2 *__restrict__ rect) {
-    fetch_entry<RECT>(s.e, list, idx0, n, proj, col, rect);
+                                             const float2 *__restrict__ thr) {
+    fetch_entry(s.e, list, idx0, n, proj, col, thr);
     s.gv = idx1 >= 0 && idx1 < n;
     if (s.gv) s.gn = __ldg(list + idx1);
 }
 
 // e ← the attributes of gid gn; gn ← the gid at idx2
-template <bool RECT = true>
 __device__ __forceinline__ void stream_next(EntryStream &s, const uint32_t *__restrict__ list, int idx2, int n,
                                             const float4 *__restrict__ proj, const float4 *__restrict__ col,
-                                            const uint2 *__restrict__ rect) {
+                                            const float2 *__restrict__ thr) {
     if (s.gv) {
         s.e.g = s.gn;
         s.e.pr = __ldg(proj + s.gn);
         s.e.co = __ldg(col + s.gn);
-        if (RECT) s.e.r = __ldg(rect + s.gn);
+        s.e.th = __ldg(thr + s.gn);
     }
     s.gv = idx2 >= 0 && idx2 < n;
     if (s.gv) s.gn = __ldg(list + idx2);
@@ -80,36 +77,88 @@ __device__ __forceinline__ uint32_t load_mask(const uint32_t *__restrict__ mlist
 }
 
 // ---- α of a (pixel, Gaussian) pair: ONE definition for every compositing kernel -----------
-// DESIGN.md §3 step 7: w = exp((−0.5·d²)/σ²), α = min(o·w, 0.999), skipped iff α < 1/255.
-// Per entry the kernels keep s2 = fl(σ·σ) and the IEEE exponent scale escale = fl(−½log2(e)/s2)
-// (exp_scale, computed once per entry, identical bits in every kernel).  Fast path:
-// w = ex2.approx(fl(d²·escale)), relative error ≤ ~7e-7 against the correctly rounded fp32 exp
-// of the fp32 argument fl(fl(−0.5·d²)/s2) — the oracle's w.  When the raw α = fl(o·w) lies within
-// kNearRel (1.5e-5, ≥ 20× that error) of 1/255 or 0.999 the decision could depend on it, so w is
-// recomputed as that correctly rounded exp (fp64 exp, rounded once): every α decision is then
-// taken on the oracle's bits.  The forward and the backward call the same function on the same
-// stored entry data, so they see the same α bits (no fwd/bwd decision mismatch).
+// DESIGN.md §3 step 7: w = exp((−0.5·d²)/σ²), α = min(o·w, 0.999), skipped iff α < 1/255.  The
+// decisions are taken on the oracle's bits — w the correctly rounded fp32 exp of the fp32
+// argument fl(fl(−0.5·d²)/s2), s2 = fl(σ·σ) — and every one of them is MONOTONE in d² (each
+// rounding step is monotone): "α ≥ 1/255" ⇔ d² ≤ D_floor and "o·w > 0.999" (clamped) ⇔
+// d² ≤ D_clamp, for per-Gaussian fp32 thresholds that k_project_count finds once per view with
+// the exact arithmetic (alpha_thresholds).  The compositing kernels then decide with compares
+// only; the VALUE of an unclamped α uses the fast w = ex2.approx(fl(d²·escale)),
+// escale = fl(−½log2(e)/s2) (relative error ≤ ~7e-7, a value difference, never a decision).
+// The forward and the backward read the same thresholds, so they composite the same pairs.
 constexpr float kAlphaMin = 1.0f / 255.0f;
-constexpr float kNearRel = 1.0f / 65536.0f;
 constexpr float kNegHalfLog2e = -0.5f * kLog2e;
 
 __device__ __forceinline__ float exp_scale(float s2) { return __fdiv_rn(kNegHalfLog2e, s2); }
 
-__device__ __forceinline__ float exact_w(float d2, float s2) {
-    return __double2float_rn(exp((double)__fdiv_rn(__fmul_rn(-0.5f, d2), s2)));
+// the oracle's raw α = fl(o·w) with the correctly rounded w (fp64 exp, rounded once)
+__device__ __forceinline__ float exact_raw_alpha(float d2, float s2, float o) {
+    const float w = __double2float_rn(exp((double)__fdiv_rn(__fmul_rn(-0.5f, d2), s2)));
+    return __fmul_rn(o, w);
 }
 
-// raw α = fl(o·w) before the 0.999 clamp (α = min(raw, 0.999); clamped ⇔ raw > 0.999); w is
-// returned for the backward's chain.  `elig` = the pair passed the 3σ test (only those decide).
-__device__ __forceinline__ float raw_alpha(float d2, float s2, float escale, float o, bool elig, float &w) {
-    w = fast_exp2(__fmul_rn(d2, escale));
-    float raw = __fmul_rn(o, w);
-    const bool near = fabsf(raw - kAlphaMax) <= kAlphaMax * kNearRel || fabsf(raw - kAlphaMin) <= kAlphaMin * kNearRel;
-    if (elig && near) {
-        w = exact_w(d2, s2);
-        raw = __fmul_rn(o, w);
+// Largest fp32 d² in [0, cap] whose exact raw α passes (raw ≥ thr, or raw > thr when strict), −1
+// if d² = 0 already fails.  The predicate is non-increasing in d², so the answer is the boundary
+// next to the continuous estimate d² = 2 s2 ln(o/thr): a few exact evaluations walk to it.
+static __device__ __noinline__ float alpha_threshold_d2(float s2, float o, float thr, bool strict, float cap) {
+    auto pass = [&](float d2) {
+        const float r = exact_raw_alpha(d2, s2, o);
+        return strict ? r > thr : r >= thr;
+    };
+    if (!pass(0.0f)) return -1.0f;
+    if (pass(cap)) return cap;
+    const double est = 2.0 * (double)s2 * log((double)o / (double)thr);
+    float d = (float)fmin(fmax(est, 0.0), (double)cap);
+    float lo, hi;   // pass(lo), !pass(hi)
+    if (pass(d)) {
+        lo = d;
+        hi = cap;
+        for (int i = 0; i < 8; ++i) {
+            const float n = __uint_as_float(__float_as_uint(lo) + 1u);
+            if (!pass(n)) return lo;
+            lo = n;
+        }
+    } else {
+        hi = d;
+        lo = 0.0f;
+        for (int i = 0; i < 8; ++i) {
+            const float n = __uint_as_float(__float_as_uint(hi) - 1u);
+            if (pass(n)) return n;
+            hi = n;
+        }
     }
-    return raw;
+    while (__float_as_uint(hi) - __float_as_uint(lo) > 1u) {   // far from the estimate: bisect the bits
+        const float m = __uint_as_float((__float_as_uint(lo) >> 1) + (__float_as_uint(hi) >> 1) +
+                                        (__float_as_uint(lo) & __float_as_uint(hi) & 1u));
+        if (pass(m)) lo = m; else hi = m;
+    }
+    return lo;
+}
+
+// (D_c, D_clamp) of a Gaussian with σ² = s2 and opacity o: composited-eligible ⇔ d² ≤ D_c =
+// min(D_floor, fl(9·s2)) (the 3σ truncation and the α floor in one compare), clamped ⇔
+// d² ≤ D_clamp (−1: never; w ≤ 1 so only o > 0.999 can clamp).
+__device__ __forceinline__ float2 alpha_thresholds(float s2, float o) {
+    const float cap = __fmul_rn(9.0f, s2);
+    const float dc = alpha_threshold_d2(s2, o, kAlphaMin, false, cap);
+    const float dcl = o > kAlphaMax ? alpha_threshold_d2(s2, o, kAlphaMax, true, cap) : -1.0f;
+    return make_float2(dc, dcl);
+}
+
+// α VALUE of a pair (the decision d² ≤ D_c is the caller's): 0.999 when clamped (d² ≤ D_clamp),
+// else min(2^(d²·escale + log2 o), 0.999) with lo = (log2 o, D_clamp) kept per entry — o folded
+// into the exponent (one FFMA + one MUFU.EX2).  Relative error vs the oracle's o·w ≤ ~8e-7.
+// Every compositing kernel calls this on the same entry data, so forward and backward see the
+// same α bits.
+__device__ __forceinline__ float pair_alpha(float d2, float escale, float2 lo) {
+    return d2 <= lo.y ? kAlphaMax : fminf(fast_exp2(fmaf(d2, escale, lo.x)), kAlphaMax);
+}
+
+// per-entry (log2 o, D_clamp)
+__device__ __forceinline__ float2 entry_lo(float o, float dcl) {
+    float l;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(o));
+    return make_float2(l, dcl);
 }
 
 // d² of pixel (xf, yf) to centre (u, v), DESIGN.md §3 step 7 (no FMA contraction)

@@ -10,6 +10,7 @@ namespace vtgs {
 
 struct FwdArgs {
     const float4 *proj;
+    const float2 *thr;     // per Gaussian (D_c, D_clamp), k_project_count
     const float4 *col_opa;
     const uint32_t *tile_count;
     const uint32_t *tile_start;
@@ -33,13 +34,14 @@ constexpr int kFwdWarps = 2;  // warps (8×4 sub-tiles) per CTA: small CTAs reti
 // the whole-list candidate count — tools/sim_batches.py: lane efficiency 0.27 → 0.87 at R = 16.
 constexpr int kInner = 6;                      // lane-independent steps between warp checks
 
-template <int R>
+template <int R, bool STATS>
 struct FwdRing {
-    float4 A[R * 32];        // u, v, s2 = σ², escale = −½log2(e)/s2
-    float4 B[R * 32];        // c_r, c_g, c_b, o
-    float Z[R * 32];         // z
+    float4 A[R * 32];        // u, v, D_c, escale = −½log2(e)/σ²
+    float4 B[R * 32];        // c_r, c_g, c_b, z
+    float2 LO[R * 32];       // log2 o, D_clamp
     uint32_t bits[R * 32];   // per lane: its candidate entries of the batch (bit 31 − j = entry j)
     uint32_t cbits[R * 32];  // per lane: the entries it composited (same orientation)
+    float S9[STATS ? R * 32 : 1];   // 9σ² (the work counter's 3σ test)
 };
 
 template <int R, bool STATS>
@@ -47,7 +49,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     extern __shared__ float4 fwd_smem[];
     static_assert((R & (R - 1)) == 0, "ring depth must be a power of two");
     const int wl = threadIdx.x >> 5;
-    FwdRing<R> &ring = reinterpret_cast<FwdRing<R> *>(fwd_smem)[wl];
+    FwdRing<R, STATS> &ring = reinterpret_cast<FwdRing<R, STATS> *>(fwd_smem)[wl];
     const int gsub = blockIdx.x * kFwdWarps + wl;
     const int tile = gsub >> 3;
     const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     const unsigned inmask = __ballot_sync(kFullMask, inside);
 
     EntryStream st;
-    stream_start<false>(st, list, (int)lane, 32 + (int)lane, cnt, p.proj, p.col_opa, nullptr);
+    stream_start(st, list, (int)lane, 32 + (int)lane, cnt, p.proj, p.col_opa, p.thr);
     const EntryRegs &nxt = st.e;
     int built = 0;
     // Exact composited masks (forward → backward): each lane ORs the entries it composites into
@@ -87,17 +89,20 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
         if (idx < cnt) {
             const float s = fabsf(nxt.pr.w);
             const float s2 = __fmul_rn(s, s);
-            ring.A[slot + lane] = make_float4(nxt.pr.x, nxt.pr.y, s2, exp_scale(s2));
-            ring.B[slot + lane] = nxt.co;
-            ring.Z[slot + lane] = nxt.pr.z;
-            const unsigned m0 =
-                lane_mask(make_float4(nxt.pr.x, nxt.pr.y, __fmul_rn(9.0f, s2), 0.f), rect_from_proj(nxt.pr, p.W, p.H), sx, sy);
+            const float s9 = __fmul_rn(9.0f, s2);
+            ring.A[slot + lane] = make_float4(nxt.pr.x, nxt.pr.y, nxt.th.x, exp_scale(s2));
+            ring.B[slot + lane] = make_float4(nxt.co.x, nxt.co.y, nxt.co.z, nxt.pr.z);
+            ring.LO[slot + lane] = entry_lo(nxt.co.w, nxt.th.y);
+            if (STATS) ring.S9[slot + lane] = s9;
+            // candidates: the pixels within D_c (the work counters also want the whole 3σ disc)
+            const unsigned m0 = lane_mask(make_float4(nxt.pr.x, nxt.pr.y, STATS ? s9 : nxt.th.x, 0.f),
+                                          rect_from_proj(nxt.pr, p.W, p.H), sx, sy);
             mj = m0 & inmask;
         }
         ring.bits[slot + lane] = __brev(transpose32(mj, lane));  // bit 31 − j = entry j
         ring.cbits[slot + lane] = 0u;
         ++built;
-        stream_next<false>(st, list, (built + 1) * 32 + (int)lane, cnt, p.proj, p.col_opa, nullptr);
+        stream_next(st, list, (built + 1) * 32 + (int)lane, cnt, p.proj, p.col_opa, p.thr);
     };
     while (built < nb && built < R) build();
     __syncwarp();
@@ -113,7 +118,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     int soff = 0;
     int lbase = 0;
     auto flush = [&]() {   // store the lane's composited bits of batch b (before leaving it)
-        if (cw) ring.cbits[soff + lane] = cw;
+        ring.cbits[soff + lane] = cw;   // (b = −1: slot 0's own column, still 0 — harmless)
         cw = 0u;
     };
     auto advance = [&]() {
@@ -134,34 +139,34 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
             const unsigned bit = 1u << (hb & 31);
             cur &= ~bit;
             const int k = soff + 31 - hb;                  // ring index of entry 31 − hb
-            float4 A, Bc;                                  // unused unless `has` (elig includes it)
+            float4 A, Bc;                                  // unused unless `has` (comp includes it)
+            float2 lo;
             if (has) {   // predicated loads: idle lanes add no shared-memory traffic
                 A = ring.A[k];
                 Bc = ring.B[k];
+                lo = ring.LO[k];
             }
             const float d2 = pair_d2(pxf, pyf, A.x, A.y);
-            const bool elig = has && d2 <= __fmul_rn(9.0f, A.z);
-            float w;
-            const float raw = raw_alpha(d2, A.z, A.w, Bc.w, elig, w);
-            const float a = fminf(raw, kAlphaMax);
-            const bool comp = elig && a >= kAlphaMin;
+            const bool comp = has && d2 <= A.z;            // 3σ truncation and α floor, exact
+            const float a = pair_alpha(d2, A.w, lo);
             const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
             const bool term = comp && Tn < kTMin;
             const bool acc = comp && !term;
             const float om = a * T;
             if (acc) {   // predicated: Bc is garbage for lanes without a candidate
-                const float zk = ring.Z[k];
                 C0 = fmaf(Bc.x, om, C0);
                 C1 = fmaf(Bc.y, om, C1);
                 C2 = fmaf(Bc.z, om, C2);
-                D = fmaf(zk, om, D);
+                D = fmaf(Bc.w, om, D);
                 Sl += om;
                 T = Tn;
                 lastc = (uint32_t)(lbase - hb);
                 cw |= bit;
             }
             if (STATS) {
-                ne += elig ? 1u : 0u;
+                float s9 = 0.f;
+                if (has) s9 = ring.S9[k];
+                ne += (has && d2 <= s9) ? 1u : 0u;
                 nc += acc ? 1u : 0u;
             }
             if (term) {
@@ -222,7 +227,7 @@ static int fwd_variant() {
 
 template <int R, bool STATS>
 static cudaError_t launch_ring_s(const FwdArgs &a, int T, cudaStream_t s) {
-    const size_t sm = sizeof(FwdRing<R>) * kFwdWarps;
+    const size_t sm = sizeof(FwdRing<R, STATS>) * kFwdWarps;
     cudaError_t e =
         cudaFuncSetAttribute(k_composite_fwd_ring<R, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
@@ -238,7 +243,7 @@ static cudaError_t launch_ring(const FwdArgs &a, int T, bool stats, cudaStream_t
 cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
     const int W = c.intr.width, H = c.intr.height;
     const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile;
-    FwdArgs a{c.proj, c.col_opa, c.tile_count, c.tile_start, c.sub_lists, c.sub_count, c.sub_masks, W, H, ntx,
+    FwdArgs a{c.proj, c.thr, c.col_opa, c.tile_count, c.tile_start, c.sub_lists, c.sub_count, c.sub_masks, W, H, ntx,
               c.color, c.depth, c.sil, c.T_final, c.last, c.dev};
     if (fwd_variant() == 8) return launch_ring<8>(a, ntx * nty, c.count_work, s);
     return launch_ring<4>(a, ntx * nty, c.count_work, s);

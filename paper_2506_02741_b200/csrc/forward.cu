@@ -56,11 +56,13 @@ __device__ __forceinline__ Footprint project_one(float4 pr, const PoseR &P, cons
     return f;
 }
 
-__global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict__ pos_rad, int64_t N,
+__global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict__ pos_rad,
+                                                       const float4 *__restrict__ col_opa, int64_t N,
                                                        const vtgs_pose *__restrict__ view,
                                                        vtgs_intrinsics in, int ntx,
                                                        float4 *__restrict__ proj,
                                                        uint2 *__restrict__ rect,
+                                                       float2 *__restrict__ thr,
                                                        uint32_t *__restrict__ tile_count) {
     __shared__ PoseR P;
     if (threadIdx.x == 0) pose_rotation(*view, P);
@@ -77,6 +79,8 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
             proj[g] = f.vis ? make_float4(f.u, f.v, f.z, f.clamped ? -f.s : f.s) : make_float4(0.f, 0.f, 0.f, 0.f);
             rect[g] = f.vis ? make_uint2((uint32_t)f.x0 | ((uint32_t)f.x1 << 16), (uint32_t)f.y0 | ((uint32_t)f.y1 << 16))
                             : make_uint2(0xffffffffu, 0xffffffffu);
+            // exact α decision thresholds in d² (composite_common.cuh): once per Gaussian per view
+            thr[g] = f.vis ? alpha_thresholds(__fmul_rn(f.s, f.s), __ldg(&col_opa[g].w)) : make_float2(-1.f, -1.f);
         }
         const int tx0 = f.vis ? f.x0 >> 4 : 0, ty0 = f.vis ? f.y0 >> 4 : 0;
         const int ntg = f.vis ? (f.x1 >> 4) - tx0 + 1 : 0;
@@ -851,7 +855,8 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     const int gN = (int)(gN64 < (int64_t)c.num_sms * 16 ? gN64 : (int64_t)c.num_sms * 16);
     if (N > 0) {
         LaunchScope ls(&c, kProject, s);
-        k_project_count<<<gN, 256, 0, s>>>(c.pos_rad, N, c.view, c.intr, ntx, c.proj, c.rect, c.tile_count);
+        k_project_count<<<gN, 256, 0, s>>>(c.pos_rad, c.col_opa, N, c.view, c.intr, ntx, c.proj, c.rect, c.thr,
+                                           c.tile_count);
         if ((err = cudaGetLastError())) return err;
     }
     {

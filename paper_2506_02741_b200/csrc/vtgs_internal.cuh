@@ -61,6 +61,7 @@ struct Ctx {
     // scratch (device)
     float4 *proj = nullptr;          // (u, v, z, ±σ) per Gaussian, −σ ⇔ σ clamped
     uint2 *rect = nullptr;           // (x0 | x1<<16, y0 | y1<<16)
+    float2 *thr = nullptr;           // (D_c, D_clamp): exact α decision thresholds in d² (composite_common.cuh)
     uint32_t *tile_count = nullptr;  // [max_tiles]
     uint32_t *tile_start = nullptr;  // [max_tiles + 1]
     uint32_t *tile_cursor = nullptr; // [max_tiles]
@@ -72,7 +73,7 @@ struct Ctx {
     uint32_t *vals2 = nullptr;
     uint32_t *offs = nullptr;        // fallback sort ranks [max_pairs]
     uint32_t *chunk_list = nullptr;  // the long-tile plans' chunk descriptors, 12 u32 each [12·(max_pairs/2048 + max_tiles + 1)]
-    uint32_t *sub_masks = nullptr;   // per sub-list entry: its 32-pixel mask (forward → backward) [8·max_pairs]
+    uint32_t *sub_masks = nullptr;   // per sub-list entry: the pixels that composited it (forward → backward) [8·max_pairs]
     uint32_t *sub_lists = nullptr;   // per tile 8 sub-lists (8×4 sub-tiles), capacity 8·n_tile [8·max_pairs]
     uint32_t *sub_count = nullptr;   // [8·max_tiles]
     float *T_final = nullptr;        // per pixel
