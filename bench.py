@@ -177,18 +177,66 @@ def oracle_step(cfg, state, view, rows):
     return loss, g
 
 
-def time_oracle(cfg, steps, warmup, rows):
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def set_oracle_threads(n: int):
+    """The oracle's OpenMP thread count (oracle/vtgs_oracle.c: rows / row bands in parallel)."""
+    import ctypes
+    try:
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+    except OSError:
+        pass
+    os.environ["OMP_NUM_THREADS"] = str(n)
+
+
+def time_oracle(cfg, steps, warmup, rows, threads=1, state=None):
+    """Seconds per oracle step (render + L1 + backward of `rows` of view 0) with `threads` OpenMP
+    threads, and the pixels per step.  `state` = the oracle's instantiated (pos_rad, col_opa)."""
     import oracle
-    pr, co, _ = oracle.instantiate(cfg.depth_stack(), cfg.rgb_stack(), cfg.pose_stack(), cfg.intr, cfg.opacity)
+    if state is None:
+        pr, co, _ = oracle.instantiate(cfg.depth_stack(), cfg.rgb_stack(), cfg.pose_stack(), cfg.intr, cfg.opacity)
+        state = (pr, co)
+    set_oracle_threads(threads)
     view = np.asarray(cfg.views[0], dtype=np.float32).astype(np.float64)
     for _ in range(warmup):
-        oracle_step(cfg, (pr, co), view, rows)
+        oracle_step(cfg, state, view, rows)
     t0 = time.perf_counter()
     for _ in range(steps):
-        oracle_step(cfg, (pr, co), view, rows)
+        oracle_step(cfg, state, view, rows)
     dt = (time.perf_counter() - t0) / max(steps, 1)
     px = (rows[1] - rows[0]) * cfg.intr.width
     return dt, px
+
+
+def cpu_baseline_runs(cfg, repeats=3):
+    """The oracle as it stands on the host: one whole step of the view (all rows), median of
+    `repeats` runs on all host cores and on 1 core."""
+    import oracle
+    pr, co, _ = oracle.instantiate(cfg.depth_stack(), cfg.rgb_stack(), cfg.pose_stack(), cfg.intr, cfg.opacity)
+    rows = (0, cfg.intr.height)
+    ncores = host_cores()
+    res = {}
+    for label, th in (("all_cores", ncores), ("one_core", 1)):
+        ts = [time_oracle(cfg, 1, 0, rows, th, (pr, co))[0] for _ in range(repeats)]
+        res[label] = {"cores": th, "seconds_median": statistics.median(ts), "seconds": ts}
+    set_oracle_threads(ncores)
+    return res, rows[1] * cfg.intr.width
 
 
 def run_reference(args):
@@ -197,18 +245,20 @@ def run_reference(args):
         return 0
     from synth.scenes import make_config
     cfg = make_config(args.config, args.seed)
-    rows = (cfg.intr.height // 2 - 8, cfg.intr.height // 2 + 8)
-    dt, px = time_oracle(cfg, args.steps, args.warmup, rows)
+    rows = (0, cfg.intr.height)   # the whole view, every step
+    ncores = host_cores()
+    dt, px = time_oracle(cfg, args.steps, args.warmup, rows, threads=ncores)
     mpix = px / dt / 1e6
-    sample = (f"rows {rows[0]}-{rows[1] - 1} of view 0 ({px} px) per step; full projection + tile lists of all "
-              f"{cfg.n_slots} slots every step (oracle/vtgs_oracle.c, single thread, -O2)")
+    sample = (f"the whole view 0 ({px} px) per step: projection + tile lists of all {cfg.n_slots} slots, render, "
+              f"L1, backward (oracle/vtgs_oracle.c, -O2, OpenMP on {ncores} host cores, {cpu_model()})")
     line = {
         "impl": "reference", "metric": METRIC, "value": mpix, "unit": "Mpix/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 decisions / f64 values", "data": "synthetic",
         "config": workload_config(cfg, args),
         "gaussians_per_s": cfg.n_slots * (px / (cfg.intr.width * cfg.intr.height)) / dt,
-        "cpu_baseline": {"value": mpix, "unit": "Mpix/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": mpix, "unit": "Mpix/s", "cores": ncores, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": mpix, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -280,6 +330,9 @@ def run_tracking(args):
     with torch.cuda.stream(s):           # warm-up (eager) before capture
         body(s)
     torch.cuda.synchronize()
+    st = R.stats()                        # work counters of the last iteration's forward (diagnostics)
+    R.set_work_counters(False)            # off in the captured loop
+    fp32_meas, ex2_meas = vtgs.measure_peaks(local)
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         body(s)
@@ -322,6 +375,15 @@ def run_tracking(args):
     body(torch.cuda.current_stream())
     prof = R.profile()
     R.set_profiling(False)
+    # roofline of the dominant kernel (per launch = one iteration): the pose backward, FP32-bound
+    peaks, _ = load_peaks()
+    per = {k: v[0] / v[1] for k, v in prof.items() if v[1]}
+    work = {"composite_fwd": FLOPS_PER_EVAL_FWD * st["e_eval"], "composite_bwd": FLOPS_PER_COMP_BWD * st["e_comp"]}
+    dom = max(work, key=lambda k: per.get(k, 0.0))
+    ach = work[dom] / (per[dom] * 1e-3) / 1e12
+    roofline = {"kernel": dom, "bound": "alu", "achieved": ach, "peak": fp32_meas, "unit": "TFLOP/s",
+                "frac": ach / fp32_meas, "traffic": measured_traffic(f"config3_tracking_{W}x{H}_K{cfg.K}", dom),
+                "peak_source": "measured: FP32 FMA-chain microbenchmark in this process (vtgs_measure_peaks)"}
     if rank == 0:
         line = {"metric": METRIC, "value": px / (ms * 1e-3) / 1e6, "unit": "Mpix/s", "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -333,6 +395,10 @@ def run_tracking(args):
                 "tracking": {"t_err_init_m": float(np.linalg.norm(np.asarray(cfg.views[0])[4:] - gt[4:])),
                              "t_err_final_m": float(np.linalg.norm(pf[4:] - gt[4:]))},
                 "stages_eager_frame_ms": {k: v[0] for k, v in prof.items() if v[1]},
+                "roofline": roofline,
+                "work_per_iteration": {"n_pairs": st["n_pairs"], "e_eval": st["e_eval"], "e_comp": st["e_comp"]},
+                "peaks": {"fp32_tflops_measured": fp32_meas, "ex2_per_s_measured": ex2_meas,
+                          "hbm_gbs": peaks.get("hbm_gbs")},
                 "clocks": clk, "gpu_launches": int(args.steps * sum(v[1] for v in prof.values()))}
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -397,6 +463,25 @@ def main():
 
     def step():
         mapper.step(allreduce=ws > 1)
+
+    # measured roofline denominators of the ALU-bound kernels (FMA chain, MUFU ex2), this process
+    fp32_meas, ex2_meas = vtgs.measure_peaks(local)
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    # (1) instantiation (a1), timed on its own: it runs once per keyframe, not per step
+    d_depth, d_rgb = torch.from_numpy(cfg.depth_stack()).to(dev), torch.from_numpy(cfg.rgb_stack()).to(dev)
+    d_kf, d_opa = vtgs.pose_tensor(cfg.pose_stack(), dev), torch.from_numpy(cfg.opacity).to(dev)
+    pr_i, co_i = torch.empty_like(pr), torch.empty_like(co)
+    for _ in range(3):
+        R.instantiate(d_depth, d_rgb, d_kf, cfg.intr, d_opa, out=(pr_i, co_i))
+    inst_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+    for a, b in inst_ev:
+        flush_inst = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev).fill_(1.0)
+        a.record(stream)
+        R.instantiate(d_depth, d_rgb, d_kf, cfg.intr, d_opa, out=(pr_i, co_i))
+        b.record(stream)
+    torch.cuda.synchronize()
+    inst_ms = statistics.median(a.elapsed_time(b) for a, b in inst_ev)
+    del pr_i, co_i, flush_inst, d_depth, d_rgb
 
     clocks = ClockSampler(local) if not args.profile_run else None
     if clocks:
@@ -474,7 +559,8 @@ def main():
     stats = dict(R.stats(), e_eval=st["e_eval"], e_comp=st["e_comp"])
     peaks, peak_src = load_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    fp32_peak = SM_COUNT * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12       # TFLOP/s at max clock
+    fp32_nominal = sm_count * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12    # TFLOP/s at max clock
+    fp32_peak, ex2_peak = fp32_meas, ex2_meas
     hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
     per_launch = {k: (v[0] / v[1] if v[1] else 0.0) for k, v in prof.items()}
     P = stats["n_pairs"]
@@ -502,14 +588,21 @@ def main():
                 ach = units / (per_launch[k] * 1e-3) / 1e12
                 e.update(bound="alu", achieved=ach, unit="TFLOP/s", frac=ach / fp32_peak)
         stage_json[k] = e
+    inst_bytes = 52.0 * N   # depth 4 + rgb 12 + opacity 4 in, pos_rad 16 + col_opa 16 out per slot
+    stage_json["instantiate"] = {"ms_per_launch": inst_ms, "launches": 10, "share": None,
+                                 "note": "timed separately (once per keyframe, not in the step), L2 flushed",
+                                 "bound": "hbm", "achieved": inst_bytes / (inst_ms * 1e-3) / 1e9, "unit": "GB/s",
+                                 "frac": inst_bytes / (inst_ms * 1e-3) / 1e9 / hbm_peak}
     dom = max((k for k in stage_json if k in work), key=lambda k: stage_json[k]["share"])
     d = stage_json[dom]
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"],
                 "peak": hbm_peak if d["bound"] == "hbm" else fp32_peak, "unit": d["unit"], "frac": d["frac"],
                 "traffic": measured_traffic(workload_config(cfg, args)["workload"], dom),
                 "peak_source": (f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)" if d["bound"] == "hbm" else
-                                f"FP32 {SM_COUNT} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz "
-                                f"(B200_PROFILING.md unit counts, max clock)")}
+                                f"measured: FP32 FMA-chain microbenchmark in this process (vtgs_measure_peaks); "
+                                f"nominal {sm_count} SMs x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz = "
+                                f"{fp32_nominal:.1f} TFLOP/s"),
+                "frac_of_nominal": d["achieved"] / (hbm_peak if d["bound"] == "hbm" else fp32_nominal)}
     # the whole step against SURVEY §8(d)'s floors, per view: bytes 32 N (state) + 20 N (gradients)
     # + 24 P (pairs written and read) + 68 HW (images, targets, saved T / last, re-reads); flops
     # 20 E_eval + 60 E_comp; t_floor = max(bytes / HBM peak, flops / FP32 peak)
@@ -517,8 +610,22 @@ def main():
     path_bytes = n_views_rank * (52.0 * N + 24.0 * P + 68.0 * HW)
     path_flops = n_views_rank * (FLOPS_PER_EVAL_FWD * stats["e_eval"] + FLOPS_PER_COMP_BWD * stats["e_comp"])
     t_floor_ms = max(path_bytes / (hbm_peak * 1e9), path_flops / (fp32_peak * 1e12)) * 1e3
+    # whole-step DRAM traffic measured by ncu (profiles/traffic.json, sum over the step's kernels)
+    step_dram = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f).get(workload_config(cfg, args)["workload"])
+        if tj:
+            step_dram = float(sum(v["bytes"] for v in tj.values()))
+    except (OSError, ValueError, KeyError, TypeError):
+        pass
     path_floor = {"bytes": path_bytes, "flops": path_flops, "t_floor_ms": t_floor_ms,
-                  "frac": t_floor_ms / ms_max}
+                  "frac": t_floor_ms / ms_max, "ex2": n_views_rank * (stats["e_eval"] + stats["e_comp"]),
+                  "t_ex2_ms": n_views_rank * (stats["e_eval"] + stats["e_comp"]) / ex2_peak * 1e3,
+                  "step_dram_bytes_ncu": step_dram,
+                  "dram_over_algorithmic": (step_dram / (path_bytes / n_views_rank)) if step_dram else None}
+    peaks_json = {"fp32_tflops_measured": fp32_meas, "ex2_per_s_measured": ex2_meas,
+                  "fp32_tflops_nominal": fp32_nominal, "hbm_gbs": hbm_peak, "hbm_source": peak_src}
 
     # ---------------- e2e: the same step through the C-ABI with HOST buffers
     e2e = None
@@ -554,12 +661,14 @@ def main():
     # ---------------- cpu baseline (oracle as it stands, bounded sample, rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_run:
-        rows = (0, H)   # the whole view: ≈ 15–25 s of single-threaded oracle work (one step)
-        dt, px = time_oracle(cfg, 1, 0, rows)
-        cpu = {"value": px / dt / 1e6, "unit": "Mpix/s", "cores": 1, "kind": "oracle",
+        runs, px = cpu_baseline_runs(cfg)
+        allc, one = runs["all_cores"], runs["one_core"]
+        cpu = {"value": px / allc["seconds_median"] / 1e6, "unit": "Mpix/s", "cores": allc["cores"], "kind": "oracle",
                "sample": f"one whole step of the same view ({px} px): projection + tile lists of all {N} slots, "
-                         f"render, L1, backward; single-threaded C (oracle/vtgs_oracle.c)",
-               "seconds": dt}
+                         f"render, L1, backward (oracle/vtgs_oracle.c, -O2, OpenMP); median of 3 runs",
+               "cpu_model": cpu_model(), "seconds_median": allc["seconds_median"],
+               "one_core": {"value": px / one["seconds_median"] / 1e6, "seconds_median": one["seconds_median"],
+                            "cores": 1}}
 
     if rank == 0:
         line = {
@@ -571,6 +680,7 @@ def main():
             "gaussians_per_s": gps,
             "roofline": roofline,
             "path_floor": path_floor,
+            "peaks": peaks_json,
             "stages": stage_json,
             "stage_timing": f"CUDA events around every kernel on every {PROFILE_EVERY}th timed step ({(args.steps + PROFILE_EVERY - 1) // PROFILE_EVERY} of {args.steps}, run eagerly), on the launching stream",
             "graph": (f"the other {replays} timed steps replay one captured CUDA graph of the step ({per_step_launches} launches)"

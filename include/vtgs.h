@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define VTGS_ABI_VERSION 2
+#define VTGS_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define VTGS_API __attribute__((visibility("default")))
@@ -97,11 +97,13 @@ VTGS_API const char *vtgs_last_error(const vtgs_ctx *ctx);
  *   opacity_init [K×H×W] or NULL (then every valid slot gets opacity_default);
  *   out pos_rad float4[K·H·W] = (R_k·X_c + t_k, d / f_mean), X_c = ((x−cx)d/fx, (y−cy)d/fy, d);
  *   out col_opa float4[K·H·W] = (rgb, opacity).  Invalid slots are written as all zeros.
- *   H, W = intr.height, intr.width.  N = K·H·W must be ≤ max_gaussians. */
+ *   n_valid: device int64 or NULL, OVERWRITTEN with the number of valid slots (SPEC.md:440
+ *   "count = valid pixels").
+ *   H, W = intr.height, intr.width.  N = K·H·W > max_gaussians → VTGS_ERR_CAPACITY. */
 VTGS_API vtgs_status vtgs_instantiate(vtgs_ctx *ctx, const float *depth, const float *rgb,
                              const vtgs_pose *kf_poses, int32_t K, vtgs_intrinsics intr,
                              const float *opacity_init, float opacity_default, float *pos_rad,
-                             float *col_opa, void *stream);
+                             float *col_opa, int64_t *n_valid, void *stream);
 
 /* Densification on a regular frame — PAPER.md:192 ("complement Gaussians at pixels uncovered by
  * the current Gaussians' renderings"), PAPER.md:261 ("0.5 as a mask threshold to determine if
@@ -160,6 +162,7 @@ VTGS_API vtgs_status vtgs_visibility_counts(vtgs_ctx *ctx, const float *depth, c
  *   view: DEVICE pointer to one vtgs_pose (so a graph-captured loop can update it in place);
  *   the forward copies it on the device, so it may be reused as soon as the call is enqueued.
  *   out color [H×W×3], depth [H×W] (Σ αT z, unnormalised), silhouette [H×W] (Σ αT).
+ * N > max_gaussians → VTGS_ERR_CAPACITY; N < 0 → VTGS_ERR_SHAPE.
  * The context remembers pos_rad, col_opa and the three output pointers: they must stay valid
  * and unmodified until the matching vtgs_render_bwd. */
 VTGS_API vtgs_status vtgs_render_fwd(vtgs_ctx *ctx, const float *pos_rad, const float *col_opa, int64_t N,
@@ -200,7 +203,7 @@ VTGS_API vtgs_status vtgs_ssim_loss(vtgs_ctx *ctx, const float *color, const flo
                            int32_t height, float tau, float *d_color, float *loss_out, void *stream);
 
 enum { VTGS_GRAD_COLOR = 1, VTGS_GRAD_OPACITY = 2, VTGS_GRAD_RADIUS = 4, VTGS_GRAD_POSE = 8,
-       VTGS_GRAD_POSITION = 16 };
+       VTGS_GRAD_POSITION = 16, VTGS_GRAD_DETERMINISTIC = 32 };
 
 /* (5) Backward of the LAST vtgs_render_fwd on this context — SPEC.md:197-205 (chain through
  * the α/T recurrence, the footprint σ = f·r/z, the projection), SPEC.md:223 (pose gradient on
@@ -218,7 +221,11 @@ enum { VTGS_GRAD_COLOR = 1, VTGS_GRAD_OPACITY = 2, VTGS_GRAD_RADIUS = 4, VTGS_GR
  *   d_pose [7] (dq_w, dq_x, dq_y, dq_z, dt_x, dt_y, dt_z) is OVERWRITTEN (NULL if not wanted).
  *   loss_out: device float, OVERWRITTEN with the loss value (NULL = not needed; requires loss).
  * Attribute gradients are summed with float atomics across tiles: run-to-run results can
- * differ in the last bits.  The pose gradient is reduced in a fixed order. */
+ * differ in the last bits — unless want has VTGS_GRAD_DETERMINISTIC: then the
+ * per-(Gaussian, sub-tile) partials are summed as int64 fixed point (2⁻⁴⁰ resolution, |sum| <
+ * 8.4e6), independent of arrival order, and added to d_col_opa / d_radius by one more pass
+ * ("privatized buffers merged deterministically"; the context allocates 40 B per
+ * Gaussian on first use).  The pose gradient is always reduced in a fixed order. */
 VTGS_API vtgs_status vtgs_render_bwd(vtgs_ctx *ctx, const float *dL_dcolor, const float *dL_ddepth,
                             const float *dL_dsil, const vtgs_l1_loss *loss, uint32_t want,
                             int64_t learn_begin, int64_t learn_end, float *d_col_opa,
@@ -273,6 +280,12 @@ VTGS_API vtgs_status vtgs_set_profiling(vtgs_ctx *ctx, int32_t enable);
  * profiling was off are not counted) per stage since the previous call; resets. */
 VTGS_API vtgs_status vtgs_get_profile(vtgs_ctx *ctx, double *ms, int64_t *counts, void *stream);
 
+/* Measurement hook (not on the path): the FP32 FMA peak (TFLOP/s, an FMA = 2 flops) and the
+ * MUFU ex2.approx throughput (ops/s) of `device`, measured by two microbenchmark kernels (every
+ * SM, 64 warps, 8 independent chains per thread; best of 4) — the roofline denominators of the
+ * ALU-bound compositing kernels.  Synchronous. */
+VTGS_API vtgs_status vtgs_measure_peaks(int32_t device, double *fp32_tflops, double *ex2_per_s);
+
 /* Synchronise `stream` and report a deferred device-side error (VTGS_ERR_CAPACITY) or a CUDA
  * error.  Synchronous. */
 VTGS_API vtgs_status vtgs_check(vtgs_ctx *ctx, void *stream);
@@ -290,7 +303,10 @@ VTGS_API vtgs_status vtgs_export_tiles(vtgs_ctx *ctx, int64_t *tile_start, int32
  * col_opa / d_col_opa / d_radius / color / depth / silhouette are DEVICE buffers (the model
  * state and the outputs stay resident).  The targets upload on a context-owned second stream
  * while projection, sort and forward run (the backward waits for them); host buffers should be
- * pinned for the copy to be asynchronous.  Synchronous (returns after the loss is on the host). */
+ * pinned for the copy to be asynchronous.  Synchronous (returns after the loss is on the host).
+ * The 5N attribute gradients (and the images) stay on the device: only the loss (4 B) and, with
+ * VTGS_GRAD_POSE, the 7 pose gradients come back.  A forward whose tile pairs exceeded the
+ * context's capacity returns VTGS_ERR_CAPACITY here (render and gradients empty). */
 VTGS_API vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col_opa, int64_t N,
                            const vtgs_pose *view_host, vtgs_intrinsics intr,
                            const float *target_rgb_host, const float *target_depth_host,

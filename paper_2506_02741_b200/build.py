@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["instantiate.cu", "forward.cu", "composite_fwd.cu", "backward.cu", "ssim.cu", "abi.cu"]
+SOURCES = ["instantiate.cu", "forward.cu", "composite_fwd.cu", "backward.cu", "ssim.cu", "abi.cu", "peaks.cu"]
 HEADERS = ["vtgs_internal.cuh", "composite_common.cuh"]
 LIB = os.path.join(HERE, "libvtgs.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -51,7 +51,7 @@ cudaError_t dalloc(T **p, size_t n) {
 
 void free_all(Ctx &c) {
     void *ptrs[] = {c.proj, c.rect, c.thr, c.tile_count, c.tile_start, c.tile_cursor, c.tile_flag, c.keys, c.vals, c.pbits, c.keys2,
-                    c.vals2, c.offs, c.sub_lists, c.sub_masks, c.chunk_list, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy, c.ssim_abc, c.ssim_partials};
+                    c.vals2, c.offs, c.sub_lists, c.sub_masks, c.chunk_list, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy, c.ssim_abc, c.ssim_partials, c.det};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -169,7 +169,7 @@ vtgs_status vtgs_destroy(vtgs_ctx *ctx) {
 vtgs_status vtgs_instantiate(vtgs_ctx *ctx, const float *depth, const float *rgb,
                              const vtgs_pose *kf_poses, int32_t K, vtgs_intrinsics intr,
                              const float *opacity_init, float opacity_default, float *pos_rad,
-                             float *col_opa, void *stream) {
+                             float *col_opa, int64_t *n_valid, void *stream) {
     if (!ctx) return VTGS_ERR_INVALID_ARG;
     ctx->c.last_error[0] = 0;
     vtgs_status st = check_intr(ctx, intr);
@@ -177,16 +177,23 @@ vtgs_status vtgs_instantiate(vtgs_ctx *ctx, const float *depth, const float *rgb
     if (K < 0) return fail(ctx, VTGS_ERR_SHAPE, "K = %d < 0", K);
     const int64_t N = (int64_t)K * intr.width * intr.height;
     if (N > ctx->c.max_gaussians)
-        return fail(ctx, VTGS_ERR_SHAPE, "K·H·W = %lld exceeds max_gaussians %lld", (long long)N,
+        return fail(ctx, VTGS_ERR_CAPACITY, "K·H·W = %lld exceeds max_gaussians %lld", (long long)N,
                     (long long)ctx->c.max_gaussians);
-    if (K == 0) return VTGS_OK;
+    if (K == 0) {
+        if (n_valid) {
+            cudaSetDevice(ctx->c.device);
+            cudaError_t e = cudaMemsetAsync(n_valid, 0, sizeof(int64_t), (cudaStream_t)stream);
+            if (e) return cuda_fail(ctx, e, "vtgs_instantiate");
+        }
+        return VTGS_OK;
+    }
     if (!depth || !rgb || !kf_poses || !pos_rad || !col_opa)
         return fail(ctx, VTGS_ERR_INVALID_ARG, "NULL depth / rgb / kf_poses / pos_rad / col_opa");
     if (!aligned16(pos_rad) || !aligned16(col_opa))
         return fail(ctx, VTGS_ERR_INVALID_ARG, "pos_rad / col_opa must be 16-byte aligned float4 arrays");
     cudaSetDevice(ctx->c.device);
     cudaError_t e = vtgs::launch_instantiate(ctx->c, depth, rgb, kf_poses, K, intr, opacity_init, opacity_default,
-                                             (float4 *)pos_rad, (float4 *)col_opa, (cudaStream_t)stream);
+                                             (float4 *)pos_rad, (float4 *)col_opa, n_valid, (cudaStream_t)stream);
     return e ? cuda_fail(ctx, e, "vtgs_instantiate") : VTGS_OK;
 }
 
@@ -198,8 +205,9 @@ vtgs_status vtgs_render_fwd(vtgs_ctx *ctx, const float *pos_rad, const float *co
     c.last_error[0] = 0;
     vtgs_status st = check_intr(ctx, intr);
     if (st) return st;
-    if (N < 0 || N > c.max_gaussians)
-        return fail(ctx, VTGS_ERR_SHAPE, "N = %lld outside 0..max_gaussians %lld", (long long)N,
+    if (N < 0) return fail(ctx, VTGS_ERR_SHAPE, "N = %lld < 0", (long long)N);
+    if (N > c.max_gaussians)
+        return fail(ctx, VTGS_ERR_CAPACITY, "N = %lld exceeds max_gaussians %lld", (long long)N,
                     (long long)c.max_gaussians);
     if ((N > 0 && (!pos_rad || !col_opa)) || !view || !color || !depth || !silhouette)
         return fail(ctx, VTGS_ERR_INVALID_ARG, "NULL state / view / output pointer");
@@ -230,7 +238,7 @@ vtgs_status vtgs_render_bwd(vtgs_ctx *ctx, const float *dL_dcolor, const float *
     Ctx &c = ctx->c;
     c.last_error[0] = 0;
     if (!c.have_fwd) return fail(ctx, VTGS_ERR_STATE, "vtgs_render_bwd before any vtgs_render_fwd");
-    if (want & ~0x1fu) return fail(ctx, VTGS_ERR_INVALID_ARG, "unknown bits in want = 0x%x", want);
+    if (want & ~0x3fu) return fail(ctx, VTGS_ERR_INVALID_ARG, "unknown bits in want = 0x%x", want);
     if (loss && (dL_dcolor || dL_ddepth || dL_dsil))
         return fail(ctx, VTGS_ERR_INVALID_ARG, "pass either upstream gradients or a fused loss, not both");
     if (loss && (!loss->target_rgb || !loss->target_depth))
@@ -494,8 +502,14 @@ vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col
     e = cudaMemcpyAsync(loss_host, d_loss, sizeof(float), cudaMemcpyDeviceToHost, s);
     if (!e && d_pose_host && (want & VTGS_GRAD_POSE))
         e = cudaMemcpyAsync(d_pose_host, d_dpose, sizeof(float) * 7, cudaMemcpyDeviceToHost, s);
+    unsigned int overflow = 0;   // the forward's device-side capacity flag, read with the loss
+    if (!e) e = cudaMemcpyAsync(&overflow, &c.dev->overflow, sizeof(unsigned int), cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaStreamSynchronize(s);
-    return e ? cuda_fail(ctx, e, "vtgs_step_host (D2H)") : VTGS_OK;
+    if (e) return cuda_fail(ctx, e, "vtgs_step_host (D2H)");
+    if (overflow)
+        return fail(ctx, VTGS_ERR_CAPACITY, "tile pairs exceeded max_pairs %lld (render and gradients empty)",
+                    (long long)c.max_pairs);
+    return VTGS_OK;
 }
 
 }  // extern "C"

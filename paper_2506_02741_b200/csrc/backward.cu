@@ -47,7 +47,17 @@ struct BwdArgs {
     float *d_radius;
     float4 *d_position;
     double *partials;
+    unsigned long long *det;   // VTGS_GRAD_DETERMINISTIC: int64 fixed-point accumulators [N][5], else NULL
 };
+
+// Deterministic attribute-gradient merge ("merged deterministically"): the
+// per-(Gaussian, sub-tile) partials are rounded to int64 multiples of 2⁻⁴⁰ and summed with
+// integer atomics — integer addition is associative, so the sum is the same whatever order the
+// warps arrive in — then k_det_finalize adds them (as fp32) to the caller's buffers.
+constexpr double kDetScale = 1099511627776.0;   // 2^40: resolution 9.1e-13, range ±8.4e6
+__device__ __forceinline__ void det_add(unsigned long long *q, float v) {
+    if (v != 0.f) atomicAdd(q, (unsigned long long)__double2ll_rn((double)v * kDetScale));
+}
 
 __device__ __forceinline__ float sgnf(float r) { return (float)((r > 0.0f) - (r < 0.0f)); }
 
@@ -286,11 +296,18 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             const float dsg = B.w * sw2 * inv_s2 * rcp_approx(s);
             if (ATTR && (int64_t)cur.g >= p.learn_begin && (int64_t)cur.g < p.learn_end) {
                 const bool wc = p.want & VTGS_GRAD_COLOR, wo = p.want & VTGS_GRAD_OPACITY;
-                if ((wc && (dc0 != 0.f || dc1 != 0.f || dc2 != 0.f)) || (wo && dop != 0.f))
-                    atomicAdd(&p.d_col_opa[cur.g],
-                              make_float4(wc ? dc0 : 0.f, wc ? dc1 : 0.f, wc ? dc2 : 0.f, wo ? dop : 0.f));
-                if ((p.want & VTGS_GRAD_RADIUS) && cur.pr.w > 0.f && dsg != 0.f)
-                    atomicAdd(&p.d_radius[cur.g], dsg * fmean * rcp_approx(z));  // ∂σ/∂r = f/z
+                const float dr = ((p.want & VTGS_GRAD_RADIUS) && cur.pr.w > 0.f) ? dsg * fmean * rcp_approx(z) : 0.f;
+                if (p.det) {   // deterministic merge: fixed-point integer atomics
+                    unsigned long long *q = p.det + (size_t)5 * cur.g;
+                    if (wc) { det_add(q, dc0); det_add(q + 1, dc1); det_add(q + 2, dc2); }
+                    if (wo) det_add(q + 3, dop);
+                    det_add(q + 4, dr);
+                } else {
+                    if ((wc && (dc0 != 0.f || dc1 != 0.f || dc2 != 0.f)) || (wo && dop != 0.f))
+                        atomicAdd(&p.d_col_opa[cur.g],
+                                  make_float4(wc ? dc0 : 0.f, wc ? dc1 : 0.f, wc ? dc2 : 0.f, wo ? dop : 0.f));
+                    if (dr != 0.f) atomicAdd(&p.d_radius[cur.g], dr);  // ∂σ/∂r = f/z
+                }
             }
             if (POSE) {
                 const float4 X = sX[wl_][lane];
@@ -678,6 +695,31 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_finalize(const double *__
     }
 }
 
+// Deterministic merge, second half: fixed point → fp32, added (+=) to the caller's buffers in
+// Gaussian order; the accumulators are zeroed for the next call.
+__global__ void __launch_bounds__(256) k_det_finalize(unsigned long long *__restrict__ det, int64_t g0, int64_t g1,
+                                                      uint32_t want, float4 *__restrict__ d_col_opa,
+                                                      float *__restrict__ d_radius) {
+    for (int64_t g = g0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < g1; g += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long *q = det + (size_t)5 * g;   // 40-byte rows: 8-byte loads
+        const ulonglong2 a = make_ulonglong2(q[0], q[1]);
+        const ulonglong2 b = make_ulonglong2(q[2], q[3]);
+        const unsigned long long c = q[4];
+        if ((a.x | a.y | b.x | b.y | c) == 0ull) continue;
+        const double k = 1.0 / kDetScale;
+        if (want & (VTGS_GRAD_COLOR | VTGS_GRAD_OPACITY)) {
+            float4 d = d_col_opa[g];
+            d.x += (float)((double)(long long)a.x * k);
+            d.y += (float)((double)(long long)a.y * k);
+            d.z += (float)((double)(long long)b.x * k);
+            d.w += (float)((double)(long long)b.y * k);
+            d_col_opa[g] = d;
+        }
+        if (want & VTGS_GRAD_RADIUS) d_radius[g] += (float)((double)(long long)c * k);
+        q[0] = q[1] = q[2] = q[3] = q[4] = 0ull;
+    }
+}
+
 constexpr size_t kBwdDynSmem = sizeof(float2) * kBwdWarps * 32 * 32;
 
 static int pose_direct() {
@@ -744,6 +786,20 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
         }
     }
     const bool A = (want & (VTGS_GRAD_COLOR | VTGS_GRAD_OPACITY | VTGS_GRAD_RADIUS)) != 0;
+    const bool DET = A && (want & VTGS_GRAD_DETERMINISTIC) != 0;
+    if (DET) {   // the fixed-point accumulators (N×5 int64), allocated zeroed on first use
+        if (c.det_cap < c.N) {
+            if (c.det) cudaFree(c.det);
+            c.det = nullptr;
+            c.det_cap = 0;
+            if ((err = cudaMalloc((void **)&c.det, sizeof(unsigned long long) * 5 * (size_t)(c.N > 0 ? c.N : 1))))
+                return err;
+            if ((err = cudaMemsetAsync(c.det, 0, sizeof(unsigned long long) * 5 * (size_t)(c.N > 0 ? c.N : 1), s)))
+                return err;
+            c.det_cap = c.N;
+        }
+        a.det = c.det;
+    }
     const bool P = (want & VTGS_GRAD_POSE) != 0 && d_pose != nullptr;
     const bool X = (want & VTGS_GRAD_POSITION) != 0 && d_position != nullptr;   // same chain as the pose
     if (!X) a.want &= ~(uint32_t)VTGS_GRAD_POSITION;
@@ -771,6 +827,16 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     }
     }
     if ((err = cudaGetLastError())) return err;
+    if (DET) {
+        const int64_t g0 = learn_begin < 0 ? 0 : learn_begin, g1 = learn_end > c.N ? c.N : learn_end;
+        if (g1 > g0) {
+            LaunchScope ls(&c, kCompBwd, s);
+            int grid = (int)((g1 - g0 + 255) / 256);
+            if (grid > c.num_sms * 16) grid = c.num_sms * 16;
+            k_det_finalize<<<grid, 256, 0, s>>>(c.det, g0, g1, want, d_col_opa, d_radius);
+            if ((err = cudaGetLastError())) return err;
+        }
+    }
     if (P || (L && loss_out)) {
         LaunchScope ls(&c, kFinalize, s);
         const int rows = T * (8 / kBwdWarps);

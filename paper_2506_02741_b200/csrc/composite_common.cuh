@@ -97,42 +97,50 @@ __device__ __forceinline__ float exact_raw_alpha(float d2, float s2, float o) {
     return __fmul_rn(o, w);
 }
 
+__device__ __forceinline__ float f32_next(float x) { return __uint_as_float(__float_as_uint(x) + 1u); }   // x ≥ 0
+__device__ __forceinline__ float f32_prev(float x) { return __uint_as_float(__float_as_uint(x) - 1u); }   // x > 0
+
 // Largest fp32 d² in [0, cap] whose exact raw α passes (raw ≥ thr, or raw > thr when strict), −1
-// if d² = 0 already fails.  The predicate is non-increasing in d², so the answer is the boundary
-// next to the continuous estimate d² = 2 s2 ln(o/thr): a few exact evaluations walk to it.
+// if d² = 0 already fails.  Each step of raw(d²) = fl(o · RN₃₂(exp(x))), x = fl(fl(−0.5 d²)/s2),
+// is monotone, so the boundary is found stage by stage without evaluating exp:
+//   1. w_min = the smallest fp32 w with fl(o·w) passing (fp32 arithmetic, a step or two);
+//   2. RN₃₂(e^x) ≥ w_min ⇔ e^x > m, m = the midpoint between w_min and its predecessor (e^x is
+//      never exactly m for fp32 x ≠ 0), ⇔ x > L = ln m: x_min = the smallest fp32 above L
+//      (one fp64 log; its 1e-16 error matters only if L lies within 1e-16 of an fp32 number);
+//   3. the largest d² with fl(fl(−0.5 d²)/s2) ≥ x_min, walking from −2·s2·x_min with the
+//      oracle's own fp32 operations.
 static __device__ __noinline__ float alpha_threshold_d2(float s2, float o, float thr, bool strict, float cap) {
-    auto pass = [&](float d2) {
-        const float r = exact_raw_alpha(d2, s2, o);
+    auto ok_w = [&](float w) {
+        const float r = __fmul_rn(o, w);
         return strict ? r > thr : r >= thr;
     };
-    if (!pass(0.0f)) return -1.0f;
-    if (pass(cap)) return cap;
-    const double est = 2.0 * (double)s2 * log((double)o / (double)thr);
-    float d = (float)fmin(fmax(est, 0.0), (double)cap);
-    float lo, hi;   // pass(lo), !pass(hi)
-    if (pass(d)) {
-        lo = d;
-        hi = cap;
-        for (int i = 0; i < 8; ++i) {
-            const float n = __uint_as_float(__float_as_uint(lo) + 1u);
-            if (!pass(n)) return lo;
-            lo = n;
-        }
+    if (!ok_w(1.0f)) return -1.0f;                 // d² = 0: w = exp(0) = 1 exactly
+    float w = __fdiv_rn(thr, o);
+    if (!(w > 0.0f)) return cap;
+    if (ok_w(w)) {
+        for (int i = 0; i < 4 && w > 0.0f && ok_w(f32_prev(w)); ++i) w = f32_prev(w);
     } else {
-        hi = d;
-        lo = 0.0f;
-        for (int i = 0; i < 8; ++i) {
-            const float n = __uint_as_float(__float_as_uint(hi) - 1u);
-            if (pass(n)) return n;
-            hi = n;
-        }
+        for (int i = 0; i < 4 && !ok_w(w); ++i) w = f32_next(w);
     }
-    while (__float_as_uint(hi) - __float_as_uint(lo) > 1u) {   // far from the estimate: bisect the bits
-        const float m = __uint_as_float((__float_as_uint(lo) >> 1) + (__float_as_uint(hi) >> 1) +
-                                        (__float_as_uint(lo) & __float_as_uint(hi) & 1u));
-        if (pass(m)) lo = m; else hi = m;
+    if (w > 1.0f) return -1.0f;
+    auto xd = [&](float d) { return __fdiv_rn(__fmul_rn(-0.5f, d), s2); };
+    {   // fast accept: the whole 3σ disc passes when even the rim's w clears w_min by far more than
+        // the fast exp's error (the usual case: o ≳ 0.36 for the 1/255 floor) — no fp64 needed
+        const float wr = fast_exp2(__fmul_rn(xd(cap), kLog2e));
+        if (wr >= w * (1.0f + 1.0f / 65536.0f)) return cap;
     }
-    return lo;
+    const double m = 0.5 * ((double)f32_prev(w) + (double)w);
+    const double L = log(m);                       // x must exceed L (L < 0 since m < 1)
+    float xm = (float)L;                           // round to nearest, then the smallest fp32 > L
+    if ((double)xm <= L) xm = __uint_as_float(__float_as_uint(xm) - 1u);   // negative: −1 ulp moves up
+    if (xd(cap) >= xm) return cap;
+    float d = (float)fmin(fmax(-2.0 * (double)s2 * (double)xm, 0.0), (double)cap);
+    if (xd(d) >= xm) {
+        for (int i = 0; i < 64 && d < cap && xd(f32_next(d)) >= xm; ++i) d = f32_next(d);
+    } else {
+        for (int i = 0; i < 64 && d > 0.0f && xd(d) < xm; ++i) d = f32_prev(d);
+    }
+    return d;
 }
 
 // (D_c, D_clamp) of a Gaussian with σ² = s2 and opacity o: composited-eligible ⇔ d² ≤ D_c =

@@ -117,8 +117,11 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     unsigned cur = 0u, cw = 0u;
     int soff = 0;
     int lbase = 0;
-    auto flush = [&]() {   // store the lane's composited bits of batch b (before leaving it)
-        ring.cbits[soff + lane] = cw;   // (b = −1: slot 0's own column, still 0 — harmless)
+    // store the lane's composited bits of batch b (before leaving it).  Only when nonzero: after a
+    // pre-build flush (below) the slot of b may already hold batch b + R, whose column this lane
+    // must not touch — cw is 0 then.
+    auto flush = [&]() {
+        if (cw) ring.cbits[soff + lane] = cw;
         cw = 0u;
     };
     auto advance = [&]() {
@@ -169,8 +172,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
                 ne += (has && d2 <= s9) ? 1u : 0u;
                 nc += acc ? 1u : 0u;
             }
-            if (term) {
-                flush();
+            if (term) {   // the lane is inside batch b (its slot is live): store unconditionally
+                ring.cbits[soff + lane] = cw;
+                cw = 0u;
                 cur = 0u;
                 b = nb;
             }

@@ -14,12 +14,14 @@ __global__ void __launch_bounds__(256) k_instantiate(const float *__restrict__ d
                                                      const float *__restrict__ opacity,
                                                      float opacity_default,
                                                      float4 *__restrict__ pos_rad,
-                                                     float4 *__restrict__ col_opa) {
+                                                     float4 *__restrict__ col_opa,
+                                                     unsigned long long *__restrict__ n_valid) {
     const int k = blockIdx.y;  // keyframe
     __shared__ PoseR P;
     if (threadIdx.x == 0) pose_rotation(poses[k], P);
     __syncthreads();
     const float fmean = __fmul_rn(0.5f, __fadd_rn(in.fx, in.fy));
+    unsigned cnt = 0;
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < HW; p += gridDim.x * blockDim.x) {
         const int64_t g = (int64_t)k * HW + p;
         const float d = depth[g];
@@ -28,6 +30,7 @@ __global__ void __launch_bounds__(256) k_instantiate(const float *__restrict__ d
             col_opa[g] = make_float4(0.f, 0.f, 0.f, 0.f);
             continue;
         }
+        ++cnt;
         const int y = p / W, x = p - y * W;
         // X_c = ((x − cx)·d / fx, (y − cy)·d / fy, d)
         const float X0 = __fdiv_rn(__fmul_rn(__fsub_rn((float)x, in.cx), d), in.fx);
@@ -42,6 +45,10 @@ __global__ void __launch_bounds__(256) k_instantiate(const float *__restrict__ d
         pos_rad[g] = make_float4(Xw[0], Xw[1], Xw[2], __fdiv_rn(d, fmean));  // r = D / f
         const float o = opacity ? opacity[g] : opacity_default;
         col_opa[g] = make_float4(rgb[3 * g], rgb[3 * g + 1], rgb[3 * g + 2], o);
+    }
+    if (n_valid) {   // the valid-slot count: warp sums, one atomic per warp
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_valid, (unsigned long long)cnt);
     }
 }
 
@@ -278,15 +285,19 @@ cudaError_t launch_visibility(Ctx &c, const float *depth, const vtgs_pose *pose,
 
 cudaError_t launch_instantiate(Ctx &c, const float *depth, const float *rgb, const vtgs_pose *poses, int K,
                                vtgs_intrinsics intr, const float *opacity, float opacity_default,
-                               float4 *pos_rad, float4 *col_opa, cudaStream_t s) {
+                               float4 *pos_rad, float4 *col_opa, int64_t *n_valid, cudaStream_t s) {
     const int HW = intr.width * intr.height;
-    if (K <= 0 || HW <= 0) return cudaSuccess;
+    if (K <= 0 || HW <= 0) return n_valid ? cudaMemsetAsync(n_valid, 0, sizeof(int64_t), s) : cudaSuccess;
     int gx = (HW + 255) / 256;
     if (gx > 4096) gx = 4096;
     dim3 grid(gx, K);
     LaunchScope ls(&c, kInstantiate, s);
+    if (n_valid) {
+        cudaError_t e = cudaMemsetAsync(n_valid, 0, sizeof(int64_t), s);
+        if (e) return e;
+    }
     k_instantiate<<<grid, 256, 0, s>>>(depth, rgb, poses, HW, intr.width, intr, opacity, opacity_default,
-                                       pos_rad, col_opa);
+                                       pos_rad, col_opa, (unsigned long long *)n_valid);
     return cudaGetLastError();
 }
 

@@ -86,6 +86,8 @@ struct Ctx {
     cudaStream_t copy_stream = nullptr;  // step_host: target upload overlapped with the forward
     cudaEvent_t ev_ready = nullptr, ev_copied = nullptr;
     vtgs_pose *view_copy = nullptr;  // the forward's view pose, copied on the device for the backward
+    unsigned long long *det = nullptr;  // VTGS_GRAD_DETERMINISTIC fixed-point accumulators [det_cap][5]
+    int64_t det_cap = 0;
     // remembered forward
     bool have_fwd = false;
     const float4 *pos_rad = nullptr;
@@ -214,7 +216,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 // ------------------------------------------------------------------------------------------
 cudaError_t launch_instantiate(Ctx &c, const float *depth, const float *rgb, const vtgs_pose *poses, int K,
                                vtgs_intrinsics intr, const float *opacity, float opacity_default,
-                               float4 *pos_rad, float4 *col_opa, cudaStream_t s);
+                               float4 *pos_rad, float4 *col_opa, int64_t *n_valid, cudaStream_t s);
 cudaError_t launch_forward(Ctx &c, cudaStream_t s);
 cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const float *dS,
                             const vtgs_l1_loss *loss, uint32_t want, int64_t learn_begin,

@@ -81,8 +81,12 @@ class BatchedMapper:
         self.ssim_loss = torch.zeros(max(len(self.views), 1), device=dev)
         self.d_ssim = torch.zeros((H, W, 3), device=dev) if self.w_ssim > 0 else None
 
-    def step(self, allreduce: bool = True) -> GradBuffer:
-        """Zero the gradients, render + backprop every local view (accumulating), all-reduce."""
+    def step(self, allreduce: bool = True, check: Optional[bool] = None) -> GradBuffer:
+        """Zero the gradients, render + backprop every local view (accumulating), all-reduce.
+        `check` (default: on the first step) synchronises once and raises VtgsError if a view's
+        tile pairs exceeded the context's capacity (the render would silently be empty)."""
+        if check is None:
+            check = not getattr(self, "_checked", False)
         self.grads.zero_()
         for i, (v, t) in enumerate(zip(self.views, self.targets)):
             self.R.render_fwd(self.pos_rad, self.col_opa, v, self.intr, out=self.out)
@@ -94,6 +98,9 @@ class BatchedMapper:
                               loss=dict(target_rgb=t["rgb"], target_depth=t["depth"], w_color=self.w_color,
                                         w_depth=self.w_depth, extra_dcolor=self.d_ssim),
                               learn=self.learn, loss_out=self.loss[i:i + 1])
+        if check:
+            self.R.check()
+            self._checked = True
         if allreduce:
             allreduce_grads(self.grads, self.group)
         return self.grads

@@ -45,9 +45,10 @@ def section_visibility(renderer, depth: torch.Tensor, pose: torch.Tensor, kf_dep
 def track(renderer, pos_rad: torch.Tensor, col_opa: torch.Tensor, intr, rgb: torch.Tensor, depth: torch.Tensor,
           init_pose: torch.Tensor, iterations: int, lr_rot: float, lr_trans: float, w_color: float = 0.5,
           w_depth: float = 1.0, vis_mask: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None,
-          graph: bool = False) -> TrackResult:
+          graph: bool = False, check: bool = False) -> TrackResult:
     """Optimise the frame's 7 pose parameters against the frozen Gaussians (Eq. 1, mean form,
-    W_i = valid ∧ S > 0.99 ∧ vis).  Returns the final pose and the per-iteration losses."""
+    W_i = valid ∧ S > 0.99 ∧ vis).  Returns the final pose and the per-iteration losses.
+    `check` synchronises at the end and raises VtgsError on a tile-pair capacity overflow."""
     from . import vtgs
     dev = pos_rad.device
     H, W = intr.height, intr.width
@@ -78,6 +79,8 @@ def track(renderer, pos_rad: torch.Tensor, col_opa: torch.Tensor, intr, rgb: tor
     else:
         with torch.cuda.stream(s):
             body()
+    if check:   # one synchronisation: a capacity overflow would have emptied every render
+        renderer.check(stream=s)
     return TrackResult(pose, losses)
 
 
@@ -97,6 +100,8 @@ def pretrack_select(renderers: Sequence, sections: Sequence[dict], intr, rgb: to
         s.wait_stream(cur)
         results.append(track(R, sec["pos_rad"], sec["col_opa"], intr, rgb, depth, init_pose, iterations, lr_rot,
                              lr_trans, w_color, w_depth, sec.get("vis_mask"), stream=s))
+    for R, s in zip(renderers, streams):
+        R.check(stream=s)   # pretrack_select synchronises anyway: surface a capacity overflow
     for s in streams:
         cur.wait_stream(s)
     torch.cuda.synchronize(dev)

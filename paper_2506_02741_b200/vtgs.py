@@ -30,6 +30,7 @@ VTGS_ERR_CUDA = -4
 VTGS_ERR_STATE = -5
 VTGS_ERR_NO_DEVICE = -6
 VTGS_GRAD_COLOR, VTGS_GRAD_OPACITY, VTGS_GRAD_RADIUS, VTGS_GRAD_POSE, VTGS_GRAD_POSITION = 1, 2, 4, 8, 16
+VTGS_GRAD_DETERMINISTIC = 32
 VTGS_GRAD_ATTR = VTGS_GRAD_COLOR | VTGS_GRAD_OPACITY | VTGS_GRAD_RADIUS
 VTGS_GRAD_ALL = VTGS_GRAD_ATTR | VTGS_GRAD_POSE
 
@@ -59,11 +60,12 @@ _c = ctypes
 _P = ctypes.c_void_p
 _SIGS = {
     "vtgs_abi_version": (_c.c_int32, []),
+    "vtgs_measure_peaks": (_c.c_int32, [_c.c_int32, _P, _P]),
     "vtgs_create": (_c.c_int32, [_c.POINTER(_P), _c.c_int32, _c.c_int64, _c.c_int32, _c.c_int32, _c.c_int64]),
     "vtgs_destroy": (_c.c_int32, [_P]),
     "vtgs_status_string": (_c.c_char_p, [_c.c_int32]),
     "vtgs_last_error": (_c.c_char_p, [_P]),
-    "vtgs_instantiate": (_c.c_int32, [_P, _P, _P, _P, _c.c_int32, vtgs_intrinsics, _P, _c.c_float, _P, _P, _P]),
+    "vtgs_instantiate": (_c.c_int32, [_P, _P, _P, _P, _c.c_int32, vtgs_intrinsics, _P, _c.c_float, _P, _P, _P, _P]),
     "vtgs_render_fwd": (_c.c_int32, [_P, _P, _P, _c.c_int64, _P, vtgs_intrinsics, _P, _P, _P, _P]),
     "vtgs_render_bwd": (_c.c_int32, [_P, _P, _P, _P, _c.POINTER(vtgs_l1_loss), _c.c_uint32, _c.c_int64, _c.c_int64,
                                      _P, _P, _P, _P, _P, _P]),
@@ -152,14 +154,17 @@ class Renderer:
     # --- (1)
     def instantiate(self, depth: torch.Tensor, rgb: torch.Tensor, kf_poses: torch.Tensor, intr,
                     opacity: Optional[torch.Tensor] = None, opacity_default: float = 0.5,
-                    out=None, stream=None):
+                    out=None, stream=None, n_valid: Optional[torch.Tensor] = None):
+        """(1) view-tied Gaussians of K keyframes → (pos_rad, col_opa); `n_valid` (int64 [1] device,
+        optional) receives the valid-slot count."""
         K = depth.shape[0]
         N = K * intr.width * intr.height
         pos_rad, col_opa = out if out is not None else (
             torch.empty((N, 4), dtype=torch.float32, device=self.device),
             torch.empty((N, 4), dtype=torch.float32, device=self.device))
         _ok(vtgs_instantiate(self.ctx, _ptr(depth), _ptr(rgb), _ptr(kf_poses), K, intrinsics(intr), _ptr(opacity),
-                             float(opacity_default), _ptr(pos_rad), _ptr(col_opa), _stream(stream)), self.ctx)
+                             float(opacity_default), _ptr(pos_rad), _ptr(col_opa), _ptr(n_valid), _stream(stream)),
+            self.ctx)
         return pos_rad, col_opa
 
     # --- (2)-(4)
@@ -299,3 +304,10 @@ class Renderer:
                            int(learn[1]), _ptr(color), _ptr(depth), _ptr(sil), _ptr(d_col_opa), _ptr(d_radius),
                            ctypes.addressof(loss), _ptr(d_pose_host), _stream(stream)), self.ctx)
         return float(loss.value)
+
+
+def measure_peaks(device: int = 0):
+    """Measured FP32 FMA peak (TFLOP/s) and MUFU ex2 throughput (ops/s) of `device` (vtgs_measure_peaks)."""
+    f, x = ctypes.c_double(), ctypes.c_double()
+    _ok(vtgs_measure_peaks(int(device), ctypes.byref(f), ctypes.byref(x)), None)
+    return f.value, x.value

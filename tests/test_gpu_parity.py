@@ -56,12 +56,17 @@ def _render_gpu(vt, R, cfg, pos_rad, col_opa, view=None):
 # ------------------------------------------------------------------------------ (a1)
 @pytest.mark.parametrize("which", [1, 2, 3])
 def test_instantiate_bitexact(vt, which):
+    """(a1) bit-exact slots, and the valid-slot count n_valid equal to the oracle's."""
     cfg = cached_config(which)
     R = _renderer(vt, cfg)
-    pr, co = gpu_instantiate(R, cfg)
-    opr, oco = oracle_instantiate(cfg)
+    nv = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    pr, co = R.instantiate(torch.from_numpy(cfg.depth_stack()).cuda(), torch.from_numpy(cfg.rgb_stack()).cuda(),
+                           vt.pose_tensor(cfg.pose_stack(), "cuda"), cfg.intr, torch.from_numpy(cfg.opacity).cuda(),
+                           n_valid=nv)
+    opr, oco, on = oracle.instantiate(cfg.depth_stack(), cfg.rgb_stack(), cfg.pose_stack(), cfg.intr, cfg.opacity)
     assert np.array_equal(pr.cpu().numpy(), opr.astype(np.float32))
     assert np.array_equal(co.cpu().numpy(), oco.astype(np.float32))
+    assert int(nv.item()) == on
 
 
 # ------------------------------------------------------------------------------ (a2)/(a3)
@@ -339,6 +344,37 @@ def test_backward_parity_long_lists_full_size(vt, which):
     _check_grads(want, dco, drad, dpose, g, ref["tainted"], vt, allow=allow, name=f"long lists config {which}")
 
 
+@pytest.mark.parametrize("which", [1, 2])
+def test_deterministic_attribute_gradients(vt, which):
+    """VTGS_GRAD_DETERMINISTIC (fixed merge order): two runs give bit-identical
+    attribute gradients, they agree with the float-atomic path to fp32 summation noise, and they
+    pass the oracle's gradient bar (config 1 checked against the oracle)."""
+    cfg = cached_config(which)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    _render_gpu(vt, R, cfg, pr, co)
+    tg = cfg.targets[0]
+    L = dict(target_rgb=torch.from_numpy(tg.rgb).cuda(), target_depth=torch.from_numpy(tg.depth).cuda(),
+             **_loss_of(cfg))
+    det = vt.VTGS_GRAD_ATTR | vt.VTGS_GRAD_DETERMINISTIC
+    runs = [_run_bwd(vt, R, cfg, det, cfg.n_slots, loss=L) for _ in range(2)]
+    fl = _run_bwd(vt, R, cfg, vt.VTGS_GRAD_ATTR, cfg.n_slots, loss=L)
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+    for a, b in ((runs[0][0], fl[0]), (runs[0][1], fl[1])):
+        assert np.allclose(a, b, rtol=1e-4, atol=1e-6)
+    if which == 1:
+        opr, oco = oracle_instantiate(cfg)
+        v = _view(cfg)
+        img = oracle.render(opr, oco, v, cfg.intr)
+        Lo = _loss_of(cfg)
+        _, gC, gD, gS, _, flip = oracle.l1_upstream(img["color"], img["depth"], img["sil"], tg.rgb, tg.depth, None,
+                                                    Lo["w_color"], Lo["w_depth"], Lo["color_mask_mode"],
+                                                    Lo["depth_mask_mode"], 0, want_flip=True)
+        ref, g, allow = _oracle_grads(cfg, opr, oco, v, gC, gD, gS, flip=flip)
+        _check_grads(vt.VTGS_GRAD_ATTR, runs[0][0], runs[0][1], None, g, ref["tainted"], vt, allow=allow,
+                     name="deterministic merge config 1")
+
+
 def test_backward_learn_range_and_accumulate(vt):
     """Only gids in [learn_begin, learn_end) get attribute gradients; gradients
     accumulate (+=) across calls (multi-view mapping is a loop)."""
@@ -466,6 +502,15 @@ def test_edge_errors(vt):
     with pytest.raises(vt.VtgsError) as e:
         R.render_fwd(e4, e4, v, big)
     assert e.value.status == vt.VTGS_ERR_SHAPE
+    # more Gaussians than the context holds → VTGS_ERR_CAPACITY (instantiate and render)
+    with pytest.raises(vt.VtgsError) as e:
+        R.instantiate(torch.zeros((2, 48, 64), device="cuda"), torch.zeros((2, 48, 64, 3), device="cuda"),
+                      vt.pose_tensor(np.tile([1.0, 0, 0, 0, 0, 0, 0], (2, 1)), "cuda"), intr)
+    assert e.value.status == vt.VTGS_ERR_CAPACITY
+    e5 = torch.zeros((3073, 4), device="cuda")
+    with pytest.raises(vt.VtgsError) as e:
+        R.render_fwd(e5, e5, v, intr)
+    assert e.value.status == vt.VTGS_ERR_CAPACITY
     # capacity: 3,072 Gaussians need > 100 pairs → deferred VTGS_ERR_CAPACITY, empty render
     cfg = cached_config(1)
     pr, co = gpu_instantiate(R, cfg)
@@ -474,6 +519,15 @@ def test_edge_errors(vt):
         R.check()
     assert e.value.status == vt.VTGS_ERR_CAPACITY
     assert not S.any()
+    # the host-buffer step reports the same overflow instead of returning an empty render's loss
+    hr = torch.zeros((48, 64, 3)).pin_memory()
+    hd = torch.zeros((48, 64)).pin_memory()
+    dco = torch.zeros((3072, 4), device="cuda")
+    drad = torch.zeros(3072, device="cuda")
+    with pytest.raises(vt.VtgsError) as e:
+        R.step_host(pr, co, np.asarray(_view(cfg), dtype=np.float32), cfg.intr, hr, hd, 1.0, 1.0, 0, 0, 0,
+                    vt.VTGS_GRAD_ATTR, (0, 3072), (C, D, S), dco, drad)
+    assert e.value.status == vt.VTGS_ERR_CAPACITY
 
 
 def test_edge_max_image_size_and_all_layers(vt):
