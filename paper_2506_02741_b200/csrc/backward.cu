@@ -28,7 +28,7 @@ struct BwdArgs {
     const uint32_t *tile_start;
     const uint32_t *sub_lists;
     const uint32_t *sub_count;
-    const uint32_t *sub_masks;   // the forward's per-entry EXACT composited pixel masks
+    const uint32_t *sub_masks;   // the forward's per-entry candidate pixel masks (lane_mask within D_c)
     int W, H, ntx;
     const float *color, *depth, *sil, *T_final;
     const uint32_t *last;
@@ -135,9 +135,9 @@ constexpr int kBwdWarps = 2;
 
 template <bool ATTR, bool POSE, bool LOSS>
 __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
-    __shared__ float4 sA[kBwdWarps][32];             // u, v, 1/o, escale
+    __shared__ float4 sA[kBwdWarps][32];             // u, v, D_c, escale
     __shared__ float4 sB[kBwdWarps][32];             // c, z
-    __shared__ float2 sL[kBwdWarps][32];             // log2 o, D_clamp
+    __shared__ float4 sL[kBwdWarps][32];             // log2 o, D_clamp, 1/o
     __shared__ float4 sX[kBwdWarps][POSE ? 32 : 1];  // X_c and ±σ (−: σ clamped)
     __shared__ float4 sG[kBwdWarps][32];             // per pixel (g_C, g_D)
     // [kBwdWarps][32 entries][32 pixels]: phase 1 writes column = own lane (conflict-free per
@@ -200,43 +200,53 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
         if (jj < wmax) {   // wmax ≤ the sub-list length
             const float s = fabsf(cur.pr.w);
             s2j = __fmul_rn(s, s);
-            sA[wl_][lane] = make_float4(cur.pr.x, cur.pr.y, 1.0f / cur.co.w, exp_scale(s2j));
+            sA[wl_][lane] = make_float4(cur.pr.x, cur.pr.y, cur.th.x, exp_scale(s2j));
             sB[wl_][lane] = make_float4(cur.co.x, cur.co.y, cur.co.z, cur.pr.z);
-            sL[wl_][lane] = entry_lo(cur.co.w, cur.th.y);
+            const float2 lo = entry_lo(cur.co.w, cur.th.y);
+            sL[wl_][lane] = make_float4(lo.x, lo.y, 1.0f / cur.co.w, 0.f);
             if (POSE)   // camera-space centre from the projection (x = (u − cx)·z / fx, …)
                 sX[wl_][lane] = make_float4((cur.pr.x - p.in.cx) * cur.pr.z * rcp_approx(p.in.fx),
                                             (cur.pr.y - p.in.cy) * cur.pr.z * rcp_approx(p.in.fy), cur.pr.z, cur.pr.w);
-            mj = mcur & onmask;   // the forward's exact composited pixels with a nonzero upstream
+            mj = mcur & onmask;   // the forward's candidate pixels with a nonzero upstream
         }
         __syncwarp();
-        unsigned bits = transpose32(mj, lane);   // lane = pixel: the entries it composited
+        // candidates at positions ≥ the pixel's `last` were not composited: drop them from the
+        // lane's column (phase 1) and, through the transposed threshold masks, from each entry's
+        // pixel set (phase 2); the rest are re-decided exactly as the forward decided (d² ≤ D_c)
+        const int rem = (int)L - bb;
+        const unsigned alive = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+        unsigned bits = transpose32(mj, lane) & alive;
+        mj &= transpose32(alive, lane);
         // ---- phase 1: lane = pixel, back to front, two pairs per iteration: both pairs' loads,
         // α (the forward's exact bits), 1/(1−α) and f carry no loop state and are computed
         // together; the recursion (T, Fb, Tb) then runs over the two in order ----
-        auto stage_a = [&](int k, bool v, float &a, float &rc, float &wgt, float &fi, bool &aclamp) {
-            float4 A, B;
-            float2 lo;
-            if (v) {   // predicated loads: lanes without a pair add no shared-memory traffic
+        auto stage_a = [&](int k, bool v, float &a, float &rc, float &wgt, float &fi, bool &comp, bool &aclamp) {
+            float4 A, B, lo;
+            if (v) {   // predicated loads: lanes without a candidate add no shared-memory traffic
                 A = sA[wl_][k];
                 B = sB[wl_][k];
                 lo = sL[wl_][k];
             }
             const float d2 = pair_d2(pxf, pyf, A.x, A.y);
-            a = pair_alpha(d2, A.w, lo);   // the forward's α bits (same entry data, same thresholds)
+            comp = v && d2 <= A.z;         // the forward's exact decision (3σ and the α floor)
+            a = pair_alpha(d2, A.w, make_float2(lo.x, lo.y));   // the forward's α bits
             aclamp = d2 <= lo.y;
-            wgt = a * A.z;                 // w = α / o (unclamped)
+            wgt = a * lo.z;                // w = α / o (unclamped)
             rc = rcp_approx(1.0f - a);
             fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (B.w - rz);
         };
-        auto stage_b = [&](int k, bool aclamp, float a, float rc, float wgt, float fi) {
-            const float oma = 1.0f - a;
-            const float Ti = T * rc;
-            const float om = a * Ti;
-            // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
-            const float dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
-            Fb = a * fi + oma * Fb;
-            Tb = oma * Tb;
-            T = Ti;
+        auto stage_b = [&](int k, bool comp, bool aclamp, float a, float rc, float wgt, float fi) {
+            float om = 0.f, dAe = 0.f;
+            if (comp) {
+                const float oma = 1.0f - a;
+                const float Ti = T * rc;
+                om = a * Ti;
+                // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
+                dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
+                Fb = a * fi + oma * Fb;
+                Tb = oma * Tb;
+                T = Ti;
+            }
             M[k][lane] = make_float2(om, dAe);
         };
         while (bits) {
@@ -246,11 +256,11 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             const int k1 = (31 - __clz(bits)) & 31;
             if (v1) bits &= ~(1u << k1);
             float a0, rc0, w0, f0, a1, rc1, w1, f1;
-            bool cl0, cl1;
-            stage_a(k0, true, a0, rc0, w0, f0, cl0);
-            stage_a(k1, v1, a1, rc1, w1, f1, cl1);
-            stage_b(k0, cl0, a0, rc0, w0, f0);
-            if (v1) stage_b(k1, cl1, a1, rc1, w1, f1);
+            bool c0, cl0, c1, cl1;
+            stage_a(k0, true, a0, rc0, w0, f0, c0, cl0);
+            stage_a(k1, v1, a1, rc1, w1, f1, c1, cl1);
+            stage_b(k0, c0, cl0, a0, rc0, w0, f0);
+            if (v1) stage_b(k1, c1, cl1, a1, rc1, w1, f1);
         }
         __syncwarp();
         // ---- phase 2: lane = entry, over the pixels that composited it, two pixels per
@@ -261,6 +271,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
             float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, sw2 = 0.f, swx = 0.f, swy = 0.f, dzd = 0.f;
             unsigned mm = __funnelshift_r(mj, mj, lane);  // rotate right by lane
             auto accum = [&](int i, float2 md, float4 gp) {
+                if (md.x == 0.f) return;   // a candidate the pixel did not composite (ω > 0 otherwise)
                 dc0 = fmaf(gp.x, md.x, dc0);
                 dc1 = fmaf(gp.y, md.x, dc1);
                 dc2 = fmaf(gp.z, md.x, dc2);
@@ -357,9 +368,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
 // (Σ g, Σ X_c gᵀ): no per-Gaussian reduction, so the lanes walk back to front ACROSS batch
 // boundaries at their own pace over a ring of R resident batches, like the forward's ring
 // (k_composite_fwd_ring): a lane only waits when it needs a batch not yet built and the ring is
-// R batches ahead of the slowest lane.  The lane's candidates are the forward's EXACT composited
-// pairs (no compositing test is re-done).  Per entry the slot keeps A = (u, v, 1/o, escale),
-// B = (c, z), Xq = (X_c.x, X_c.y, log2 o, o/σ²) and (±1/z (−: σ clamped, ∂σ/∂z = 0), D_clamp); per pair
+// R batches ahead of the slowest lane.  The lane's candidates are the forward's
+// candidates, re-decided with the forward's exact thresholds (d² ≤ D_c, candidates before `last`).
+// Per entry the slot keeps A = (u, v, 1/o, escale), B = (c, z), Xq = (X_c.x, X_c.y, log2 o, o/σ²)
+// and (±1/z (−: σ clamped, ∂σ/∂z = 0), D_clamp, D_c); per pair
 //   q = (o/σ²)·dL/dα·w,  g = (q·dx·fx/z, q·dy·fy/z, g_D·ω − q·dx·(u−cx)/z − q·dy·(v−cy)/z − q·d²·[1/z])
 // ------------------------------------------------------------------------------------------
 template <int R>
@@ -367,7 +379,7 @@ struct PoseRing {
     float4 A[R * 32];        // u, v, 1/o, escale
     float4 B[R * 32];        // c, z
     float4 Xq[R * 32];       // X_c.x, X_c.y, log2 o, o/σ²
-    float2 iz[R * 32];       // ±1/z (−: σ clamped), D_clamp
+    float4 iz[R * 32];       // ±1/z (−: σ clamped), D_clamp, D_c
     uint32_t bits[R * 32];   // per lane: its composited entries of the batch (bit k = entry k)
 };
 
@@ -429,10 +441,13 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
             const float2 lo = entry_lo(e.co.w, e.th.y);
             ring.Xq[slot + lane] = make_float4((e.pr.x - cxp) * e.pr.z * ifx, (e.pr.y - cyp) * e.pr.z * ify, lo.x,
                                                e.co.w * rcp_approx(s2));
-            ring.iz[slot + lane] = make_float2(e.pr.w > 0.f ? iz : -iz, lo.y);
-            mj = mnx & onmask;   // the forward's exact composited pixels with a nonzero upstream
+            ring.iz[slot + lane] = make_float4(e.pr.w > 0.f ? iz : -iz, lo.y, e.th.x, 0.f);
+            mj = mnx & onmask;   // the forward's candidate pixels with a nonzero upstream
         }
-        ring.bits[slot + lane] = transpose32(mj, lane);
+        // positions ≥ the pixel's `last` were not composited
+        const int rem = L - bb;
+        const unsigned alive = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+        ring.bits[slot + lane] = transpose32(mj, lane) & alive;
         ++built;
         const int nidx = bb - 32 + (int)lane;
         stream_next(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, p.thr);
@@ -461,12 +476,13 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
                 A = ring.A[soff + k];
                 B = ring.B[soff + k];
             }
-            if (has) {   // every candidate is a composited pair
+            float4 izl;
+            if (has) izl = ring.iz[soff + k];
+            const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
+            const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
+            if (has && d2 <= izl.z) {   // composited: the forward's exact decision
                 const float4 Xq = ring.Xq[soff + k];
-                const float2 izl = ring.iz[soff + k];
                 const float izs = izl.x;
-                const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
-                const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
                 const float a = pair_alpha(d2, A.w, make_float2(Xq.z, izl.y));   // the forward's α bits
                 const bool aclamp = d2 <= izl.y;
                 const float wgt = a * A.z;   // w = α / o (unclamped)

@@ -124,11 +124,6 @@ static __device__ __noinline__ float alpha_threshold_d2(float s2, float o, float
     }
     if (w > 1.0f) return -1.0f;
     auto xd = [&](float d) { return __fdiv_rn(__fmul_rn(-0.5f, d), s2); };
-    {   // fast accept: the whole 3σ disc passes when even the rim's w clears w_min by far more than
-        // the fast exp's error (the usual case: o ≳ 0.36 for the 1/255 floor) — no fp64 needed
-        const float wr = fast_exp2(__fmul_rn(xd(cap), kLog2e));
-        if (wr >= w * (1.0f + 1.0f / 65536.0f)) return cap;
-    }
     const double m = 0.5 * ((double)f32_prev(w) + (double)w);
     const double L = log(m);                       // x must exceed L (L < 0 since m < 1)
     float xm = (float)L;                           // round to nearest, then the smallest fp32 > L
@@ -141,6 +136,25 @@ static __device__ __noinline__ float alpha_threshold_d2(float s2, float o, float
         for (int i = 0; i < 64 && d > 0.0f && xd(d) < xm; ++i) d = f32_prev(d);
     }
     return d;
+}
+
+// The common case without the search: o ≤ 0.999 (never clamped) and either o < 1/255 (nothing
+// passes: at d² = 0 the raw α is o itself) or the fast w at the disc's rim d² = 9σ² clears the
+// floor by 3e-5 — far more than the fast exp's ~1e-6 error — so the whole disc passes exactly.
+// Returns false when the exact search (alpha_thresholds) is needed.
+__device__ __forceinline__ bool alpha_thresholds_fast(float s2, float o, float2 &th) {
+    if (o > kAlphaMax) return false;
+    const float cap = __fmul_rn(9.0f, s2);
+    if (!(o >= kAlphaMin)) {
+        th = make_float2(-1.0f, -1.0f);
+        return true;
+    }
+    const float wr = fast_exp2(__fmul_rn(__fdiv_rn(__fmul_rn(-0.5f, cap), s2), kLog2e));
+    if (__fmul_rn(o, wr) >= kAlphaMin * (1.0f + 1.0f / 32768.0f)) {
+        th = make_float2(cap, -1.0f);
+        return true;
+    }
+    return false;
 }
 
 // (D_c, D_clamp) of a Gaussian with σ² = s2 and opacity o: composited-eligible ⇔ d² ≤ D_c =

@@ -16,7 +16,7 @@ struct FwdArgs {
     const uint32_t *tile_start;
     const uint32_t *sub_lists;
     const uint32_t *sub_count;
-    uint32_t *sub_masks;   // per sub-list entry: the EXACT set of its sub-tile's pixels that composited it
+    uint32_t *sub_masks;   // per sub-list entry: its candidate pixels (lane_mask within D_c), read by the backward
     int W, H, ntx;
     float *color, *depth, *sil, *T_final;
     uint32_t *last;
@@ -40,12 +40,11 @@ struct FwdRing {
     float4 B[R * 32];        // c_r, c_g, c_b, z
     float2 LO[R * 32];       // log2 o, D_clamp
     uint32_t bits[R * 32];   // per lane: its candidate entries of the batch (bit 31 − j = entry j)
-    uint32_t cbits[R * 32];  // per lane: the entries it composited (same orientation)
     float S9[STATS ? R * 32 : 1];   // 9σ² (the work counter's 3σ test)
 };
 
-template <int R, bool STATS>
-__global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p) {
+template <int R, bool STATS, int MINB>
+__global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(FwdArgs p) {
     extern __shared__ float4 fwd_smem[];
     static_assert((R & (R - 1)) == 0, "ring depth must be a power of two");
     const int wl = threadIdx.x >> 5;
@@ -70,20 +69,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     stream_start(st, list, (int)lane, 32 + (int)lane, cnt, p.proj, p.col_opa, p.thr);
     const EntryRegs &nxt = st.e;
     int built = 0;
-    // Exact composited masks (forward → backward): each lane ORs the entries it composites into
-    // its column word of the batch (ring.cbits, stored when it leaves the batch).  When a slot
-    // is rebuilt every lane has left its old batch; the 32 column words are bit-transposed so
-    // lane j holds entry j's pixel set, which is stored next to the sub-list.  The backward
-    // walks exactly these pairs and never re-decides a compositing test.
-    auto emit = [&](int t) {
-        const int slot = (t & (R - 1)) * 32;
-        const unsigned m = transpose32(__brev(ring.cbits[slot + lane]), lane);
-        if (t * 32 + (int)lane < cnt) mout[t * 32 + lane] = m;
-    };
     // build batch `built` from the prefetched registers, prefetch the one after it
     auto build = [&]() {
         const int slot = (built & (R - 1)) * 32;
-        if (built >= R) emit(built - R);
         const int idx = built * 32 + (int)lane;
         unsigned mj = 0u;
         if (idx < cnt) {
@@ -97,10 +85,10 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
             // candidates: the pixels within D_c (the work counters also want the whole 3σ disc)
             const unsigned m0 = lane_mask(make_float4(nxt.pr.x, nxt.pr.y, STATS ? s9 : nxt.th.x, 0.f),
                                           rect_from_proj(nxt.pr, p.W, p.H), sx, sy);
+            mout[idx] = m0;   // the backward walks the same candidates and re-takes the same exact decisions
             mj = m0 & inmask;
         }
         ring.bits[slot + lane] = __brev(transpose32(mj, lane));  // bit 31 − j = entry j
-        ring.cbits[slot + lane] = 0u;
         ++built;
         stream_next(st, list, (built + 1) * 32 + (int)lane, cnt, p.proj, p.col_opa, p.thr);
     };
@@ -111,21 +99,13 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
     uint32_t lastc = 0, ne = 0, nc = 0;
     // lane state: batch b, its remaining candidate bits cur (bit 31 − j = entry j, so the lowest
     // remaining entry is the highest set bit, one FLO), the address of the batch's entry 31,
-    // 1 + the sub-list position of its entry 31, and cw = the entries of batch b it composited.
+    // and 1 + the sub-list position of its entry 31.
     // Finished (terminated, walked the whole list, or outside the image) ⇔ cur == 0 && b + 1 ≥ nb.
     int b = inside ? -1 : nb;
-    unsigned cur = 0u, cw = 0u;
+    unsigned cur = 0u;
     int soff = 0;
     int lbase = 0;
-    // store the lane's composited bits of batch b (before leaving it).  Only when nonzero: after a
-    // pre-build flush (below) the slot of b may already hold batch b + R, whose column this lane
-    // must not touch — cw is 0 then.
-    auto flush = [&]() {
-        if (cw) ring.cbits[soff + lane] = cw;
-        cw = 0u;
-    };
     auto advance = [&]() {
-        flush();
         ++b;
         soff = (b & (R - 1)) * 32;
         cur = ring.bits[soff + lane];
@@ -139,8 +119,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
             if (cur == 0u && b + 1 < built) advance();
             const bool has = cur != 0u;
             const int hb = 31 - __clz(cur);                // highest set bit = lowest remaining entry
-            const unsigned bit = 1u << (hb & 31);
-            cur &= ~bit;
+            cur &= ~(1u << (hb & 31));
             const int k = soff + 31 - hb;                  // ring index of entry 31 − hb
             float4 A, Bc;                                  // unused unless `has` (comp includes it)
             float2 lo;
@@ -164,7 +143,6 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
                 Sl += om;
                 T = Tn;
                 lastc = (uint32_t)(lbase - hb);
-                cw |= bit;
             }
             if (STATS) {
                 float s9 = 0.f;
@@ -172,9 +150,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
                 ne += (has && d2 <= s9) ? 1u : 0u;
                 nc += acc ? 1u : 0u;
             }
-            if (term) {   // the lane is inside batch b (its slot is live): store unconditionally
-                ring.cbits[soff + lane] = cw;
-                cw = 0u;
+            if (term) {
                 cur = 0u;
                 b = nb;
             }
@@ -188,14 +164,11 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_composite_fwd_ring(FwdArgs p
             const int need = !live ? 0x7fffffff : (cur ? b : b + 1);  // earliest batch still needed
             const int lo = __reduce_min_sync(kFullMask, need);
             if (built < nb && built < lo + R) {
-                if (cur == 0u && b >= 0 && b < nb) flush();   // batch b is done for this lane: it may be emitted now
                 while (built < nb && built < lo + R) build();
                 __syncwarp();
             }
         }
     }
-    if (b >= 0 && b < nb) flush();
-    for (int t = built > R ? built - R : 0; t < built; ++t) emit(t);
     if (inside) {
         const int pix = py * p.W + px;
         p.color[3 * pix + 0] = C0;
@@ -224,24 +197,24 @@ static int fwd_variant() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("VTGS_FWD");
-        v = e ? atoi(e) : 4;    // ring depth 4 (default) or 8
+        v = e ? atoi(e) : 4;    // ring depth 4 (default) or 8; 14: R = 4 with 14 CTAs/SM (≤ 72 registers)
     }
     return v;
 }
 
-template <int R, bool STATS>
+template <int R, bool STATS, int MINB>
 static cudaError_t launch_ring_s(const FwdArgs &a, int T, cudaStream_t s) {
     const size_t sm = sizeof(FwdRing<R, STATS>) * kFwdWarps;
-    cudaError_t e =
-        cudaFuncSetAttribute(k_composite_fwd_ring<R, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(k_composite_fwd_ring<R, STATS, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
-    k_composite_fwd_ring<R, STATS><<<T * 8 / kFwdWarps, kFwdWarps * 32, sm, s>>>(a);
+    k_composite_fwd_ring<R, STATS, MINB><<<T * 8 / kFwdWarps, kFwdWarps * 32, sm, s>>>(a);
     return cudaGetLastError();
 }
 
-template <int R>
+template <int R, int MINB>
 static cudaError_t launch_ring(const FwdArgs &a, int T, bool stats, cudaStream_t s) {
-    return stats ? launch_ring_s<R, true>(a, T, s) : launch_ring_s<R, false>(a, T, s);
+    return stats ? launch_ring_s<R, true, MINB>(a, T, s) : launch_ring_s<R, false, MINB>(a, T, s);
 }
 
 cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
@@ -249,8 +222,11 @@ cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
     const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile;
     FwdArgs a{c.proj, c.thr, c.col_opa, c.tile_count, c.tile_start, c.sub_lists, c.sub_count, c.sub_masks, W, H, ntx,
               c.color, c.depth, c.sil, c.T_final, c.last, c.dev};
-    if (fwd_variant() == 8) return launch_ring<8>(a, ntx * nty, c.count_work, s);
-    return launch_ring<4>(a, ntx * nty, c.count_work, s);
+    switch (fwd_variant()) {
+        case 8: return launch_ring<8, 1>(a, ntx * nty, c.count_work, s);
+        case 14: return launch_ring<4, 14>(a, ntx * nty, c.count_work, s);
+        default: return launch_ring<4, 1>(a, ntx * nty, c.count_work, s);
+    }
 }
 
 }  // namespace vtgs

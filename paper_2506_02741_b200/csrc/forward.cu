@@ -63,6 +63,8 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
                                                        float4 *__restrict__ proj,
                                                        uint2 *__restrict__ rect,
                                                        float2 *__restrict__ thr,
+                                                       uint32_t *__restrict__ thr_list,
+                                                       DevScalars *__restrict__ dev,
                                                        uint32_t *__restrict__ tile_count) {
     __shared__ PoseR P;
     if (threadIdx.x == 0) pose_rotation(*view, P);
@@ -74,13 +76,24 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < Nr; g += stride) {
         Footprint f;
         f.vis = false;
+        bool slow = false;
         if (g < N) {
             f = project_one(pos_rad[g], P, in, fmean, Wm1, Hm1);
             proj[g] = f.vis ? make_float4(f.u, f.v, f.z, f.clamped ? -f.s : f.s) : make_float4(0.f, 0.f, 0.f, 0.f);
             rect[g] = f.vis ? make_uint2((uint32_t)f.x0 | ((uint32_t)f.x1 << 16), (uint32_t)f.y0 | ((uint32_t)f.y1 << 16))
                             : make_uint2(0xffffffffu, 0xffffffffu);
-            // exact α decision thresholds in d² (composite_common.cuh): once per Gaussian per view
-            thr[g] = f.vis ? alpha_thresholds(__fmul_rn(f.s, f.s), __ldg(&col_opa[g].w)) : make_float2(-1.f, -1.f);
+            // exact α decision thresholds in d² (composite_common.cuh), once per Gaussian per view:
+            // the common case here, the search for the rest on a dense work list (no divergence)
+            float2 th = make_float2(-1.f, -1.f);
+            slow = f.vis && !alpha_thresholds_fast(__fmul_rn(f.s, f.s), __ldg(&col_opa[g].w), th);
+            thr[g] = th;
+        }
+        const unsigned sm = __ballot_sync(kFull, slow);
+        if (sm) {   // warp-aggregated append to the threshold work list
+            uint32_t base = 0;
+            if (lane_id() == 0) base = atomicAdd(&dev->thr_count, (uint32_t)__popc(sm));
+            base = __shfl_sync(kFull, base, 0);
+            if (slow) thr_list[base + __popc(sm & lanemask_lt())] = (uint32_t)g;
         }
         const int tx0 = f.vis ? f.x0 >> 4 : 0, ty0 = f.vis ? f.y0 >> 4 : 0;
         const int ntg = f.vis ? (f.x1 >> 4) - tx0 + 1 : 0;
@@ -93,6 +106,21 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
             const unsigned peers = __match_any_sync(kFull, tile);
             if (tile >= 0 && (int)lane_id() == __ffs(peers) - 1) atomicAdd(&tile_count[tile], (uint32_t)__popc(peers));
         }
+    }
+}
+
+// The exact threshold search for the Gaussians k_project_count could not settle with its fast
+// test (a third or so: low opacity, or o > 0.999), one per thread, on a dense list.
+__global__ void __launch_bounds__(256) k_alpha_thresholds(const uint32_t *__restrict__ thr_list,
+                                                          const DevScalars *__restrict__ dev,
+                                                          const float4 *__restrict__ proj,
+                                                          const float4 *__restrict__ col_opa,
+                                                          float2 *__restrict__ thr) {
+    const uint32_t n = dev->thr_count;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t g = thr_list[i];
+        const float s = fabsf(proj[g].w);
+        thr[g] = alpha_thresholds(__fmul_rn(s, s), __ldg(&col_opa[g].w));
     }
 }
 
@@ -856,7 +884,10 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     if (N > 0) {
         LaunchScope ls(&c, kProject, s);
         k_project_count<<<gN, 256, 0, s>>>(c.pos_rad, c.col_opa, N, c.view, c.intr, ntx, c.proj, c.rect, c.thr,
-                                           c.tile_count);
+                                           c.thr_list, c.dev, c.tile_count);
+        if ((err = cudaGetLastError())) return err;
+        k_alpha_thresholds<<<c.num_sms * 8, 256, 0, s>>>(c.thr_list, c.dev, c.proj, c.col_opa, c.thr);
+        ++c.launches;
         if ((err = cudaGetLastError())) return err;
     }
     {
