@@ -50,7 +50,7 @@ cudaError_t dalloc(T **p, size_t n) {
 }
 
 void free_all(Ctx &c) {
-    void *ptrs[] = {c.proj, c.rect, c.thr, c.thr_list, c.tile_count, c.tile_start, c.tile_cursor, c.tile_flag, c.keys, c.vals, c.pbits, c.keys2,
+    void *ptrs[] = {c.proj, c.rect, c.thr, c.tile_count, c.tile_start, c.tile_cursor, c.tile_flag, c.keys, c.vals, c.pbits, c.keys2,
                     c.vals2, c.offs, c.sub_lists, c.sub_masks, c.chunk_list, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy, c.ssim_abc, c.ssim_partials, c.det};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -109,7 +109,6 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = dalloc(&c.proj, (size_t)max_gaussians);
     if (!e) e = dalloc(&c.rect, (size_t)max_gaussians);
     if (!e) e = dalloc(&c.thr, (size_t)max_gaussians);
-    if (!e) e = dalloc(&c.thr_list, (size_t)max_gaussians);
     if (!e) e = dalloc(&c.tile_count, (size_t)c.max_tiles);
     if (!e) e = dalloc(&c.tile_start, (size_t)c.max_tiles + 1);
     if (!e) e = dalloc(&c.tile_cursor, (size_t)c.max_tiles);

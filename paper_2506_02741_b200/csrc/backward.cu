@@ -133,8 +133,8 @@ __device__ __forceinline__ PixelUp pixel_upstream(const BwdArgs &p, int px, int 
 // One warp per 8×4 sub-tile, kBwdWarps warps per CTA, no block barriers.
 constexpr int kBwdWarps = 2;
 
-template <bool ATTR, bool POSE, bool LOSS>
-__global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd(BwdArgs p) {
+template <bool ATTR, bool POSE, bool LOSS, int MINB = 1>
+__global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs p) {
     __shared__ float4 sA[kBwdWarps][32];             // u, v, D_c, escale
     __shared__ float4 sB[kBwdWarps][32];             // c, z
     __shared__ float4 sL[kBwdWarps][32];             // log2 o, D_clamp, 1/o
@@ -747,15 +747,35 @@ static int pose_direct() {
     return v;
 }
 
+static int bwd_minb() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("VTGS_BWD_MINB");
+        v = e ? atoi(e) : 0;   // 12: the mapping backward held to 12 two-warp CTAs per SM (≤ 85 registers)
+    }
+    return v;
+}
+
 template <bool A, bool P, bool L>
 static void launch_bwd_t(const BwdArgs &a, int T, cudaStream_t s) {
+    if constexpr (A && !P) {
+        if (bwd_minb() == 12) {
+            k_composite_bwd<A, P, L, 12><<<T * (8 / kBwdWarps), kBwdWarps * 32, kBwdDynSmem, s>>>(a);
+            return;
+        }
+    }
     k_composite_bwd<A, P, L><<<T * (8 / kBwdWarps), kBwdWarps * 32, kBwdDynSmem, s>>>(a);
 }
 
 template <bool A, bool P, bool L>
 static cudaError_t set_bwd_attr() {
-    return cudaFuncSetAttribute(k_composite_bwd<A, P, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)kBwdDynSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_composite_bwd<A, P, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kBwdDynSmem);
+    if constexpr (A && !P) {
+        if (!e) e = cudaFuncSetAttribute(k_composite_bwd<A, P, L, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kBwdDynSmem);
+    }
+    return e;
 }
 
 cudaError_t backward_set_attributes() {

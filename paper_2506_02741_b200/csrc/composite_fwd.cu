@@ -38,7 +38,7 @@ template <int R, bool STATS>
 struct FwdRing {
     float4 A[R * 32];        // u, v, D_c, escale = −½log2(e)/σ²
     float4 B[R * 32];        // c_r, c_g, c_b, z
-    float2 LO[R * 32];       // log2 o, D_clamp
+    float LO[R * 32];        // log2 o
     uint32_t bits[R * 32];   // per lane: its candidate entries of the batch (bit 31 − j = entry j)
     float S9[STATS ? R * 32 : 1];   // 9σ² (the work counter's 3σ test)
 };
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
             const float s9 = __fmul_rn(9.0f, s2);
             ring.A[slot + lane] = make_float4(nxt.pr.x, nxt.pr.y, nxt.th.x, exp_scale(s2));
             ring.B[slot + lane] = make_float4(nxt.co.x, nxt.co.y, nxt.co.z, nxt.pr.z);
-            ring.LO[slot + lane] = entry_lo(nxt.co.w, nxt.th.y);
+            ring.LO[slot + lane] = entry_lo(nxt.co.w, 0.f).x;
             if (STATS) ring.S9[slot + lane] = s9;
             // candidates: the pixels within D_c (the work counters also want the whole 3σ disc)
             const unsigned m0 = lane_mask(make_float4(nxt.pr.x, nxt.pr.y, STATS ? s9 : nxt.th.x, 0.f),
@@ -122,15 +122,17 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
             cur &= ~(1u << (hb & 31));
             const int k = soff + 31 - hb;                  // ring index of entry 31 − hb
             float4 A, Bc;                                  // unused unless `has` (comp includes it)
-            float2 lo;
+            float l2o;
             if (has) {   // predicated loads: idle lanes add no shared-memory traffic
                 A = ring.A[k];
                 Bc = ring.B[k];
-                lo = ring.LO[k];
+                l2o = ring.LO[k];
             }
             const float d2 = pair_d2(pxf, pyf, A.x, A.y);
             const bool comp = has && d2 <= A.z;            // 3σ truncation and α floor, exact
-            const float a = pair_alpha(d2, A.w, lo);
+            // α value; the 0.999 clamp enters only as this cap here (the clamp DECISION, d² ≤ D_clamp,
+            // matters for the backward's ∂α/∂o and is taken there)
+            const float a = fminf(fast_exp2(fmaf(d2, A.w, l2o)), kAlphaMax);
             const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
             const bool term = comp && Tn < kTMin;
             const bool acc = comp && !term;
@@ -197,7 +199,8 @@ static int fwd_variant() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("VTGS_FWD");
-        v = e ? atoi(e) : 4;    // ring depth 4 (default) or 8; 14: R = 4 with 14 CTAs/SM (≤ 72 registers)
+        v = e ? atoi(e) : 14;   // 14 (default): R = 4 with 14 two-warp CTAs per SM (≤ 72 registers);
+                                // 4: R = 4 at the compiler's register count; 8: R = 8
     }
     return v;
 }
@@ -224,8 +227,8 @@ cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
               c.color, c.depth, c.sil, c.T_final, c.last, c.dev};
     switch (fwd_variant()) {
         case 8: return launch_ring<8, 1>(a, ntx * nty, c.count_work, s);
-        case 14: return launch_ring<4, 14>(a, ntx * nty, c.count_work, s);
-        default: return launch_ring<4, 1>(a, ntx * nty, c.count_work, s);
+        case 4: return launch_ring<4, 1>(a, ntx * nty, c.count_work, s);
+        default: return launch_ring<4, 14>(a, ntx * nty, c.count_work, s);
     }
 }
 

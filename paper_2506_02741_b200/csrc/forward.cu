@@ -63,8 +63,6 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
                                                        float4 *__restrict__ proj,
                                                        uint2 *__restrict__ rect,
                                                        float2 *__restrict__ thr,
-                                                       uint32_t *__restrict__ thr_list,
-                                                       DevScalars *__restrict__ dev,
                                                        uint32_t *__restrict__ tile_count) {
     __shared__ PoseR P;
     if (threadIdx.x == 0) pose_rotation(*view, P);
@@ -73,6 +71,10 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
     const float Wm1 = (float)(in.width - 1), Hm1 = (float)(in.height - 1);
     const int64_t Nr = (N + 31) & ~(int64_t)31;  // whole warps iterate together
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    __shared__ uint32_t qg[8][64];   // per warp: Gaussians waiting for the exact threshold search
+    __shared__ float qs[8][64];      // and their σ
+    const int wq = threadIdx.x >> 5;
+    int qn = 0;
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < Nr; g += stride) {
         Footprint f;
         f.vis = false;
@@ -88,12 +90,29 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
             slow = f.vis && !alpha_thresholds_fast(__fmul_rn(f.s, f.s), __ldg(&col_opa[g].w), th);
             thr[g] = th;
         }
+        // the Gaussians the fast test could not settle join the warp's queue; every 32 of them the
+        // whole warp runs the exact search, one per lane (no divergence, no global atomics)
         const unsigned sm = __ballot_sync(kFull, slow);
-        if (sm) {   // warp-aggregated append to the threshold work list
-            uint32_t base = 0;
-            if (lane_id() == 0) base = atomicAdd(&dev->thr_count, (uint32_t)__popc(sm));
-            base = __shfl_sync(kFull, base, 0);
-            if (slow) thr_list[base + __popc(sm & lanemask_lt())] = (uint32_t)g;
+        if (sm) {
+            if (slow) {
+                const int at = qn + __popc(sm & lanemask_lt());
+                qg[wq][at] = (uint32_t)g;
+                qs[wq][at] = f.s;
+            }
+            qn += __popc(sm);
+            __syncwarp();
+            if (qn >= 32) {
+                const uint32_t gq = qg[wq][lane_id()];
+                const float sq = qs[wq][lane_id()];
+                thr[gq] = alpha_thresholds(__fmul_rn(sq, sq), __ldg(&col_opa[gq].w));
+                __syncwarp();
+                qn -= 32;
+                if ((int)lane_id() < qn) {
+                    qg[wq][lane_id()] = qg[wq][32 + lane_id()];
+                    qs[wq][lane_id()] = qs[wq][32 + lane_id()];
+                }
+                __syncwarp();
+            }
         }
         const int tx0 = f.vis ? f.x0 >> 4 : 0, ty0 = f.vis ? f.y0 >> 4 : 0;
         const int ntg = f.vis ? (f.x1 >> 4) - tx0 + 1 : 0;
@@ -107,20 +126,10 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
             if (tile >= 0 && (int)lane_id() == __ffs(peers) - 1) atomicAdd(&tile_count[tile], (uint32_t)__popc(peers));
         }
     }
-}
-
-// The exact threshold search for the Gaussians k_project_count could not settle with its fast
-// test (a third or so: low opacity, or o > 0.999), one per thread, on a dense list.
-__global__ void __launch_bounds__(256) k_alpha_thresholds(const uint32_t *__restrict__ thr_list,
-                                                          const DevScalars *__restrict__ dev,
-                                                          const float4 *__restrict__ proj,
-                                                          const float4 *__restrict__ col_opa,
-                                                          float2 *__restrict__ thr) {
-    const uint32_t n = dev->thr_count;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t g = thr_list[i];
-        const float s = fabsf(proj[g].w);
-        thr[g] = alpha_thresholds(__fmul_rn(s, s), __ldg(&col_opa[g].w));
+    if ((int)lane_id() < qn) {   // the queue's remainder
+        const uint32_t gq = qg[wq][lane_id()];
+        const float sq = qs[wq][lane_id()];
+        thr[gq] = alpha_thresholds(__fmul_rn(sq, sq), __ldg(&col_opa[gq].w));
     }
 }
 
@@ -884,10 +893,7 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     if (N > 0) {
         LaunchScope ls(&c, kProject, s);
         k_project_count<<<gN, 256, 0, s>>>(c.pos_rad, c.col_opa, N, c.view, c.intr, ntx, c.proj, c.rect, c.thr,
-                                           c.thr_list, c.dev, c.tile_count);
-        if ((err = cudaGetLastError())) return err;
-        k_alpha_thresholds<<<c.num_sms * 8, 256, 0, s>>>(c.thr_list, c.dev, c.proj, c.col_opa, c.thr);
-        ++c.launches;
+                                           c.tile_count);
         if ((err = cudaGetLastError())) return err;
     }
     {

@@ -40,7 +40,6 @@ struct DevScalars {
     unsigned int radix_count; // entries in the radix-sort work list (Ctx::tile_flag)
     unsigned int chunk_count; // chunks of long tiles planned by plan_tile (Ctx::chunk_list)
     unsigned int chunk_next;  // their dynamic fetch cursor
-    unsigned int thr_count;   // Gaussians on the exact-threshold work list (Ctx::thr_list)
 };
 
 enum Stage { kProject = 0, kScan, kEmit, kSort, kCompFwd, kL1Count, kCompBwd, kFinalize, kInstantiate,
@@ -63,7 +62,6 @@ struct Ctx {
     float4 *proj = nullptr;          // (u, v, z, ±σ) per Gaussian, −σ ⇔ σ clamped
     uint2 *rect = nullptr;           // (x0 | x1<<16, y0 | y1<<16)
     float2 *thr = nullptr;           // (D_c, D_clamp): exact α decision thresholds in d² (composite_common.cuh)
-    uint32_t *thr_list = nullptr;    // Gaussians whose thresholds need the exact search [max_gaussians]
     uint32_t *tile_count = nullptr;  // [max_tiles]
     uint32_t *tile_start = nullptr;  // [max_tiles + 1]
     uint32_t *tile_cursor = nullptr; // [max_tiles]
