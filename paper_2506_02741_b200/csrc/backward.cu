@@ -137,7 +137,7 @@ template <bool ATTR, bool POSE, bool LOSS, int MINB = 1>
 __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs p) {
     __shared__ float4 sA[kBwdWarps][32];             // u, v, D_c, escale
     __shared__ float4 sB[kBwdWarps][32];             // c, z
-    __shared__ float4 sL[kBwdWarps][32];             // log2 o, D_clamp, 1/o
+    __shared__ float2 sL[kBwdWarps][32];             // log2 o, D_clamp
     __shared__ float4 sX[kBwdWarps][POSE ? 32 : 1];  // X_c and ±σ (−: σ clamped)
     __shared__ float4 sG[kBwdWarps][32];             // per pixel (g_C, g_D)
     // [kBwdWarps][32 entries][32 pixels]: phase 1 writes column = own lane (conflict-free per
@@ -202,8 +202,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
             s2j = __fmul_rn(s, s);
             sA[wl_][lane] = make_float4(cur.pr.x, cur.pr.y, cur.th.x, exp_scale(s2j));
             sB[wl_][lane] = make_float4(cur.co.x, cur.co.y, cur.co.z, cur.pr.z);
-            const float2 lo = entry_lo(cur.co.w, cur.th.y);
-            sL[wl_][lane] = make_float4(lo.x, lo.y, 1.0f / cur.co.w, 0.f);
+            sL[wl_][lane] = entry_lo(cur.co.w, cur.th.y);
             if (POSE)   // camera-space centre from the projection (x = (u − cx)·z / fx, …)
                 sX[wl_][lane] = make_float4((cur.pr.x - p.in.cx) * cur.pr.z * rcp_approx(p.in.fx),
                                             (cur.pr.y - p.in.cy) * cur.pr.z * rcp_approx(p.in.fy), cur.pr.z, cur.pr.w);
@@ -221,7 +220,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
         // α (the forward's exact bits), 1/(1−α) and f carry no loop state and are computed
         // together; the recursion (T, Fb, Tb) then runs over the two in order ----
         auto stage_a = [&](int k, bool v, float &a, float &rc, float &wgt, float &fi, bool &comp, bool &aclamp) {
-            float4 A, B, lo;
+            float4 A, B;
+            float2 lo;
             if (v) {   // predicated loads: lanes without a candidate add no shared-memory traffic
                 A = sA[wl_][k];
                 B = sB[wl_][k];
@@ -229,9 +229,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
             }
             const float d2 = pair_d2(pxf, pyf, A.x, A.y);
             comp = v && d2 <= A.z;         // the forward's exact decision (3σ and the α floor)
-            a = pair_alpha(d2, A.w, make_float2(lo.x, lo.y));   // the forward's α bits
+            a = pair_alpha(d2, A.w, lo);   // the forward's α (same entry data, same thresholds)
             aclamp = d2 <= lo.y;
-            wgt = a * lo.z;                // w = α / o (unclamped)
+            wgt = fast_exp2(d2 * A.w);     // w (∂α/∂o when unclamped)
             rc = rcp_approx(1.0f - a);
             fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (B.w - rz);
         };
