@@ -274,6 +274,14 @@ def measured_traffic(workload, kernel):
         return None
 
 
+def context_scratch_bytes(N, P, W, H):
+    """Device scratch a vtgs context allocates (csrc/abi.cu vtgs_create): per slot proj 16 + rect 8
+    + thresholds 8 B; per pair keys / values / fallback-sort scratch 21 B + 8 sub-lists and masks
+    64 B; per pixel T, last, SSIM factors, staging ≈ 60 B."""
+    tiles = ((W + 15) // 16) * ((H + 15) // 16)
+    return int(32 * N + 85 * P + 60 * W * H + 12 * 4 * (P // 2048 + tiles + 1) + 16 * 8 * 16 * tiles)
+
+
 def workload_config(cfg, args, n_views=1, views_per_rank=1):
     return {"workload": f"config{args.config}_{cfg.name}_{cfg.intr.width}x{cfg.intr.height}_K{cfg.K}",
             "n_gaussians": cfg.n_slots, "image": [cfg.intr.width, cfg.intr.height], "views_per_step": n_views,
@@ -427,7 +435,11 @@ def main():
     cfg = make_config(args.config, args.seed)
     W, H = cfg.intr.width, cfg.intr.height
     N = cfg.n_slots
-    R = vtgs.Renderer(local, N, W, H)
+    # config 5 (40 keyframes, 32.6M slots): one view needs ≤ 0.72 pairs per slot (23.5M), so the
+    # context holds N pairs — its scratch stays under 4 GB; the others take the default 2N
+    max_pairs = N + 262144 if args.config == 5 else 0
+    R = vtgs.Renderer(local, N, W, H, max_pairs=max_pairs)
+    scratch_bytes = context_scratch_bytes(N, max_pairs or 2 * N + 262144, W, H)
     # the section's Gaussians: every rank instantiates the same keyframes (no broadcast needed)
     pr, co = R.instantiate(torch.from_numpy(cfg.depth_stack()).to(dev), torch.from_numpy(cfg.rgb_stack()).to(dev),
                            vtgs.pose_tensor(cfg.pose_stack(), dev), cfg.intr, torch.from_numpy(cfg.opacity).to(dev))
@@ -688,6 +700,7 @@ def main():
             "graph": (f"the other {replays} timed steps replay one captured CUDA graph of the step ({per_step_launches} launches)"
                       if graph is not None else "eager"),
             "work": {"n_pairs": P, "e_eval": stats["e_eval"], "e_comp": stats["e_comp"], "max_tile": stats["max_tile"]},
+            "context_scratch_bytes": scratch_bytes,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,

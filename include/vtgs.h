@@ -78,8 +78,10 @@ VTGS_API int32_t vtgs_abi_version(void);
 
 /* Create a context on CUDA device `device`.  The context OWNS all scratch of the path, sized
  * for at most `max_gaussians` slots, images up to max_width × max_height (≤ 65535 each), and
- * `max_pairs` (Gaussian, tile) pairs per forward (0 ⇒ 4·max_gaussians).  One context serves
- * one in-flight forward/backward: use one per stream.  Synchronous. */
+ * `max_pairs` (Gaussian, tile) pairs per forward (0 ⇒ 2·max_gaussians + 262144; the five configs
+ * need ≤ 1.75 per slot).  Scratch ≈ 32 B per slot + 85 B per pair (the 8 per-tile sub-lists and
+ * their masks dominate).  One context serves one in-flight forward/backward: use one per stream.
+ * Synchronous. */
 VTGS_API vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, int32_t max_width,
                         int32_t max_height, int64_t max_pairs);
 /* Release the context and its scratch (synchronises the device first).  NULL is a no-op. */

@@ -90,7 +90,9 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
         return VTGS_ERR_NO_DEVICE;
     }
     if (device < 0 || device >= ndev) return VTGS_ERR_INVALID_ARG;
-    if (max_pairs <= 0) max_pairs = 4 * (max_gaussians > 0 ? max_gaussians : 1);
+    // default: 2 pairs per slot (+256k for small contexts) — the five configs measure P ≤ 1.75 N
+    // for one view (config 2: 7.0M of 4.08M slots); a view that needs more reports VTGS_ERR_CAPACITY
+    if (max_pairs <= 0) max_pairs = 2 * (max_gaussians > 0 ? max_gaussians : 1) + 262144;
     if (max_pairs > 0xfffffff0LL) max_pairs = 0xfffffff0LL;
     vtgs_ctx *ctx = new (std::nothrow) vtgs_ctx();
     if (!ctx) return VTGS_ERR_CUDA;

@@ -136,8 +136,8 @@ constexpr int kBwdWarps = 2;
 template <bool ATTR, bool POSE, bool LOSS, int MINB = 1>
 __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs p) {
     __shared__ float4 sA[kBwdWarps][32];             // u, v, D_c, escale
-    __shared__ float4 sB[kBwdWarps][32];             // c, z
-    __shared__ float2 sL[kBwdWarps][32];             // log2 o, D_clamp
+    __shared__ float4 sB[kBwdWarps][32];             // c, o
+    __shared__ float2 sL[kBwdWarps][32];             // z, D_clamp
     __shared__ float4 sX[kBwdWarps][POSE ? 32 : 1];  // X_c and ±σ (−: σ clamped)
     __shared__ float4 sG[kBwdWarps][32];             // per pixel (g_C, g_D)
     // [kBwdWarps][32 entries][32 pixels]: phase 1 writes column = own lane (conflict-free per
@@ -201,8 +201,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
             const float s = fabsf(cur.pr.w);
             s2j = __fmul_rn(s, s);
             sA[wl_][lane] = make_float4(cur.pr.x, cur.pr.y, cur.th.x, exp_scale(s2j));
-            sB[wl_][lane] = make_float4(cur.co.x, cur.co.y, cur.co.z, cur.pr.z);
-            sL[wl_][lane] = entry_lo(cur.co.w, cur.th.y);
+            sB[wl_][lane] = cur.co;
+            sL[wl_][lane] = make_float2(cur.pr.z, cur.th.y);
             if (POSE)   // camera-space centre from the projection (x = (u − cx)·z / fx, …)
                 sX[wl_][lane] = make_float4((cur.pr.x - p.in.cx) * cur.pr.z * rcp_approx(p.in.fx),
                                             (cur.pr.y - p.in.cy) * cur.pr.z * rcp_approx(p.in.fy), cur.pr.z, cur.pr.w);
@@ -229,11 +229,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
             }
             const float d2 = pair_d2(pxf, pyf, A.x, A.y);
             comp = v && d2 <= A.z;         // the forward's exact decision (3σ and the α floor)
-            a = pair_alpha(d2, A.w, lo);   // the forward's α (same entry data, same thresholds)
+            a = pair_alpha(d2, A.w, B.w, lo.y, wgt);   // the forward's α (same entry data, thresholds)
             aclamp = d2 <= lo.y;
-            wgt = fast_exp2(d2 * A.w);     // w (∂α/∂o when unclamped)
             rc = rcp_approx(1.0f - a);
-            fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (B.w - rz);
+            fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (lo.x - rz);
         };
         auto stage_b = [&](int k, bool comp, bool aclamp, float a, float rc, float wgt, float fi) {
             float om = 0.f, dAe = 0.f;
@@ -370,16 +369,16 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
 // (k_composite_fwd_ring): a lane only waits when it needs a batch not yet built and the ring is
 // R batches ahead of the slowest lane.  The lane's candidates are the forward's
 // candidates, re-decided with the forward's exact thresholds (d² ≤ D_c, candidates before `last`).
-// Per entry the slot keeps A = (u, v, 1/o, escale), B = (c, z), Xq = (X_c.x, X_c.y, log2 o, o/σ²)
-// and (±1/z (−: σ clamped, ∂σ/∂z = 0), D_clamp, D_c); per pair
+// Per entry the slot keeps A = (u, v, D_c, escale), B = (c, o), Xq = (X_c.x, X_c.y, z, o/σ²) and
+// (±1/z (−: σ clamped, ∂σ/∂z = 0), D_clamp); per pair
 //   q = (o/σ²)·dL/dα·w,  g = (q·dx·fx/z, q·dy·fy/z, g_D·ω − q·dx·(u−cx)/z − q·dy·(v−cy)/z − q·d²·[1/z])
 // ------------------------------------------------------------------------------------------
 template <int R>
 struct PoseRing {
-    float4 A[R * 32];        // u, v, 1/o, escale
-    float4 B[R * 32];        // c, z
-    float4 Xq[R * 32];       // X_c.x, X_c.y, log2 o, o/σ²
-    float4 iz[R * 32];       // ±1/z (−: σ clamped), D_clamp, D_c
+    float4 A[R * 32];        // u, v, D_c, escale
+    float4 B[R * 32];        // c, o
+    float4 Xq[R * 32];       // X_c.x, X_c.y, z, o/σ²
+    float2 iz[R * 32];       // ±1/z (−: σ clamped), D_clamp
     uint32_t bits[R * 32];   // per lane: its composited entries of the batch (bit k = entry k)
 };
 
@@ -434,14 +433,13 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
             const EntryRegs &e = st.e;
             const float s = fabsf(e.pr.w);
             const float s2 = __fmul_rn(s, s);
-            ring.A[slot + lane] = make_float4(e.pr.x, e.pr.y, 1.0f / e.co.w, exp_scale(s2));
-            ring.B[slot + lane] = make_float4(e.co.x, e.co.y, e.co.z, e.pr.z);
+            ring.A[slot + lane] = make_float4(e.pr.x, e.pr.y, e.th.x, exp_scale(s2));
+            ring.B[slot + lane] = e.co;
             // X_c from the projection itself (x = (u − cx)·z / fx, …): no gather of the world centre
             const float iz = rcp_approx(e.pr.z);
-            const float2 lo = entry_lo(e.co.w, e.th.y);
-            ring.Xq[slot + lane] = make_float4((e.pr.x - cxp) * e.pr.z * ifx, (e.pr.y - cyp) * e.pr.z * ify, lo.x,
+            ring.Xq[slot + lane] = make_float4((e.pr.x - cxp) * e.pr.z * ifx, (e.pr.y - cyp) * e.pr.z * ify, e.pr.z,
                                                e.co.w * rcp_approx(s2));
-            ring.iz[slot + lane] = make_float4(e.pr.w > 0.f ? iz : -iz, lo.y, e.th.x, 0.f);
+            ring.iz[slot + lane] = make_float2(e.pr.w > 0.f ? iz : -iz, e.th.y);
             mj = mnx & onmask;   // the forward's candidate pixels with a nonzero upstream
         }
         // positions ≥ the pixel's `last` were not composited
@@ -476,20 +474,19 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
                 A = ring.A[soff + k];
                 B = ring.B[soff + k];
             }
-            float4 izl;
-            if (has) izl = ring.iz[soff + k];
             const float dx = __fsub_rn(pxf, A.x), dy = __fsub_rn(pyf, A.y);
             const float d2 = __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
-            if (has && d2 <= izl.z) {   // composited: the forward's exact decision
+            if (has && d2 <= A.z) {   // composited: the forward's exact decision
                 const float4 Xq = ring.Xq[soff + k];
+                const float2 izl = ring.iz[soff + k];
                 const float izs = izl.x;
-                const float a = pair_alpha(d2, A.w, make_float2(Xq.z, izl.y));   // the forward's α bits
+                float wgt;
+                const float a = pair_alpha(d2, A.w, B.w, izl.y, wgt);   // the forward's α
                 const bool aclamp = d2 <= izl.y;
-                const float wgt = a * A.z;   // w = α / o (unclamped)
                 const float oma = 1.0f - a;
                 const float Ti = T * rcp_approx(oma);
                 const float om = a * Ti;
-                const float fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (B.w - rz);
+                const float fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (Xq.z - rz);
                 const float dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
                 Fb = a * fi + oma * Fb;
                 Tb = oma * Tb;
@@ -499,7 +496,7 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
                 const float du = q * dx, dv = q * dy;
                 const float gx = du * fx * iz, gy = dv * fy * iz;
                 const float gz = gD * om - (du * (A.x - cxp) + dv * (A.y - cyp)) * iz - q * d2 * kz;
-                const float X0 = Xq.x, X1 = Xq.y, X2 = B.w;
+                const float X0 = Xq.x, X1 = Xq.y, X2 = Xq.z;
                 h0 += gx; h1 += gy; h2 += gz;
                 K00 = fmaf(X0, gx, K00); K01 = fmaf(X0, gy, K01); K02 = fmaf(X0, gz, K02);
                 K10 = fmaf(X1, gx, K10); K11 = fmaf(X1, gy, K11); K12 = fmaf(X1, gz, K12);
@@ -751,7 +748,8 @@ static int bwd_minb() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("VTGS_BWD_MINB");
-        v = e ? atoi(e) : 0;   // 12: the mapping backward held to 12 two-warp CTAs per SM (≤ 85 registers)
+        v = e ? atoi(e) : 12;  // 12 (default): the mapping backward held to 12 two-warp CTAs per SM (80
+                               // registers; shared memory allows 11); 0: the compiler's choice (~107)
     }
     return v;
 }
@@ -767,13 +765,30 @@ static void launch_bwd_t(const BwdArgs &a, int T, cudaStream_t s) {
     k_composite_bwd<A, P, L><<<T * (8 / kBwdWarps), kBwdWarps * 32, kBwdDynSmem, s>>>(a);
 }
 
+// Shared memory is the occupancy limit of the two-phase backward (19.7 KB per two-warp CTA: 11
+// CTAs need the largest carve-out; the entry gathers hit L1 < 10 % of the time anyway).
+static int bwd_carveout() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("VTGS_BWD_CARVEOUT");
+        v = e ? atoi(e) : 100;   // percent of the unified L1 / shared storage given to shared memory
+    }
+    return v;
+}
+
 template <bool A, bool P, bool L>
 static cudaError_t set_bwd_attr() {
     cudaError_t e = cudaFuncSetAttribute(k_composite_bwd<A, P, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kBwdDynSmem);
+    if (!e && bwd_carveout() >= 0)
+        e = cudaFuncSetAttribute(k_composite_bwd<A, P, L>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 bwd_carveout());
     if constexpr (A && !P) {
         if (!e) e = cudaFuncSetAttribute(k_composite_bwd<A, P, L, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kBwdDynSmem);
+        if (!e && bwd_carveout() >= 0)
+            e = cudaFuncSetAttribute(k_composite_bwd<A, P, L, 12>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     bwd_carveout());
     }
     return e;
 }

@@ -168,19 +168,13 @@ __device__ __forceinline__ float2 alpha_thresholds(float s2, float o) {
 }
 
 // α VALUE of a pair (the decision d² ≤ D_c is the caller's): 0.999 when clamped (d² ≤ D_clamp),
-// else min(2^(d²·escale + log2 o), 0.999) with lo = (log2 o, D_clamp) kept per entry — o folded
-// into the exponent (one FFMA + one MUFU.EX2).  Relative error vs the oracle's o·w ≤ ~8e-7.
-// Every compositing kernel calls this on the same entry data, so forward and backward see the
-// same α bits.
-__device__ __forceinline__ float pair_alpha(float d2, float escale, float2 lo) {
-    return d2 <= lo.y ? kAlphaMax : fminf(fast_exp2(fmaf(d2, escale, lo.x)), kAlphaMax);
-}
-
-// per-entry (log2 o, D_clamp)
-__device__ __forceinline__ float2 entry_lo(float o, float dcl) {
-    float l;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(o));
-    return make_float2(l, dcl);
+// else min(o·w, 0.999) with the fast w = 2^(d²·escale) (relative error ≤ ~7e-7 against the
+// oracle's o·w).  The forward passes dcl = −1: its α value needs no clamp decision (an exact-vs-
+// fast difference at the clamp is a value difference of ~1e-6); the backward passes D_clamp, for
+// ∂α/∂o = 0 on clamped pairs.  w is returned for the backward's chain.
+__device__ __forceinline__ float pair_alpha(float d2, float escale, float o, float dcl, float &w) {
+    w = fast_exp2(d2 * escale);
+    return d2 <= dcl ? kAlphaMax : fminf(o * w, kAlphaMax);
 }
 
 // d² of pixel (xf, yf) to centre (u, v), DESIGN.md §3 step 7 (no FMA contraction)

@@ -37,8 +37,8 @@ constexpr int kInner = 6;                      // lane-independent steps between
 template <int R, bool STATS>
 struct FwdRing {
     float4 A[R * 32];        // u, v, D_c, escale = −½log2(e)/σ²
-    float4 B[R * 32];        // c_r, c_g, c_b, z
-    float LO[R * 32];        // log2 o
+    float4 B[R * 32];        // c_r, c_g, c_b, o
+    float Z[R * 32];         // z
     uint32_t bits[R * 32];   // per lane: its candidate entries of the batch (bit 31 − j = entry j)
     float S9[STATS ? R * 32 : 1];   // 9σ² (the work counter's 3σ test)
 };
@@ -79,8 +79,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
             const float s2 = __fmul_rn(s, s);
             const float s9 = __fmul_rn(9.0f, s2);
             ring.A[slot + lane] = make_float4(nxt.pr.x, nxt.pr.y, nxt.th.x, exp_scale(s2));
-            ring.B[slot + lane] = make_float4(nxt.co.x, nxt.co.y, nxt.co.z, nxt.pr.z);
-            ring.LO[slot + lane] = entry_lo(nxt.co.w, 0.f).x;
+            ring.B[slot + lane] = nxt.co;
+            ring.Z[slot + lane] = nxt.pr.z;
             if (STATS) ring.S9[slot + lane] = s9;
             // candidates: the pixels within D_c (the work counters also want the whole 3σ disc)
             const unsigned m0 = lane_mask(make_float4(nxt.pr.x, nxt.pr.y, STATS ? s9 : nxt.th.x, 0.f),
@@ -122,17 +122,16 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
             cur &= ~(1u << (hb & 31));
             const int k = soff + 31 - hb;                  // ring index of entry 31 − hb
             float4 A, Bc;                                  // unused unless `has` (comp includes it)
-            float l2o;
+            float zk;
             if (has) {   // predicated loads: idle lanes add no shared-memory traffic
                 A = ring.A[k];
                 Bc = ring.B[k];
-                l2o = ring.LO[k];
+                zk = ring.Z[k];
             }
             const float d2 = pair_d2(pxf, pyf, A.x, A.y);
             const bool comp = has && d2 <= A.z;            // 3σ truncation and α floor, exact
-            // α value; the 0.999 clamp enters only as this cap here (the clamp DECISION, d² ≤ D_clamp,
-            // matters for the backward's ∂α/∂o and is taken there)
-            const float a = fminf(fast_exp2(fmaf(d2, A.w, l2o)), kAlphaMax);
+            float w;
+            const float a = pair_alpha(d2, A.w, Bc.w, -1.0f, w);   // value only (clamp decision: backward)
             const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
             const bool term = comp && Tn < kTMin;
             const bool acc = comp && !term;
@@ -141,7 +140,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
                 C0 = fmaf(Bc.x, om, C0);
                 C1 = fmaf(Bc.y, om, C1);
                 C2 = fmaf(Bc.z, om, C2);
-                D = fmaf(Bc.w, om, D);
+                D = fmaf(zk, om, D);
                 Sl += om;
                 T = Tn;
                 lastc = (uint32_t)(lbase - hb);
