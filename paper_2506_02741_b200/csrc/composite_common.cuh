@@ -139,22 +139,16 @@ static __device__ __noinline__ float alpha_threshold_d2(float s2, float o, float
 }
 
 // The common case without the search: o ≤ 0.999 (never clamped) and either o < 1/255 (nothing
-// passes: at d² = 0 the raw α is o itself) or the fast w at the disc's rim d² = 9σ² clears the
-// floor by 3e-5 — far more than the fast exp's ~1e-6 error — so the whole disc passes exactly.
-// Returns false when the exact search (alpha_thresholds) is needed.
+// passes: at d² = 0 the raw α is o itself) or o ≥ kOpaFast: at the disc's rim d² = fl(9·s2) the
+// argument fl(fl(−0.5 d²)/s2) is −4.5 within 2 ulp, so w ≥ e^−4.5·(1 − 7e-7) there and
+// fl(o·w) ≥ 1/255 whenever o ≥ (1/255)·e^4.5·(1 + 1e-5) = 0.353012… — the whole disc passes.
+// Returns false when the exact search (alpha_thresholds) is needed (o in [1/255, 0.3530), or
+// o > 0.999).
+constexpr float kOpaFast = 0.35302f;   // ≥ (1/255)·e^4.5·(1 + 1e-5) = 0.3530119…
 __device__ __forceinline__ bool alpha_thresholds_fast(float s2, float o, float2 &th) {
-    if (o > kAlphaMax) return false;
-    const float cap = __fmul_rn(9.0f, s2);
-    if (!(o >= kAlphaMin)) {
-        th = make_float2(-1.0f, -1.0f);
-        return true;
-    }
-    const float wr = fast_exp2(__fmul_rn(__fdiv_rn(__fmul_rn(-0.5f, cap), s2), kLog2e));
-    if (__fmul_rn(o, wr) >= kAlphaMin * (1.0f + 1.0f / 32768.0f)) {
-        th = make_float2(cap, -1.0f);
-        return true;
-    }
-    return false;
+    if (o > kAlphaMax || (o >= kAlphaMin && o < kOpaFast)) return false;
+    th = make_float2(o >= kAlphaMin ? __fmul_rn(9.0f, s2) : -1.0f, -1.0f);
+    return true;
 }
 
 // (D_c, D_clamp) of a Gaussian with σ² = s2 and opacity o: composited-eligible ⇔ d² ≤ D_c =
