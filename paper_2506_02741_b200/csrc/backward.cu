@@ -21,7 +21,7 @@ constexpr unsigned kFull = kFullMask;
 
 struct BwdArgs {
     const float4 *proj;
-    const float2 *thr;            // per Gaussian (D_c, D_clamp), k_project_count
+    const float *thr;             // per Gaussian packed (D_c, D_clamp), k_project_count
     const float4 *col_opa;
     const float4 *pos_rad;
     const uint32_t *tile_count;
@@ -200,9 +200,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
         if (jj < wmax) {   // wmax ≤ the sub-list length
             const float s = fabsf(cur.pr.w);
             s2j = __fmul_rn(s, s);
-            sA[wl_][lane] = make_float4(cur.pr.x, cur.pr.y, cur.th.x, exp_scale(s2j));
+            const float2 th = thr_unpack(cur.th, s2j);
+            sA[wl_][lane] = make_float4(cur.pr.x, cur.pr.y, th.x, exp_scale(s2j));
             sB[wl_][lane] = cur.co;
-            sL[wl_][lane] = make_float2(cur.pr.z, cur.th.y);
+            sL[wl_][lane] = make_float2(cur.pr.z, th.y);
             if (POSE)   // camera-space centre from the projection (x = (u − cx)·z / fx, …)
                 sX[wl_][lane] = make_float4((cur.pr.x - p.in.cx) * cur.pr.z * rcp_approx(p.in.fx),
                                             (cur.pr.y - p.in.cy) * cur.pr.z * rcp_approx(p.in.fy), cur.pr.z, cur.pr.w);
@@ -269,19 +270,21 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
             const float z = cur.pr.z;
             float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, sw2 = 0.f, swx = 0.f, swy = 0.f, dzd = 0.f;
             unsigned mm = __funnelshift_r(mj, mj, lane);  // rotate right by lane
+            const float ux = cur.pr.x, uy = cur.pr.y;
             auto accum = [&](int i, float2 md, float4 gp) {
-                if (md.x == 0.f) return;   // a candidate the pixel did not composite (ω > 0 otherwise)
-                dc0 = fmaf(gp.x, md.x, dc0);
-                dc1 = fmaf(gp.y, md.x, dc1);
-                dc2 = fmaf(gp.z, md.x, dc2);
-                dzd = fmaf(gp.w, md.x, dzd);
-                const float dx = (float)(sx + (i & 7)) - cur.pr.x, dy = (float)(sy + (i >> 3)) - cur.pr.y;
-                const float d2 = dx * dx + dy * dy;
-                const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution; 0 when α clamped)
-                dop += dw;
-                sw2 = fmaf(dw, d2, sw2);
-                swx = fmaf(dw, dx, swx);
-                swy = fmaf(dw, dy, swy);
+                if (md.x != 0.f) {   // composited (ω > 0 for every composited pair)
+                    dc0 = fmaf(gp.x, md.x, dc0);
+                    dc1 = fmaf(gp.y, md.x, dc1);
+                    dc2 = fmaf(gp.z, md.x, dc2);
+                    dzd = fmaf(gp.w, md.x, dzd);
+                    const float dx = (float)(sx + (i & 7)) - ux, dy = (float)(sy + (i >> 3)) - uy;
+                    const float d2 = dx * dx + dy * dy;
+                    const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution; 0 when α clamped)
+                    dop += dw;
+                    sw2 = fmaf(dw, d2, sw2);
+                    swx = fmaf(dw, dx, swx);
+                    swy = fmaf(dw, dy, swy);
+                }
             };
             while (mm) {
                 const int i0 = ((__ffs(mm) - 1) + (int)lane) & 31;
@@ -292,17 +295,17 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
                 const float2 md0 = M[lane][i0];
                 const float4 gp0 = sG[wl_][i0];
                 float2 md1 = make_float2(0.f, 0.f);
-                float4 gp1 = make_float4(0.f, 0.f, 0.f, 0.f);
+                float4 gp1;
                 if (v1) {
                     md1 = M[lane][i1];
                     gp1 = sG[wl_][i1];
                 }
                 accum(i0, md0, gp0);
-                if (v1) accum(i1, md1, gp1);
+                accum(i1, md1, gp1);   // md1.x == 0 when there is no second pixel
             }
             // dL/dw·w = dL/dα·o·w;  ∂w/∂σ = w d²/σ³, ∂w/∂u = w (x−u)/σ², ∂w/∂v = w (y−v)/σ²
             const float s = fabsf(cur.pr.w);
-            const float inv_s2 = rcp_approx(s2j);
+            const float inv_s2 = rcp_approx(s * s);
             const float dsg = B.w * sw2 * inv_s2 * rcp_approx(s);
             if (ATTR && (int64_t)cur.g >= p.learn_begin && (int64_t)cur.g < p.learn_end) {
                 const bool wc = p.want & VTGS_GRAD_COLOR, wo = p.want & VTGS_GRAD_OPACITY;
@@ -433,13 +436,14 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
             const EntryRegs &e = st.e;
             const float s = fabsf(e.pr.w);
             const float s2 = __fmul_rn(s, s);
-            ring.A[slot + lane] = make_float4(e.pr.x, e.pr.y, e.th.x, exp_scale(s2));
+            const float2 th = thr_unpack(e.th, s2);
+            ring.A[slot + lane] = make_float4(e.pr.x, e.pr.y, th.x, exp_scale(s2));
             ring.B[slot + lane] = e.co;
             // X_c from the projection itself (x = (u − cx)·z / fx, …): no gather of the world centre
             const float iz = rcp_approx(e.pr.z);
             ring.Xq[slot + lane] = make_float4((e.pr.x - cxp) * e.pr.z * ifx, (e.pr.y - cyp) * e.pr.z * ify, e.pr.z,
                                                e.co.w * rcp_approx(s2));
-            ring.iz[slot + lane] = make_float2(e.pr.w > 0.f ? iz : -iz, e.th.y);
+            ring.iz[slot + lane] = make_float2(e.pr.w > 0.f ? iz : -iz, th.y);
             mj = mnx & onmask;   // the forward's candidate pixels with a nonzero upstream
         }
         // positions ≥ the pixel's `last` were not composited
@@ -748,8 +752,9 @@ static int bwd_minb() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("VTGS_BWD_MINB");
-        v = e ? atoi(e) : 12;  // 12 (default): the mapping backward held to 12 two-warp CTAs per SM (80
-                               // registers; shared memory allows 11); 0: the compiler's choice (~107)
+        v = e ? atoi(e) : 11;  // 11 (default): the mapping backward held to 11 two-warp CTAs per SM (≤ 93
+                               // registers) — shared memory allows 10–11 anyway; 12 (80 registers)
+                               // makes ptxas rematerialise phase 1's f; 0: the compiler's choice (~107)
     }
     return v;
 }
@@ -759,6 +764,10 @@ static void launch_bwd_t(const BwdArgs &a, int T, cudaStream_t s) {
     if constexpr (A && !P) {
         if (bwd_minb() == 12) {
             k_composite_bwd<A, P, L, 12><<<T * (8 / kBwdWarps), kBwdWarps * 32, kBwdDynSmem, s>>>(a);
+            return;
+        }
+        if (bwd_minb() == 11) {
+            k_composite_bwd<A, P, L, 11><<<T * (8 / kBwdWarps), kBwdWarps * 32, kBwdDynSmem, s>>>(a);
             return;
         }
     }
@@ -788,6 +797,11 @@ static cudaError_t set_bwd_attr() {
                                          (int)kBwdDynSmem);
         if (!e && bwd_carveout() >= 0)
             e = cudaFuncSetAttribute(k_composite_bwd<A, P, L, 12>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     bwd_carveout());
+        if (!e) e = cudaFuncSetAttribute(k_composite_bwd<A, P, L, 11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kBwdDynSmem);
+        if (!e && bwd_carveout() >= 0)
+            e = cudaFuncSetAttribute(k_composite_bwd<A, P, L, 11>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      bwd_carveout());
     }
     return e;

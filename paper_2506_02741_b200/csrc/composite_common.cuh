@@ -25,12 +25,12 @@ struct EntryRegs {
     uint32_t g;
     float4 pr;
     float4 co;
-    float2 th;   // (D_c, D_clamp) of k_project_count
+    float th;    // the packed (D_c, D_clamp) of k_project_count (thr_pack / thr_unpack)
 };
 
 __device__ __forceinline__ void fetch_entry(EntryRegs &er, const uint32_t *__restrict__ list, int idx, int n,
                                             const float4 *__restrict__ proj, const float4 *__restrict__ col,
-                                            const float2 *__restrict__ thr) {
+                                            const float *__restrict__ thr) {
     if (idx >= 0 && idx < n) {
         er.g = __ldg(list + idx);
         er.pr = __ldg(proj + er.g);
@@ -50,7 +50,7 @@ struct EntryStream {
 
 __device__ __forceinline__ void stream_start(EntryStream &s, const uint32_t *__restrict__ list, int idx0, int idx1,
                                              int n, const float4 *__restrict__ proj, const float4 *__restrict__ col,
-                                             const float2 *__restrict__ thr) {
+                                             const float *__restrict__ thr) {
     fetch_entry(s.e, list, idx0, n, proj, col, thr);
     s.gv = idx1 >= 0 && idx1 < n;
     if (s.gv) s.gn = __ldg(list + idx1);
@@ -59,7 +59,7 @@ __device__ __forceinline__ void stream_start(EntryStream &s, const uint32_t *__r
 // e ← the attributes of gid gn; gn ← the gid at idx2
 __device__ __forceinline__ void stream_next(EntryStream &s, const uint32_t *__restrict__ list, int idx2, int n,
                                             const float4 *__restrict__ proj, const float4 *__restrict__ col,
-                                            const float2 *__restrict__ thr) {
+                                            const float *__restrict__ thr) {
     if (s.gv) {
         s.e.g = s.gn;
         s.e.pr = __ldg(proj + s.gn);
@@ -149,6 +149,16 @@ __device__ __forceinline__ bool alpha_thresholds_fast(float s2, float o, float2 
     if (o > kAlphaMax || (o >= kAlphaMin && o < kOpaFast)) return false;
     th = make_float2(o >= kAlphaMin ? __fmul_rn(9.0f, s2) : -1.0f, -1.0f);
     return true;
+}
+
+// One float per Gaussian carries both thresholds: D_c ≥ 0 (not clampable, D_clamp = −1); −1 (no
+// pixel passes); ≤ −2 for a clampable Gaussian (o > 0.999), which always passes its whole disc
+// (o·w at the rim ≥ 0.999·e^−4.5 > 1/255, so D_c = fl(9·s2)) — the value is −D_clamp − 2.
+__device__ __forceinline__ float thr_pack(float2 t, float s2) {
+    return t.y >= 0.0f ? -t.y - 2.0f : t.x;
+}
+__device__ __forceinline__ float2 thr_unpack(float th, float s2) {
+    return th <= -2.0f ? make_float2(__fmul_rn(9.0f, s2), -th - 2.0f) : make_float2(th, -1.0f);
 }
 
 // (D_c, D_clamp) of a Gaussian with σ² = s2 and opacity o: composited-eligible ⇔ d² ≤ D_c =

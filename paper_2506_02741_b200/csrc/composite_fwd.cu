@@ -10,7 +10,7 @@ namespace vtgs {
 
 struct FwdArgs {
     const float4 *proj;
-    const float2 *thr;     // per Gaussian (D_c, D_clamp), k_project_count
+    const float *thr;      // per Gaussian packed (D_c, D_clamp), k_project_count
     const float4 *col_opa;
     const uint32_t *tile_count;
     const uint32_t *tile_start;
@@ -78,12 +78,13 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
             const float s = fabsf(nxt.pr.w);
             const float s2 = __fmul_rn(s, s);
             const float s9 = __fmul_rn(9.0f, s2);
-            ring.A[slot + lane] = make_float4(nxt.pr.x, nxt.pr.y, nxt.th.x, exp_scale(s2));
+            const float dc = thr_unpack(nxt.th, s2).x;
+            ring.A[slot + lane] = make_float4(nxt.pr.x, nxt.pr.y, dc, exp_scale(s2));
             ring.B[slot + lane] = nxt.co;
             ring.Z[slot + lane] = nxt.pr.z;
             if (STATS) ring.S9[slot + lane] = s9;
             // candidates: the pixels within D_c (the work counters also want the whole 3σ disc)
-            const unsigned m0 = lane_mask(make_float4(nxt.pr.x, nxt.pr.y, STATS ? s9 : nxt.th.x, 0.f),
+            const unsigned m0 = lane_mask(make_float4(nxt.pr.x, nxt.pr.y, STATS ? s9 : dc, 0.f),
                                           rect_from_proj(nxt.pr, p.W, p.H), sx, sy);
             mout[idx] = m0;   // the backward walks the same candidates and re-takes the same exact decisions
             mj = m0 & inmask;

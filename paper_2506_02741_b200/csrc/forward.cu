@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
                                                        vtgs_intrinsics in, int ntx,
                                                        float4 *__restrict__ proj,
                                                        uint2 *__restrict__ rect,
-                                                       float2 *__restrict__ thr,
+                                                       float *__restrict__ thr,
                                                        uint32_t *__restrict__ tile_count) {
     __shared__ PoseR P;
     if (threadIdx.x == 0) pose_rotation(*view, P);
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
             // the common case here, the search for the rest on a dense work list (no divergence)
             float2 th = make_float2(-1.f, -1.f);
             slow = f.vis && !alpha_thresholds_fast(__fmul_rn(f.s, f.s), __ldg(&col_opa[g].w), th);
-            thr[g] = th;
+            thr[g] = th.x;
         }
         // the Gaussians the fast test could not settle join the warp's queue; every 32 of them the
         // whole warp runs the exact search, one per lane (no divergence, no global atomics)
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
             if (qn >= 32) {
                 const uint32_t gq = qg[wq][lane_id()];
                 const float sq = qs[wq][lane_id()];
-                thr[gq] = alpha_thresholds(__fmul_rn(sq, sq), __ldg(&col_opa[gq].w));
+                thr[gq] = thr_pack(alpha_thresholds(__fmul_rn(sq, sq), __ldg(&col_opa[gq].w)), 0.f);
                 __syncwarp();
                 qn -= 32;
                 if ((int)lane_id() < qn) {
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
     if ((int)lane_id() < qn) {   // the queue's remainder
         const uint32_t gq = qg[wq][lane_id()];
         const float sq = qs[wq][lane_id()];
-        thr[gq] = alpha_thresholds(__fmul_rn(sq, sq), __ldg(&col_opa[gq].w));
+        thr[gq] = thr_pack(alpha_thresholds(__fmul_rn(sq, sq), __ldg(&col_opa[gq].w)), 0.f);
     }
 }
 

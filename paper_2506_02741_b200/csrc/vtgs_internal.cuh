@@ -61,7 +61,7 @@ struct Ctx {
     // scratch (device)
     float4 *proj = nullptr;          // (u, v, z, ±σ) per Gaussian, −σ ⇔ σ clamped
     uint2 *rect = nullptr;           // (x0 | x1<<16, y0 | y1<<16)
-    float2 *thr = nullptr;           // (D_c, D_clamp): exact α decision thresholds in d² (composite_common.cuh)
+    float *thr = nullptr;            // packed (D_c, D_clamp): exact α decision thresholds in d² (composite_common.cuh)
     uint32_t *tile_count = nullptr;  // [max_tiles]
     uint32_t *tile_start = nullptr;  // [max_tiles + 1]
     uint32_t *tile_cursor = nullptr; // [max_tiles]
