@@ -83,13 +83,15 @@ __device__ __forceinline__ uint32_t load_mask(const uint32_t *__restrict__ mlist
 // rounding step is monotone): "α ≥ 1/255" ⇔ d² ≤ D_floor and "o·w > 0.999" (clamped) ⇔
 // d² ≤ D_clamp, for per-Gaussian fp32 thresholds that k_project_count finds once per view with
 // the exact arithmetic (alpha_thresholds).  The compositing kernels then decide with compares
-// only; the VALUE of an unclamped α uses the fast w = ex2.approx(fl(d²·escale)),
-// escale = fl(−½log2(e)/s2) (relative error ≤ ~7e-7, a value difference, never a decision).
+// only; the VALUE of an unclamped α uses the fast w = ex2.approx(d²·escale),
+// escale = −½log2(e)·rcp(s2) (relative error ≤ ~1e-6, a value difference, never a decision).
 // The forward and the backward read the same thresholds, so they composite the same pairs.
 constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kNegHalfLog2e = -0.5f * kLog2e;
 
-__device__ __forceinline__ float exp_scale(float s2) { return __fdiv_rn(kNegHalfLog2e, s2); }
+// −½log2(e)/s2 for the α VALUE (never a decision): one approximate reciprocal, the same
+// instructions in every kernel, so the forward and the backward use the same bits
+__device__ __forceinline__ float exp_scale(float s2) { return kNegHalfLog2e * rcp_approx(s2); }
 
 // the oracle's raw α = fl(o·w) with the correctly rounded w (fp64 exp, rounded once)
 __device__ __forceinline__ float exact_raw_alpha(float d2, float s2, float o) {
@@ -172,7 +174,7 @@ __device__ __forceinline__ float2 alpha_thresholds(float s2, float o) {
 }
 
 // α VALUE of a pair (the decision d² ≤ D_c is the caller's): 0.999 when clamped (d² ≤ D_clamp),
-// else min(o·w, 0.999) with the fast w = 2^(d²·escale) (relative error ≤ ~7e-7 against the
+// else min(o·w, 0.999) with the fast w = 2^(d²·escale) (relative error ≤ ~1.1e-6 against the
 // oracle's o·w).  The forward passes dcl = −1: its α value needs no clamp decision (an exact-vs-
 // fast difference at the clamp is a value difference of ~1e-6); the backward passes D_clamp, for
 // ∂α/∂o = 0 on clamped pairs.  w is returned for the backward's chain.
