@@ -343,7 +343,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
     }
 
     if (POSE || LOSS) {   // fixed-order reduction: lanes → warp → CTA (one partial per CTA)
-        __shared__ double sRed[kBwdWarps][13];
+        // each warp's 13 doubles go into its own (now dead) row of sA: no extra shared memory
+        // (K7's occupancy is shared-memory bound: 11 two-warp CTAs per SM need ≤ 19.9 KB each)
         double v[13] = {h0, h1, h2, K00, K01, K02, K10, K11, K12, K20, K21, K22, lossv};
 #pragma unroll
         for (int q = 0; q < 13; ++q) {
@@ -352,12 +353,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
         }
         if (lane == 0)
 #pragma unroll
-            for (int q = 0; q < 13; ++q) sRed[wl_][q] = v[q];
+            for (int q = 0; q < 13; ++q) reinterpret_cast<double *>(&sA[wl_][0])[q] = v[q];
         __syncthreads();
         if (threadIdx.x < 13) {
             double s = 0.0;
 #pragma unroll
-            for (int i = 0; i < kBwdWarps; ++i) s += sRed[i][threadIdx.x];
+            for (int i = 0; i < kBwdWarps; ++i) s += reinterpret_cast<const double *>(&sA[i][0])[threadIdx.x];
             p.partials[(size_t)blockIdx.x * 16 + threadIdx.x] = s;
         }
     }
