@@ -75,19 +75,29 @@ __global__ void __launch_bounds__(256) k_project_count(const float4 *__restrict_
     __shared__ float qs[8][64];      // and their σ
     const int wq = threadIdx.x >> 5;
     int qn = 0;
-    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < Nr; g += stride) {
+    // the next iteration's state is loaded one iteration ahead (the loop is latency-bound)
+    const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float4 pr_next = g0 < N ? __ldg(pos_rad + g0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float o_next = g0 < N ? __ldg(&col_opa[g0].w) : 0.f;
+    for (int64_t g = g0; g < Nr; g += stride) {
         Footprint f;
         f.vis = false;
         bool slow = false;
+        const float4 pr_g = pr_next;
+        const float o_g = o_next;
+        if (g + stride < N) {
+            pr_next = __ldg(pos_rad + g + stride);
+            o_next = __ldg(&col_opa[g + stride].w);
+        }
         if (g < N) {
-            f = project_one(pos_rad[g], P, in, fmean, Wm1, Hm1);
+            f = project_one(pr_g, P, in, fmean, Wm1, Hm1);
             proj[g] = f.vis ? make_float4(f.u, f.v, f.z, f.clamped ? -f.s : f.s) : make_float4(0.f, 0.f, 0.f, 0.f);
             rect[g] = f.vis ? make_uint2((uint32_t)f.x0 | ((uint32_t)f.x1 << 16), (uint32_t)f.y0 | ((uint32_t)f.y1 << 16))
                             : make_uint2(0xffffffffu, 0xffffffffu);
             // exact α decision thresholds in d² (composite_common.cuh), once per Gaussian per view:
             // the common case here, the search for the rest on a dense work list (no divergence)
             float2 th = make_float2(-1.f, -1.f);
-            slow = f.vis && !alpha_thresholds_fast(__fmul_rn(f.s, f.s), __ldg(&col_opa[g].w), th);
+            slow = f.vis && !alpha_thresholds_fast(__fmul_rn(f.s, f.s), o_g, th);
             thr[g] = th.x;
         }
         // the Gaussians the fast test could not settle join the warp's queue; every 32 of them the
