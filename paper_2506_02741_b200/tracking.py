@@ -129,11 +129,19 @@ def overlap_candidates(renderer, depth: torch.Tensor, init_pose: torch.Tensor, c
     counts, n_valid = renderer.visibility_counts(depth, init_pose, cand_depth, cand_poses, intr, tol)
     counts = counts.cpu().tolist()
     nv = int(n_valid.item())
-    kept = [i for i, c in enumerate(counts) if nv > 0 and c / nv > gamma]
+    return choose_sections(counts, nv, cand_section, gamma, n_sections), counts, nv
+
+
+def choose_sections(counts: Sequence[int], n_valid: int, cand_section: Sequence[int], gamma: float,
+                    n_sections: int = 3) -> List[int]:
+    """The host half of steps (3)-(4) of SPEC.md:382-387: keep the candidates whose visible
+    fraction count / n_valid exceeds γ (R29); return the `n_sections` earliest distinct
+    sections holding a kept candidate (R30); none kept → the most recent section."""
+    kept = [i for i, c in enumerate(counts) if n_valid > 0 and c / n_valid > gamma]
     secs = sorted({int(cand_section[i]) for i in kept})[:n_sections]
     if not secs:
         secs = [max(int(s) for s in cand_section)]
-    return secs, counts, nv
+    return secs
 
 
 def select_overlap_section(renderers: Sequence, sections: Sequence[dict], depth: torch.Tensor, rgb: torch.Tensor,

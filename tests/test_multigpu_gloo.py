@@ -84,3 +84,62 @@ def test_allreduce_equals_single_rank_sum():
     for r in range(world):
         np.testing.assert_allclose(out[r], ref, rtol=1e-5, atol=1e-6)
     assert np.array_equal(out[0], out[1])   # identical buffers on every rank after the all-reduce
+
+
+def _mapper_worker(rank, world, port, q):
+    """One rank of BatchedMapper.step on config 1 with 4 views, gloo all-reduce of the CUDA
+    gradient buffer (the NCCL path is the same call with backend "nccl")."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, _mapper_step(rank, world)))
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+def _mapper_step(rank, world):
+    from paper_2506_02741_b200 import vtgs
+    from paper_2506_02741_b200.mapping import BatchedMapper, shard_views
+    from synth.scenes import make_config, perturb_pose
+    cfg = make_config(1, 0)
+    dev = "cuda"
+    R = vtgs.Renderer(0, cfg.n_slots, cfg.intr.width, cfg.intr.height)
+    pr, co = R.instantiate(torch.from_numpy(cfg.depth_stack()).to(dev), torch.from_numpy(cfg.rgb_stack()).to(dev),
+                           vtgs.pose_tensor(cfg.pose_stack(), dev), cfg.intr, torch.from_numpy(cfg.opacity).to(dev))
+    rng = np.random.default_rng(0)
+    all_views = [perturb_pose(cfg.keyframes[0].pose, 1.0 * k, 0.01 * k, rng) for k in range(4)]
+    mine = shard_views(len(all_views), world, rank)
+    views = [vtgs.pose_tensor(np.asarray(all_views[k], dtype=np.float32), dev) for k in mine]
+    tg = cfg.targets[0]
+    tgts = [dict(rgb=torch.from_numpy(tg.rgb).to(dev), depth=torch.from_numpy(tg.depth).to(dev)) for _ in mine]
+    m = BatchedMapper(R, pr, co, cfg.intr, views, tgts, 1.0, 0.5,
+                      group=dist.group.WORLD if world > 1 else None)
+    g = m.step(allreduce=True)
+    torch.cuda.synchronize()
+    return g.flat.cpu().numpy().copy()
+
+
+@pytest.mark.gpu
+def test_batched_mapper_two_ranks_equals_one():
+    """BatchedMapper.step over 2 ranks (2 views each) with the all-reduce gives the same 5N
+    gradient buffer on both ranks as one rank rendering all 4 views (up to the float-atomic
+    summation order)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mapper_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = _mapper_step(0, 1)
+    for r in range(2):
+        np.testing.assert_allclose(out[r], ref, rtol=1e-4, atol=1e-6)
+    assert np.array_equal(out[0], out[1])
