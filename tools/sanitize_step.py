@@ -14,8 +14,21 @@ import torch  # noqa: E402
 from paper_2506_02741_b200 import vtgs  # noqa: E402
 from synth.scenes import make_config  # noqa: E402
 
-which = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-cfg = make_config(which)
+arg = sys.argv[1] if len(sys.argv) > 1 else "1"
+if arg == "long":   # 60,000 Gaussians in a 40×36 image: tile lists > 16,384 (chunked sort paths)
+    from synth.scenes import Config, Frame, Intrinsics
+    rng = np.random.Generator(np.random.PCG64([7, 3]))
+    W_, H_ = 40, 36
+    intr_ = Intrinsics(30.0, 30.0, (W_ - 1) / 2, (H_ - 1) / 2, W_, H_)
+    depth = rng.uniform(1.0, 4.0, size=(1, H_, W_)).astype(np.float32)
+    kf = Frame(depth[0], rng.random((H_, W_, 3)).astype(np.float32), np.array([1.0, 0, 0, 0, 0, 0, 0]))
+    kfs = [kf] * 40
+    cfg = Config("long", intr_, kfs, rng.uniform(0.01, 0.2, (40, H_, W_)).astype(np.float32),
+                 [np.array([1.0, 0, 0, 0, 0.01, 0, 0])], [kf], (0.8, 1.0), "mapping", 0)
+    which = "long"
+else:
+    which = int(arg)
+    cfg = make_config(which)
 intr = cfg.intr
 H, W = intr.height, intr.width
 N = cfg.n_slots
