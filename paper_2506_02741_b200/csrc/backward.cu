@@ -48,6 +48,8 @@ struct BwdArgs {
     float4 *d_position;
     double *partials;
     unsigned long long *det;   // VTGS_GRAD_DETERMINISTIC: int64 fixed-point accumulators [N][5], else NULL
+    uint64_t sub_cap;          // entries of sub_lists / sub_masks (checked build)
+    int64_t N;                 // Gaussians (checked build)
 };
 
 // Deterministic attribute-gradient merge ("merged deterministically"): the
@@ -159,6 +161,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
     const int n = (int)p.tile_count[tile];
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
+    VTGS_CHECK((uint64_t)8 * p.tile_start[tile] + (uint64_t)(sub + 1) * n <= p.sub_cap);
     PoseR P;
     if (POSE) pose_rotation(*p.view, P);
 
@@ -172,6 +175,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
     sG[wl_][lane] = make_float4(g0, g1, g2, gD);
     const unsigned onmask = __ballot_sync(kFullMask, on);
     const int wmax = (int)__reduce_max_sync(kFullMask, L);  // sub-list positions < wmax matter
+    VTGS_CHECK(wmax <= (int)p.sub_count[tile * 8 + sub]);
 
     // Behind-accumulator, relative to the pixel's references and already dotted with the
     // (constant) upstream gradient: Fb = Σ_{j behind} w_j f_j with f_j = g_C·(c_j − c_ref) +
@@ -198,6 +202,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
         unsigned mj = 0u;
         float s2j = 1.0f;
         if (jj < wmax) {   // wmax ≤ the sub-list length
+            VTGS_CHECK((int64_t)cur.g < p.N && cur.pr.z > 0.0f);
             const float s = fabsf(cur.pr.w);
             s2j = __fmul_rn(s, s);
             const float2 th = thr_unpack(cur.th, s2j);
@@ -408,6 +413,7 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
     const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
     const int cnt = (int)p.sub_count[tile * 8 + sub];
+    VTGS_CHECK(cnt <= n && (uint64_t)8 * p.tile_start[tile] + (uint64_t)(sub + 1) * n <= p.sub_cap);
     const PixelUp up = pixel_upstream<LOSS>(p, px, py, inside);
     const float g0 = up.g0, g1 = up.g1, g2 = up.g2, gD = up.gD, gS = up.gS;
     const float r0 = up.r0, r1 = up.r1, r2 = up.r2, rz = up.rz;
@@ -435,6 +441,7 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
         unsigned mj = 0u;
         if (bb + (int)lane < wmax) {   // wmax ≤ cnt
             const EntryRegs &e = st.e;
+            VTGS_CHECK((int64_t)e.g < p.N && e.pr.z > 0.0f && wmax <= cnt);
             const float s = fabsf(e.pr.w);
             const float s2 = __fmul_rn(s, s);
             const float2 th = thr_unpack(e.th, s2);
@@ -837,6 +844,7 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
     a.dev = c.dev; a.view = c.view_copy; a.in = c.intr;
     a.learn_begin = learn_begin; a.learn_end = learn_end; a.want = want;
     a.d_col_opa = d_col_opa; a.d_radius = d_radius; a.d_position = d_position; a.partials = c.partials;
+    a.sub_cap = (uint64_t)8 * c.max_pairs; a.N = c.N;
     const bool L = loss != nullptr;
     if (L) {
         a.tC = loss->target_rgb; a.tD = loss->target_depth; a.vis = loss->vis_mask; a.extra_dc = loss->extra_dcolor;

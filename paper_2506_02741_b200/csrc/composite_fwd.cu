@@ -21,6 +21,8 @@ struct FwdArgs {
     float *color, *depth, *sil, *T_final;
     uint32_t *last;
     DevScalars *dev;
+    uint64_t sub_cap;   // entries of sub_lists / sub_masks (checked build)
+    int64_t N;          // Gaussians (checked build)
 };
 
 constexpr int kFwdWarps = 2;  // warps (8×4 sub-tiles) per CTA: small CTAs retire independently
@@ -63,6 +65,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
     uint32_t *mout = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)w * n;
     const int cnt = (int)p.sub_count[tile * 8 + w];
     const int nb = (cnt + 31) >> 5;
+    VTGS_CHECK(cnt <= n && (uint64_t)8 * p.tile_start[tile] + (uint64_t)(w + 1) * n <= p.sub_cap);
     const unsigned inmask = __ballot_sync(kFullMask, inside);
 
     EntryStream st;
@@ -75,6 +78,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
         const int idx = built * 32 + (int)lane;
         unsigned mj = 0u;
         if (idx < cnt) {
+            VTGS_CHECK((int64_t)nxt.g < p.N && nxt.pr.z > 0.0f);
             const float s = fabsf(nxt.pr.w);
             const float s2 = __fmul_rn(s, s);
             const float s9 = __fmul_rn(9.0f, s2);
@@ -173,6 +177,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
     }
     if (inside) {
         const int pix = py * p.W + px;
+        VTGS_CHECK(lastc <= (uint32_t)cnt && T >= kTMin);
         p.color[3 * pix + 0] = C0;
         p.color[3 * pix + 1] = C1;
         p.color[3 * pix + 2] = C2;
@@ -224,7 +229,7 @@ cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
     const int W = c.intr.width, H = c.intr.height;
     const int ntx = (W + kTile - 1) / kTile, nty = (H + kTile - 1) / kTile;
     FwdArgs a{c.proj, c.thr, c.col_opa, c.tile_count, c.tile_start, c.sub_lists, c.sub_count, c.sub_masks, W, H, ntx,
-              c.color, c.depth, c.sil, c.T_final, c.last, c.dev};
+              c.color, c.depth, c.sil, c.T_final, c.last, c.dev, (uint64_t)8 * c.max_pairs, c.N};
     switch (fwd_variant()) {
         case 8: return launch_ring<8, 1>(a, ntx * nty, c.count_work, s);
         case 4: return launch_ring<4, 1>(a, ntx * nty, c.count_work, s);

@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t *__restrict__ tile
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_emit_pairs(const float4 *__restrict__ proj,
                                                     const uint2 *__restrict__ rect, int64_t N, int ntx,
+                                                    const uint32_t *__restrict__ tile_start,
                                                     uint32_t *__restrict__ cursor,
                                                     uint32_t *__restrict__ keys,
                                                     uint32_t *__restrict__ vals,
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(256) k_emit_pairs(const float4 *__restrict__ p
             base = __shfl_sync(kFull, base, leader);
             if (tile >= 0) {
                 const uint32_t slot = base + __popc(peers & lanemask_lt());
+                VTGS_CHECK(slot < tile_start[tile + 1]);   // the counts of k_project_count hold
                 keys[slot] = zb;
                 vals[slot] = (uint32_t)g;
                 pbits[slot] = (uint8_t)subtile_bits(r, tcx * kTile, tcy * kTile);
@@ -914,7 +916,8 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     if ((err = cudaGetLastError())) return err;
     if (N > 0) {
         LaunchScope ls(&c, kEmit, s);
-        k_emit_pairs<<<gE, 256, 0, s>>>(c.proj, c.rect, N, ntx, c.tile_cursor, c.keys, c.vals, c.pbits, c.dev);
+        k_emit_pairs<<<gE, 256, 0, s>>>(c.proj, c.rect, N, ntx, c.tile_start, c.tile_cursor, c.keys, c.vals, c.pbits,
+                                         c.dev);
         if ((err = cudaGetLastError())) return err;
     }
     {

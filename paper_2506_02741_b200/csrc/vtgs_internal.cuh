@@ -15,6 +15,24 @@
 
 #include "../../include/vtgs.h"
 
+// Checked build (`python -m paper_2506_02741_b200.build --checked` → libvtgs_checked.so): bounds and
+// invariant checks in the kernels that trap on failure — this pool has compute-sanitizer closed,
+// so the GPU test suite runs once against this build instead (tests/test_gpu_variants.py).
+#ifdef VTGS_CHECKED
+#include <cstdio>
+#define VTGS_CHECK(cond)                                                                                  \
+    do {                                                                                                  \
+        if (!(cond)) {                                                                                    \
+            printf("VTGS_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);                           \
+            __trap();                                                                                     \
+        }                                                                                                 \
+    } while (0)
+#else
+#define VTGS_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace vtgs {
 
 constexpr int kTile = 16;                 // 16×16 tiles

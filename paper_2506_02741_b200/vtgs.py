@@ -16,7 +16,8 @@ from typing import Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvtgs.so")
+# VTGS_LIB=checked loads the bounds-checked build (libvtgs_checked.so, tests/test_gpu_variants.py)
+LIB_PATH = os.path.join(_HERE, "libvtgs_checked.so" if os.environ.get("VTGS_LIB") == "checked" else "libvtgs.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2506_02741_b200.build` "
                       "(there is no CPU fallback)")
