@@ -232,6 +232,7 @@ cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
               c.color, c.depth, c.sil, c.T_final, c.last, c.dev, (uint64_t)8 * c.max_pairs, c.N};
     switch (fwd_variant()) {
         case 8: return launch_ring<8, 1>(a, ntx * nty, c.count_work, s);
+        case 812: return launch_ring<8, 12>(a, ntx * nty, c.count_work, s);
         case 4: return launch_ring<4, 1>(a, ntx * nty, c.count_work, s);
         default: return launch_ring<4, 14>(a, ntx * nty, c.count_work, s);
     }
