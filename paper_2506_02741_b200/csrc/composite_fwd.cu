@@ -45,7 +45,9 @@ struct FwdRing {
     float S9[STATS ? R * 32 : 1];   // 9σ² (the work counter's 3σ test)
 };
 
-template <int R, bool STATS, int MINB>
+// AHEAD: how far past the furthest batch a lane needs the warp builds when it has to build (the
+// ring's R bounds it too); batches built past the point where every pixel terminates are wasted
+template <int R, bool STATS, int MINB, int AHEAD = R>
 __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(FwdArgs p) {
     extern __shared__ float4 fwd_smem[];
     static_assert((R & (R - 1)) == 0, "ring depth must be a power of two");
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
         ++built;
         stream_next(st, list, (built + 1) * 32 + (int)lane, cnt, p.proj, p.col_opa, p.thr);
     };
-    while (built < nb && built < R) build();
+    while (built < nb && built < R && built <= AHEAD) build();
     __syncwarp();
 
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f, D = 0.f, Sl = 0.f;
@@ -169,8 +171,13 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
         if (__any_sync(kFullMask, blocked)) {
             const int need = !live ? 0x7fffffff : (cur ? b : b + 1);  // earliest batch still needed
             const int lo = __reduce_min_sync(kFullMask, need);
-            if (built < nb && built < lo + R) {
-                while (built < nb && built < lo + R) build();
+            int target = lo + R < nb ? lo + R : nb;
+            if (AHEAD < R) {
+                const int hi = (int)__reduce_max_sync(kFullMask, live ? (unsigned)need : 0u);
+                target = min(target, hi + 1 + AHEAD);
+            }
+            if (built < target) {
+                while (built < target) build();
                 __syncwarp();
             }
         }
@@ -204,25 +211,26 @@ static int fwd_variant() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("VTGS_FWD");
-        v = e ? atoi(e) : 14;   // 14 (default): R = 4 with 14 two-warp CTAs per SM (≤ 72 registers);
-                                // 4: R = 4 at the compiler's register count; 8: R = 8
+        v = e ? atoi(e) : 0;   // 0 (default): R = 4, 14 two-warp CTAs per SM (≤ 72 registers), lazy
+                               // build; 14: the same with an eager ring fill; 4: R = 4 at the
+                               // compiler's register count; 8: R = 8; 812: R = 8, 12 CTAs/SM
     }
     return v;
 }
 
-template <int R, bool STATS, int MINB>
+template <int R, bool STATS, int MINB, int AHEAD>
 static cudaError_t launch_ring_s(const FwdArgs &a, int T, cudaStream_t s) {
     const size_t sm = sizeof(FwdRing<R, STATS>) * kFwdWarps;
-    cudaError_t e = cudaFuncSetAttribute(k_composite_fwd_ring<R, STATS, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(k_composite_fwd_ring<R, STATS, MINB, AHEAD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e) return e;
-    k_composite_fwd_ring<R, STATS, MINB><<<T * 8 / kFwdWarps, kFwdWarps * 32, sm, s>>>(a);
+    k_composite_fwd_ring<R, STATS, MINB, AHEAD><<<T * 8 / kFwdWarps, kFwdWarps * 32, sm, s>>>(a);
     return cudaGetLastError();
 }
 
-template <int R, int MINB>
+template <int R, int MINB, int AHEAD = R>
 static cudaError_t launch_ring(const FwdArgs &a, int T, bool stats, cudaStream_t s) {
-    return stats ? launch_ring_s<R, true, MINB>(a, T, s) : launch_ring_s<R, false, MINB>(a, T, s);
+    return stats ? launch_ring_s<R, true, MINB, AHEAD>(a, T, s) : launch_ring_s<R, false, MINB, AHEAD>(a, T, s);
 }
 
 cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
@@ -233,8 +241,9 @@ cudaError_t launch_composite_fwd(Ctx &c, cudaStream_t s) {
     switch (fwd_variant()) {
         case 8: return launch_ring<8, 1>(a, ntx * nty, c.count_work, s);
         case 812: return launch_ring<8, 12>(a, ntx * nty, c.count_work, s);
+        case 14: return launch_ring<4, 14>(a, ntx * nty, c.count_work, s);   // eager ring fill
         case 4: return launch_ring<4, 1>(a, ntx * nty, c.count_work, s);
-        default: return launch_ring<4, 14>(a, ntx * nty, c.count_work, s);
+        default: return launch_ring<4, 14, 0>(a, ntx * nty, c.count_work, s);   // lazy build
     }
 }
 

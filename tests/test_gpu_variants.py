@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("var", ["VTGS_SORT=0", "VTGS_FWD=8", "VTGS_FWD=4", "VTGS_BWD_POSE=0", "VTGS_BWD_MINB=12",
+@pytest.mark.parametrize("var", ["VTGS_SORT=0", "VTGS_FWD=8", "VTGS_FWD=4", "VTGS_FWD=14", "VTGS_BWD_POSE=0", "VTGS_BWD_MINB=12",
                                  "VTGS_LIB=checked"])
 def test_variant_parity(var):
     k, v = var.split("=")
