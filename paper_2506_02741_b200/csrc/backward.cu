@@ -548,6 +548,274 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// Mapping backward as a ring walk (VTGS_BWD_RING): phase 1 (lane = pixel) walks its candidates
+// back to front ACROSS batch boundaries at its own pace over R resident batches, like the
+// forward's ring, and writes each pair's (ω, dL/dα·w) into a per-warp shared-memory pair ring
+// at a popc-ranked slot: entry k's pairs sit at base_k + rank of the pixel in k's pixel mask.
+// Phase 2 (lane = entry) runs per batch once every lane has passed it, reads the entry's pairs
+// in pixel order and leaves with the same per-(Gaussian, sub-tile) atomics as k_composite_bwd.
+// The arithmetic per pair and per entry is that of k_composite_bwd (same decisions, same α,
+// same recursion, same per-entry summation order), only the schedule differs.
+// ------------------------------------------------------------------------------------------
+template <int R>
+struct BwdRing {
+    float4 A[R * 32];         // u, v, D_c, escale
+    float4 B[R * 32];         // c, o
+    float4 Z[R * 32];         // z, D_clamp, σ (signed: − when clamped), gid (bits)
+    uint2 EM[R * 32];         // entry: pixel mask (candidate ∧ upstream ≠ 0 ∧ before the pixel's last), pair base
+    uint32_t bits[R * 32];    // pixel lane: its entries of the batch (bit k = entry k)
+};
+constexpr int kRingPairs = 1024;   // ≥ 32 × 32: any one batch fits, so the walk cannot deadlock
+constexpr int kRingInner = 6;      // lane-independent steps between warp checks
+template <int R>
+__host__ __device__ constexpr size_t bwd_ring_warp_bytes() {
+    return sizeof(BwdRing<R>) + sizeof(float2) * kRingPairs + sizeof(float4) * 32;
+}
+
+template <int R, bool LOSS>
+__global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_ring(BwdArgs p) {
+    extern __shared__ float4 bwd_ring_smem[];
+    static_assert((R & (R - 1)) == 0, "ring depth must be a power of two");
+    constexpr unsigned CP = kRingPairs;
+    const int wl_ = threadIdx.x >> 5;
+    char *wbase = reinterpret_cast<char *>(bwd_ring_smem) + (size_t)wl_ * bwd_ring_warp_bytes<R>();
+    BwdRing<R> &ring = *reinterpret_cast<BwdRing<R> *>(wbase);
+    float2 *pairs = reinterpret_cast<float2 *>(wbase + sizeof(BwdRing<R>));
+    float4 *sG = reinterpret_cast<float4 *>(wbase + sizeof(BwdRing<R>) + sizeof(float2) * CP);
+    const int gsub = blockIdx.x * kBwdWarps + wl_;
+    const int tile = gsub >> 3;
+    const int sub = gsub & 7;
+    const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
+    const unsigned lane = lane_id();
+    const unsigned lmlt = lanemask_lt();
+    const int sx = tx * kTile + (sub & 1) * 8, sy = ty * kTile + (sub >> 1) * 4;
+    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const bool inside = px < p.W && py < p.H;
+    const float pxf = (float)px, pyf = (float)py;
+    const int n = (int)p.tile_count[tile];
+    const uint32_t *list = p.sub_lists + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
+    const uint32_t *mlist = p.sub_masks + (size_t)8 * p.tile_start[tile] + (size_t)sub * n;
+    const int cnt = (int)p.sub_count[tile * 8 + sub];
+    VTGS_CHECK(cnt <= n && (uint64_t)8 * p.tile_start[tile] + (uint64_t)(sub + 1) * n <= p.sub_cap);
+    const PixelUp up = pixel_upstream<LOSS>(p, px, py, inside);
+    const float g0 = up.g0, g1 = up.g1, g2 = up.g2, gD = up.gD, gS = up.gS;
+    const float r0 = up.r0, r1 = up.r1, r2 = up.r2, rz = up.rz;
+    float T = up.T;
+    const bool on = inside && up.L > 0 && (g0 != 0.f || g1 != 0.f || g2 != 0.f || gD != 0.f || gS != 0.f);
+    const int L = on ? (int)up.L : 0;
+    sG[lane] = make_float4(g0, g1, g2, gD);
+    const unsigned onmask = __ballot_sync(kFullMask, on);
+    const int wmax = (int)__reduce_max_sync(kFullMask, (unsigned)L);
+    VTGS_CHECK(wmax <= cnt);
+    const int bb_top = wmax > 0 ? ((wmax - 1) >> 5) << 5 : -32;
+    const int nb = (bb_top >> 5) + 1;   // batch t covers sub-list positions [bb_top − 32t, +32)
+    float Fb = 0.f, Tb = 1.0f;          // behind-accumulators (k_composite_bwd)
+    const float Kr = g0 * r0 + g1 * r1 + g2 * r2 + gD * rz + gS;
+    const float fmean = 0.5f * (p.in.fx + p.in.fy);
+
+    EntryStream st;
+    stream_start(st, list, bb_top + (int)lane, bb_top - 32 + (int)lane, cnt, p.proj, p.col_opa, p.thr);
+    uint32_t mnx = load_mask(mlist, bb_top + (int)lane, wmax);
+    int built = 0;          // batches committed (visible to phase 1)
+    int flushed = 0;        // batches reduced by phase 2
+    unsigned head = 0u, tail = 0u;   // pair ring in use: [tail, head)
+    bool pend = false;      // batch `built` staged (slot written) but its pairs not yet allocated
+    unsigned pem = 0u, pbits = 0u;   // the staged batch: entry lane's pixel mask, pixel lane's entries
+    auto stage = [&]() {
+        const int bb = bb_top - 32 * built;
+        const int slot = (built & (R - 1)) * 32;
+        unsigned mj = 0u;
+        if (bb + (int)lane < wmax) {
+            const EntryRegs &e = st.e;
+            VTGS_CHECK((int64_t)e.g < p.N && e.pr.z > 0.0f);
+            const float s = fabsf(e.pr.w);
+            const float s2 = __fmul_rn(s, s);
+            const float2 th = thr_unpack(e.th, s2);
+            ring.A[slot + lane] = make_float4(e.pr.x, e.pr.y, th.x, exp_scale(s2));
+            ring.B[slot + lane] = e.co;
+            ring.Z[slot + lane] = make_float4(e.pr.z, th.y, e.pr.w, __uint_as_float(e.g));
+            mj = mnx & onmask;   // the forward's candidate pixels with a nonzero upstream
+        }
+        const int rem = L - bb;  // positions ≥ the pixel's `last` were not composited
+        const unsigned alive = rem >= 32 ? 0xffffffffu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+        pbits = transpose32(mj, lane) & alive;
+        pem = mj & transpose32(alive, lane);
+        pend = true;
+        stream_next(st, list, bb - 64 + (int)lane, cnt, p.proj, p.col_opa, p.thr);
+        mnx = load_mask(mlist, bb - 32 + (int)lane, wmax);
+    };
+    auto try_commit = [&]() {
+        const unsigned c = __popc(pem);
+        unsigned incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(kFullMask, incl, o);
+            if ((int)lane >= o) incl += t;
+        }
+        const unsigned tot = __shfl_sync(kFullMask, incl, 31);
+        if (head - tail + tot > CP) return;
+        const int slot = (built & (R - 1)) * 32;
+        ring.EM[slot + lane] = make_uint2(pem, head + incl - c);
+        ring.bits[slot + lane] = pbits;
+        head += tot;
+        ++built;
+        pend = false;
+    };
+    // phase 2 of batch f (lane = entry): the entry's pairs in ascending pixel order
+    auto reduce = [&](int f) {
+        const int slot = (f & (R - 1)) * 32;
+        const uint2 em = ring.EM[slot + lane];
+        const unsigned mj = em.x;
+        if (mj) {
+            const float4 A = ring.A[slot + lane];
+            const float4 Zs = ring.Z[slot + lane];
+            const float o = ring.B[slot + lane].w;
+            const float ux = A.x, uy = A.y, z = Zs.x, sg = Zs.z;
+            const uint32_t g = __float_as_uint(Zs.w);
+            float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, sw2 = 0.f;
+            auto accum = [&](int i, float2 md, float4 gp) {
+                if (md.x != 0.f) {   // composited (ω > 0 for every composited pair)
+                    dc0 = fmaf(gp.x, md.x, dc0);
+                    dc1 = fmaf(gp.y, md.x, dc1);
+                    dc2 = fmaf(gp.z, md.x, dc2);
+                    const float dx = (float)(sx + (i & 7)) - ux, dy = (float)(sy + (i >> 3)) - uy;
+                    const float d2 = dx * dx + dy * dy;
+                    dop += md.y;
+                    sw2 = fmaf(md.y, d2, sw2);
+                }
+            };
+            unsigned mm = mj;
+            unsigned q = em.y;
+            while (mm) {
+                const int i0 = __ffs(mm) - 1;
+                mm &= mm - 1u;
+                const bool v1 = mm != 0u;
+                const int i1 = (__ffs(mm) - 1) & 31;
+                mm &= mm - 1u;
+                const float2 md0 = pairs[q & (CP - 1)];
+                const float4 gp0 = sG[i0];
+                float2 md1 = make_float2(0.f, 0.f);
+                float4 gp1;
+                if (v1) {
+                    md1 = pairs[(q + 1) & (CP - 1)];
+                    gp1 = sG[i1];
+                }
+                q += 2;
+                accum(i0, md0, gp0);
+                accum(i1, md1, gp1);
+            }
+            const float s = fabsf(sg);
+            const float inv_s2 = rcp_approx(s * s);
+            const float dsg = o * sw2 * inv_s2 * rcp_approx(s);
+            if ((int64_t)g >= p.learn_begin && (int64_t)g < p.learn_end) {
+                const bool wc = p.want & VTGS_GRAD_COLOR, wo = p.want & VTGS_GRAD_OPACITY;
+                const float dr = ((p.want & VTGS_GRAD_RADIUS) && sg > 0.f) ? dsg * fmean * rcp_approx(z) : 0.f;
+                if (p.det) {
+                    unsigned long long *qd = p.det + (size_t)5 * g;
+                    if (wc) { det_add(qd, dc0); det_add(qd + 1, dc1); det_add(qd + 2, dc2); }
+                    if (wo) det_add(qd + 3, dop);
+                    det_add(qd + 4, dr);
+                } else {
+                    if ((wc && (dc0 != 0.f || dc1 != 0.f || dc2 != 0.f)) || (wo && dop != 0.f))
+                        atomicAdd(&p.d_col_opa[g],
+                                  make_float4(wc ? dc0 : 0.f, wc ? dc1 : 0.f, wc ? dc2 : 0.f, wo ? dop : 0.f));
+                    if (dr != 0.f) atomicAdd(&p.d_radius[g], dr);
+                }
+            }
+        }
+        tail = __shfl_sync(kFullMask, em.y + __popc(mj), 31);   // the batch's pairs are free again
+    };
+
+    while (built < nb && built < R) {   // first fill: R batches (or what the pair ring holds)
+        stage();
+        try_commit();
+        if (pend) break;
+    }
+    __syncwarp();
+
+    int b = -1;
+    unsigned cur = 0u;
+    int soff = 0;
+    auto advance = [&]() {
+        ++b;
+        soff = (b & (R - 1)) * 32;
+        cur = ring.bits[soff + lane];
+    };
+    for (;;) {
+#pragma unroll
+        for (int it = 0; it < kRingInner; ++it) {
+            if (cur == 0u && b + 1 < built) advance();
+            const bool has = cur != 0u;
+            const int k = 31 - __clz(cur);   // highest remaining entry (back to front)
+            cur &= ~(1u << (k & 31));
+            float4 A, B;
+            float2 Zl;
+            uint2 em;
+            if (has) {   // predicated loads: idle lanes add no shared-memory traffic
+                A = ring.A[soff + k];
+                B = ring.B[soff + k];
+                Zl = *reinterpret_cast<const float2 *>(&ring.Z[soff + k]);
+                em = ring.EM[soff + k];
+            }
+            const float d2 = pair_d2(pxf, pyf, A.x, A.y);
+            float om = 0.f, dAe = 0.f;
+            if (has && d2 <= A.z) {   // composited: the forward's exact decision
+                float wgt;
+                const float a = pair_alpha(d2, A.w, B.w, Zl.y, wgt);   // the forward's α
+                const bool aclamp = d2 <= Zl.y;
+                const float oma = 1.0f - a;
+                const float Ti = T * rcp_approx(oma);
+                om = a * Ti;
+                const float fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (Zl.x - rz);
+                dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
+                Fb = a * fi + oma * Fb;
+                Tb = oma * Tb;
+                T = Ti;
+            }
+            if (has) pairs[(em.y + __popc(em.x & lmlt)) & (CP - 1)] = make_float2(om, dAe);
+        }
+        while (cur == 0u && b + 1 < built) advance();
+        const bool live = cur != 0u || b + 1 < nb;
+        if (!__any_sync(kFullMask, live)) break;
+        const unsigned need = !live ? 0x7fffffffu : (unsigned)(cur ? b : b + 1);   // earliest batch still needed
+        const int lo = (int)__reduce_min_sync(kFullMask, need);
+        if (flushed < lo && flushed < built) {
+            __syncwarp();   // phase 1's pair stores before phase 2's loads
+            do reduce(flushed++);
+            while (flushed < lo && flushed < built);
+        }
+        const bool blocked = cur == 0u && b + 1 < nb && b + 1 >= built;
+        if (__any_sync(kFullMask, blocked)) {   // lazy build: up to the furthest batch a live lane needs
+            const int hi = (int)__reduce_max_sync(kFullMask, live ? need : 0u);
+            const int target = min(min(nb, flushed + R), hi + 1);
+            if (pend) try_commit();
+            while (!pend && built < target) {
+                stage();
+                try_commit();
+            }
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+    while (flushed < built) reduce(flushed++);
+
+    if (LOSS) {   // fixed-order loss reduction: lanes → warp → CTA (the rows k_loss_finalize sums)
+        double v = up.lossv;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+        __shared__ double sRedL[kBwdWarps];
+        if (lane == 0) sRedL[wl_] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {   // k_loss_finalize reads column 12 only
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < kBwdWarps; ++i) s += sRedL[i];
+            p.partials[(size_t)blockIdx.x * 16 + 12] = s;
+        }
+    }
+}
+
 // mask counts for the mean-normalised loss (normalize = 1)
 __global__ void __launch_bounds__(256) k_l1_count(const float *__restrict__ sil, const float *__restrict__ tD,
                                                   const uint8_t *__restrict__ vis, int npx, int cmode,
@@ -793,6 +1061,26 @@ static int bwd_carveout() {
     return v;
 }
 
+static int bwd_ring() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("VTGS_BWD_RING");
+        v = e ? atoi(e) : 0;   // 1: the mapping backward (attributes only) as a ring walk
+    }
+    return v;
+}
+constexpr int kBwdRingR = 4;
+constexpr size_t kBwdRingSmem = kBwdWarps * bwd_ring_warp_bytes<kBwdRingR>();
+
+template <bool L>
+static cudaError_t set_bwd_ring_attr() {
+    cudaError_t e = cudaFuncSetAttribute(k_composite_bwd_ring<kBwdRingR, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kBwdRingSmem);
+    if (!e) e = cudaFuncSetAttribute(k_composite_bwd_ring<kBwdRingR, L>,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return e;
+}
+
 template <bool A, bool P, bool L>
 static cudaError_t set_bwd_attr() {
     cudaError_t e = cudaFuncSetAttribute(k_composite_bwd<A, P, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -824,6 +1112,8 @@ cudaError_t backward_set_attributes() {
     if (!e) e = set_bwd_attr<true, false, true>();
     if (!e) e = set_bwd_attr<true, true, false>();
     if (!e) e = set_bwd_attr<true, true, true>();
+    if (!e) e = set_bwd_ring_attr<false>();
+    if (!e) e = set_bwd_ring_attr<true>();
     return e;
 }
 
@@ -885,6 +1175,10 @@ cudaError_t launch_backward(Ctx &c, const float *dC, const float *dD, const floa
         static_assert(kPoseRingWarps == kBwdWarps, "k_pose_finalize rows: one partial per CTA of kBwdWarps warps");
         if (L) k_composite_bwd_pose_ring<R, true><<<T * (8 / kPoseRingWarps), kPoseRingWarps * 32, sm, s>>>(a);
         else k_composite_bwd_pose_ring<R, false><<<T * (8 / kPoseRingWarps), kPoseRingWarps * 32, sm, s>>>(a);
+    } else if (A && !P && !X && bwd_ring()) {   // mapping: attribute gradients, ring walk
+        LaunchScope ls(&c, kCompBwd, s);
+        if (L) k_composite_bwd_ring<kBwdRingR, true><<<T * (8 / kBwdWarps), kBwdWarps * 32, kBwdRingSmem, s>>>(a);
+        else k_composite_bwd_ring<kBwdRingR, false><<<T * (8 / kBwdWarps), kBwdWarps * 32, kBwdRingSmem, s>>>(a);
     } else {
     {
     LaunchScope ls(&c, kCompBwd, s);

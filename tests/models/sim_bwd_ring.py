@@ -30,7 +30,7 @@ def main(n_sub=300, seed=0):
     ntx = (intr.width + 15) // 16
     T = len(start) - 1
     rng = np.random.default_rng(seed)
-    confs = [(R, C) for R in (2, 4, 8, 16) for C in (1024, 2048, 4096)]
+    confs = [(R, C) for R in (2, 4, 8) for C in (512, 768, 1024)]
     steps = {c: 0 for c in confs}
     lock = 0
     wins = [(2, 1024), (4, 1024), (4, 2048), (8, 2048)]
