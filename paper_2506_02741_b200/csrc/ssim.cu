@@ -8,24 +8,32 @@
 // vertical pass 4 consecutive outputs of a column from 14 staged row sums.
 //   K_ssim_moments: 11-tap sums of x, y, x², y², xy → SSIM_p and the three per-pixel chain
 //     factors a = dL/dS·∂S/∂μx, b = dL/dS·∂S/∂E[x²], c = dL/dS·∂S/∂E[xy] (9 floats / pixel to
-//     scratch) and a per-CTA partial of Σ SSIM;
+//     scratch) and a per-CTA partial of Σ SSIM; the last CTA to finish (ticket) sums the partials
+//     in a fixed order → loss = τ (1 − Σ S / 3HW) (no separate finalize launch);
 //   K_ssim_grad: the adjoint stencil (the window is symmetric, zero padding ⇒ the same filter)
 //     dL/dx_q = (G⋆a)_q + 2 x_q (G⋆b)_q + y_q (G⋆c)_q, ACCUMULATED into d_color;
-//   K_ssim_finalize: fixed-order sum of the partials → loss = τ (1 − Σ S / 3HW).
 #include "vtgs_internal.cuh"
 
 namespace vtgs {
 
 constexpr int kSsTX = 64, kSsTY = 16, kSsR = 5, kSsThreads = 256;
 constexpr int kSsW = kSsTX + 2 * kSsR, kSsH = kSsTY + 2 * kSsR;   // 74 × 26 input tile
+constexpr int kSsWp = kSsW + 1;    // staged row stride (odd: the row-per-lane reads spread over banks)
 constexpr int kHSeg = 8;                                          // horizontal outputs per thread
 constexpr int kVSeg = 4;                                          // vertical outputs per thread
+constexpr int kHTasks = kSsH * (kSsTX / kHSeg);                   // 208 (row, segment) tasks
 __constant__ float c_ssim_w[11];
 constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
 
+// Horizontal-pass ownership: lane-consecutive tasks take consecutive ROWS of one 8-column segment
+// (row = t mod 26), and the row sums are stored XOR-swizzled (column ^ row): a warp's stores of
+// one output column hit 32 distinct banks, and the vertical pass (consecutive columns of one row)
+// reads through the same swizzle conflict-free.
+__device__ __forceinline__ int hm_col(int r, int q) { return q ^ (r & 31); }
+
 // Stage one channel of NQ planes (tile + halo, zero outside the image) into s[q][r][c].
 template <int NQ>
-__device__ __forceinline__ void ss_load(float (*s)[kSsH][kSsW], const float *const *src, int c, size_t stride_q,
+__device__ __forceinline__ void ss_load(float (*s)[kSsH][kSsWp], const float *const *src, int c, size_t stride_q,
                                         bool interleaved, int ox, int oy, int W, int H) {
     for (int i = threadIdx.x; i < kSsH * kSsW; i += kSsThreads) {
         const int r = i / kSsW, q = i - r * kSsW;
@@ -38,28 +46,30 @@ __device__ __forceinline__ void ss_load(float (*s)[kSsH][kSsW], const float *con
     }
 }
 
-__global__ void __launch_bounds__(kSsThreads) k_ssim_moments(const float *__restrict__ x,
+__global__ void __launch_bounds__(kSsThreads, 4) k_ssim_moments(const float *__restrict__ x,
                                                             const float *__restrict__ y, int W, int H,
                                                             float dLdS, float *__restrict__ abc,
-                                                            double *__restrict__ partials) {
-    __shared__ float sin[2][kSsH][kSsW];
+                                                            double *__restrict__ partials, double npx3, float tau,
+                                                            float *__restrict__ loss_out,
+                                                            unsigned int *__restrict__ ticket) {
+    __shared__ float sin[2][kSsH][kSsWp];
     __shared__ float hm[5][kSsH][kSsTX];
     __shared__ double red[kSsThreads / 32];
+    __shared__ bool last;
     const int ox = blockIdx.x * kSsTX, oy = blockIdx.y * kSsTY;
     const size_t npx = (size_t)W * H;
     const float *srcs[2] = {x, y};
     // vertical-pass ownership: column vc, rows vr .. vr + kVSeg − 1
     const int vc = threadIdx.x & (kSsTX - 1), vr = (threadIdx.x / kSsTX) * kVSeg;
+    const int hr = threadIdx.x % kSsH, hq0 = (threadIdx.x / kSsH) * kHSeg;   // horizontal task
     double ssum = 0.0;
     for (int c = 0; c < 3; ++c) {
         ss_load<2>(sin, srcs, c, 0, true, ox, oy, W, H);
         __syncthreads();
-        // horizontal pass: (row, 8-column segment) per thread
-        for (int i = threadIdx.x; i < kSsH * (kSsTX / kHSeg); i += kSsThreads) {
-            const int r = i / (kSsTX / kHSeg), q0 = (i - r * (kSsTX / kHSeg)) * kHSeg;
+        if (threadIdx.x < kHTasks) {   // horizontal pass: 8 consecutive outputs of one row
             float a[kHSeg + 10], b[kHSeg + 10];
 #pragma unroll
-            for (int k = 0; k < kHSeg + 10; ++k) { a[k] = sin[0][r][q0 + k]; b[k] = sin[1][r][q0 + k]; }
+            for (int k = 0; k < kHSeg + 10; ++k) { a[k] = sin[0][hr][hq0 + k]; b[k] = sin[1][hr][hq0 + k]; }
 #pragma unroll
             for (int o = 0; o < kHSeg; ++o) {
                 float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
@@ -72,8 +82,9 @@ __global__ void __launch_bounds__(kSsThreads) k_ssim_moments(const float *__rest
                     m3 = fmaf(w, v * v, m3);
                     m4 = fmaf(w, u * v, m4);
                 }
-                hm[0][r][q0 + o] = m0; hm[1][r][q0 + o] = m1; hm[2][r][q0 + o] = m2;
-                hm[3][r][q0 + o] = m3; hm[4][r][q0 + o] = m4;
+                const int q = hm_col(hr, hq0 + o);
+                hm[0][hr][q] = m0; hm[1][hr][q] = m1; hm[2][hr][q] = m2;
+                hm[3][hr][q] = m3; hm[4][hr][q] = m4;
             }
         }
         __syncthreads();
@@ -82,7 +93,7 @@ __global__ void __launch_bounds__(kSsThreads) k_ssim_moments(const float *__rest
         for (int m = 0; m < 5; ++m) {
             float col[kVSeg + 10];
 #pragma unroll
-            for (int k = 0; k < kVSeg + 10; ++k) col[k] = hm[m][vr + k][vc];
+            for (int k = 0; k < kVSeg + 10; ++k) col[k] = hm[m][vr + k][hm_col(vr + k, vc)];
 #pragma unroll
             for (int o = 0; o < kVSeg; ++o) {
                 float s = 0.f;
@@ -115,38 +126,61 @@ __global__ void __launch_bounds__(kSsThreads) k_ssim_moments(const float *__rest
     for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ssum;
     __syncthreads();
+    const int nblk = gridDim.x * gridDim.y;
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int i = 0; i < kSsThreads / 32; ++i) t += red[i];
         partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+        last = false;
+        if (loss_out) {   // the last CTA to finish sums the partials (no finalize launch)
+            __threadfence();
+            last = atomicAdd(ticket, 1u) == (unsigned)nblk - 1u;
+        }
+    }
+    __syncthreads();
+    if (last) {   // fixed order: strided per-thread sums, then a tree (deterministic)
+        __threadfence();
+        double *tree = reinterpret_cast<double *>(&hm[0][0][0]);   // the row sums are dead now
+        double t = 0.0;
+        for (int i = threadIdx.x; i < nblk; i += kSsThreads) t += __ldcg(partials + i);
+        tree[threadIdx.x] = t;
+        __syncthreads();
+        for (int o = kSsThreads / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o) tree[threadIdx.x] += tree[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            *loss_out = (float)((double)tau * (1.0 - tree[0] / npx3));
+            *ticket = 0u;
+        }
     }
 }
 
 __global__ void __launch_bounds__(kSsThreads) k_ssim_grad(const float *__restrict__ x, const float *__restrict__ y,
                                                          int W, int H, const float *__restrict__ abc,
                                                          float *__restrict__ d_color) {
-    __shared__ float sa[3][kSsH][kSsW];
+    __shared__ float sa[3][kSsH][kSsWp];
     __shared__ float hm[3][kSsH][kSsTX];
     const int ox = blockIdx.x * kSsTX, oy = blockIdx.y * kSsTY;
     const size_t npx = (size_t)W * H;
     const float *srcs[3] = {abc, abc + 3 * npx, abc + 6 * npx};
     const int vc = threadIdx.x & (kSsTX - 1), vr = (threadIdx.x / kSsTX) * kVSeg;
+    const int hr = threadIdx.x % kSsH, hq0 = (threadIdx.x / kSsH) * kHSeg;
     for (int c = 0; c < 3; ++c) {
         ss_load<3>(sa, srcs, c, npx, false, ox, oy, W, H);
         __syncthreads();
-        for (int i = threadIdx.x; i < kSsH * (kSsTX / kHSeg); i += kSsThreads) {
-            const int r = i / (kSsTX / kHSeg), q0 = (i - r * (kSsTX / kHSeg)) * kHSeg;
+        if (threadIdx.x < kHTasks) {
 #pragma unroll
             for (int m = 0; m < 3; ++m) {
                 float a[kHSeg + 10];
 #pragma unroll
-                for (int k = 0; k < kHSeg + 10; ++k) a[k] = sa[m][r][q0 + k];
+                for (int k = 0; k < kHSeg + 10; ++k) a[k] = sa[m][hr][hq0 + k];
 #pragma unroll
                 for (int o = 0; o < kHSeg; ++o) {
                     float s = 0.f;
 #pragma unroll
                     for (int k = 0; k < 11; ++k) s = fmaf(c_ssim_w[k], a[o + k], s);
-                    hm[m][r][q0 + o] = s;
+                    hm[m][hr][hm_col(hr, hq0 + o)] = s;
                 }
             }
         }
@@ -156,7 +190,7 @@ __global__ void __launch_bounds__(kSsThreads) k_ssim_grad(const float *__restric
         for (int m = 0; m < 3; ++m) {
             float col[kVSeg + 10];
 #pragma unroll
-            for (int k = 0; k < kVSeg + 10; ++k) col[k] = hm[m][vr + k][vc];
+            for (int k = 0; k < kVSeg + 10; ++k) col[k] = hm[m][vr + k][hm_col(vr + k, vc)];
 #pragma unroll
             for (int o = 0; o < kVSeg; ++o) {
                 float s = 0.f;
@@ -175,20 +209,6 @@ __global__ void __launch_bounds__(kSsThreads) k_ssim_grad(const float *__restric
         }
         __syncthreads();
     }
-}
-
-__global__ void k_ssim_finalize(const double *__restrict__ partials, int n, double npx3, float tau,
-                                float *__restrict__ loss_out) {
-    __shared__ double red[256];
-    double s = 0.0;
-    for (int i = threadIdx.x; i < n; i += 256) s += partials[i];
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *loss_out = (float)((double)tau * (1.0 - red[0] / npx3));
 }
 
 cudaError_t ssim_set_constants() {
@@ -210,17 +230,13 @@ cudaError_t launch_ssim(Ctx &c, const float *color, const float *target, int W, 
     cudaError_t e;
     {
         LaunchScope ls(&c, kSsim, s);
-        k_ssim_moments<<<grid, kSsThreads, 0, s>>>(color, target, W, H, dLdS, c.ssim_abc, c.ssim_partials);
+        k_ssim_moments<<<grid, kSsThreads, 0, s>>>(color, target, W, H, dLdS, c.ssim_abc, c.ssim_partials, n3, tau,
+                                                   loss_out, &c.dev->ssim_ticket);
         if ((e = cudaGetLastError())) return e;
     }
     if (d_color) {
         LaunchScope ls(&c, kSsim, s);
         k_ssim_grad<<<grid, kSsThreads, 0, s>>>(color, target, W, H, c.ssim_abc, d_color);
-        if ((e = cudaGetLastError())) return e;
-    }
-    if (loss_out) {
-        LaunchScope ls(&c, kSsim, s);
-        k_ssim_finalize<<<1, 256, 0, s>>>(c.ssim_partials, (int)(grid.x * grid.y), n3, tau, loss_out);
         if ((e = cudaGetLastError())) return e;
     }
     return cudaSuccess;

@@ -58,6 +58,7 @@ struct DevScalars {
     unsigned int radix_count; // entries in the radix-sort work list (Ctx::tile_flag)
     unsigned int chunk_count; // chunks of long tiles planned by plan_tile (Ctx::chunk_list)
     unsigned int chunk_next;  // their dynamic fetch cursor
+    unsigned int ssim_ticket; // k_ssim_moments last-block ticket (self-resetting)
 };
 
 enum Stage { kProject = 0, kScan, kEmit, kSort, kCompFwd, kL1Count, kCompBwd, kFinalize, kInstantiate,
