@@ -11,6 +11,7 @@
 //   * pose gradient (tracking): each lane chains its pairs straight into 12 register
 //     accumulators (Σ g, Σ X_c gᵀ), reduced per CTA in fp64 into a per-tile partial; a
 //     one-CTA kernel sums the partials in a fixed order and applies the rotation chain.
+#include <stddef.h>
 #include <stdlib.h>
 
 #include "composite_common.cuh"
@@ -59,6 +60,14 @@ struct BwdArgs {
 constexpr double kDetScale = 1099511627776.0;   // 2^40: resolution 9.1e-13, range ±8.4e6
 __device__ __forceinline__ void det_add(unsigned long long *q, float v) {
     if (v != 0.f) atomicAdd(q, (unsigned long long)__double2ll_rn((double)v * kDetScale));
+}
+
+// index of the highest set bit (bfind: one FLO; 0xffffffff for 0) — `31 − __clz` costs the
+// compiler an extra subtract and an XOR per use
+__device__ __forceinline__ int msb_index(unsigned x) {
+    unsigned r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return (int)r;
 }
 
 __device__ __forceinline__ float sgnf(float r) { return (float)((r > 0.0f) - (r < 0.0f)); }
@@ -134,12 +143,17 @@ __device__ __forceinline__ PixelUp pixel_upstream(const BwdArgs &p, int px, int 
 //             applied per (Gaussian, sub-tile) into the lane's 12 accumulators.
 // One warp per 8×4 sub-tile, kBwdWarps warps per CTA, no block barriers.
 constexpr int kBwdWarps = 2;
+struct __align__(16) BwdStage {
+    float4 A[32];   // u, v, D_c, escale
+    float4 B[32];   // c, o
+    float2 L[32];   // z, D_clamp
+};
 
 template <bool ATTR, bool POSE, bool LOSS, int MINB = 1>
 __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs p) {
-    __shared__ float4 sA[kBwdWarps][32];             // u, v, D_c, escale
-    __shared__ float4 sB[kBwdWarps][32];             // c, o
-    __shared__ float2 sL[kBwdWarps][32];             // z, D_clamp
+    // per warp, one block: A (u, v, D_c, escale) | B (c, o) | L (z, D_clamp) — one base register
+    // and immediate offsets address all three of a candidate's loads
+    __shared__ BwdStage sS[kBwdWarps];
     __shared__ float4 sX[kBwdWarps][POSE ? 32 : 1];  // X_c and ±σ (−: σ clamped)
     __shared__ float4 sG[kBwdWarps][32];             // per pixel (g_C, g_D)
     // [kBwdWarps][32 entries][32 pixels]: phase 1 writes column = own lane (conflict-free per
@@ -152,6 +166,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
     const int wl_ = threadIdx.x >> 5;
     const int sub = gsub & 7;  // sub-tile 0..7 of the tile
     float2 (*M)[32] = reinterpret_cast<float2 (*)[32]>(sMdyn + (size_t)wl_ * 32 * 32);
+    const char *sbase = reinterpret_cast<const char *>(&sS[wl_]);
     const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
     const unsigned lane = lane_id();
     const int sx = tx * kTile + (sub & 1) * 8, sy = ty * kTile + (sub >> 1) * 4;
@@ -206,9 +221,9 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
             const float s = fabsf(cur.pr.w);
             s2j = __fmul_rn(s, s);
             const float2 th = thr_unpack(cur.th, s2j);
-            sA[wl_][lane] = make_float4(cur.pr.x, cur.pr.y, th.x, exp_scale(s2j));
-            sB[wl_][lane] = cur.co;
-            sL[wl_][lane] = make_float2(cur.pr.z, th.y);
+            sS[wl_].A[lane] = make_float4(cur.pr.x, cur.pr.y, th.x, exp_scale(s2j));
+            sS[wl_].B[lane] = cur.co;
+            sS[wl_].L[lane] = make_float2(cur.pr.z, th.y);
             if (POSE)   // camera-space centre from the projection (x = (u − cx)·z / fx, …)
                 sX[wl_][lane] = make_float4((cur.pr.x - p.in.cx) * cur.pr.z * rcp_approx(p.in.fx),
                                             (cur.pr.y - p.in.cy) * cur.pr.z * rcp_approx(p.in.fy), cur.pr.z, cur.pr.w);
@@ -229,9 +244,10 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
             float4 A, B;
             float2 lo;
             if (v) {   // predicated loads: lanes without a candidate add no shared-memory traffic
-                A = sA[wl_][k];
-                B = sB[wl_][k];
-                lo = sL[wl_][k];
+                const char *pk = sbase + 16 * k;
+                A = *reinterpret_cast<const float4 *>(pk);
+                B = *reinterpret_cast<const float4 *>(pk + offsetof(BwdStage, B));
+                lo = *reinterpret_cast<const float2 *>(sbase + offsetof(BwdStage, L) + 8 * k);
             }
             const float d2 = pair_d2(pxf, pyf, A.x, A.y);
             comp = v && d2 <= A.z;         // the forward's exact decision (3σ and the α floor)
@@ -240,32 +256,31 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
             rc = rcp_approx(1.0f - a);
             fi = g0 * (B.x - r0) + g1 * (B.y - r1) + g2 * (B.z - r2) + gD * (lo.x - rz);
         };
-        auto stage_b = [&](int k, bool comp, bool aclamp, float a, float rc, float wgt, float fi) {
-            float om = 0.f, dAe = 0.f;
-            if (comp) {
-                const float oma = 1.0f - a;
-                const float Ti = T * rc;
-                om = a * Ti;
-                // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
-                dAe = aclamp ? 0.f : Ti * (fi - Fb + Kr * Tb) * wgt;
-                Fb = a * fi + oma * Fb;
-                Tb = oma * Tb;
-                T = Ti;
-            }
-            M[k][lane] = make_float2(om, dAe);
+        // branch-free: every value is computed and a pair that was not composited selects the
+        // old state (a branch here cost a reconvergence per pair)
+        auto stage_b = [&](int k, bool comp, bool aclamp, float a, float rc, float wgt, float fi, bool store) {
+            const float oma = 1.0f - a;
+            const float Ti = T * rc;
+            const float om = comp ? a * Ti : 0.f;
+            // M.y = dL/dα · w (0 when α is clamped): phase 2 needs only that product
+            const float dAe = (comp && !aclamp) ? Ti * (fi - Fb + Kr * Tb) * wgt : 0.f;
+            Fb = comp ? a * fi + oma * Fb : Fb;
+            Tb = comp ? oma * Tb : Tb;
+            T = comp ? Ti : T;
+            if (store) M[k][lane] = make_float2(om, dAe);   // predicated: no second candidate, no store
         };
         while (bits) {
-            const int k0 = 31 - __clz(bits);
-            bits &= ~(1u << k0);
+            const int k0 = msb_index(bits);
+            bits ^= 1u << k0;
             const bool v1 = bits != 0u;
-            const int k1 = (31 - __clz(bits)) & 31;
-            if (v1) bits &= ~(1u << k1);
+            const int k1 = msb_index(bits) & 31;
+            if (v1) bits ^= 1u << k1;
             float a0, rc0, w0, f0, a1, rc1, w1, f1;
             bool c0, cl0, c1, cl1;
             stage_a(k0, true, a0, rc0, w0, f0, c0, cl0);
             stage_a(k1, v1, a1, rc1, w1, f1, c1, cl1);
-            stage_b(k0, c0, cl0, a0, rc0, w0, f0);
-            if (v1) stage_b(k1, c1, cl1, a1, rc1, w1, f1);
+            stage_b(k0, c0, cl0, a0, rc0, w0, f0, true);
+            stage_b(k1, c1, cl1, a1, rc1, w1, f1, v1);   // c1 is false without a second candidate
         }
         __syncwarp();
         // ---- phase 2: lane = entry, over the pixels that composited it, two pixels per
@@ -276,20 +291,19 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
             float dc0 = 0.f, dc1 = 0.f, dc2 = 0.f, dop = 0.f, sw2 = 0.f, swx = 0.f, swy = 0.f, dzd = 0.f;
             unsigned mm = __funnelshift_r(mj, mj, lane);  // rotate right by lane
             const float ux = cur.pr.x, uy = cur.pr.y;
+            // branch-free: a pair that was not composited holds (0, 0) in M and adds exact zeros
             auto accum = [&](int i, float2 md, float4 gp) {
-                if (md.x != 0.f) {   // composited (ω > 0 for every composited pair)
-                    dc0 = fmaf(gp.x, md.x, dc0);
-                    dc1 = fmaf(gp.y, md.x, dc1);
-                    dc2 = fmaf(gp.z, md.x, dc2);
-                    dzd = fmaf(gp.w, md.x, dzd);
-                    const float dx = (float)(sx + (i & 7)) - ux, dy = (float)(sy + (i >> 3)) - uy;
-                    const float d2 = dx * dx + dy * dy;
-                    const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution; 0 when α clamped)
-                    dop += dw;
-                    sw2 = fmaf(dw, d2, sw2);
-                    swx = fmaf(dw, dx, swx);
-                    swy = fmaf(dw, dy, swy);
-                }
+                dc0 = fmaf(gp.x, md.x, dc0);
+                dc1 = fmaf(gp.y, md.x, dc1);
+                dc2 = fmaf(gp.z, md.x, dc2);
+                dzd = fmaf(gp.w, md.x, dzd);
+                const float dx = (float)(sx + (i & 7)) - ux, dy = (float)(sy + (i >> 3)) - uy;
+                const float d2 = dx * dx + dy * dy;
+                const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution; 0 when α clamped)
+                dop += dw;
+                sw2 = fmaf(dw, d2, sw2);
+                swx = fmaf(dw, dx, swx);
+                swy = fmaf(dw, dy, swy);
             };
             while (mm) {
                 const int i0 = ((__ffs(mm) - 1) + (int)lane) & 31;
@@ -300,13 +314,13 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
                 const float2 md0 = M[lane][i0];
                 const float4 gp0 = sG[wl_][i0];
                 float2 md1 = make_float2(0.f, 0.f);
-                float4 gp1;
+                float4 gp1 = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (v1) {
                     md1 = M[lane][i1];
                     gp1 = sG[wl_][i1];
                 }
                 accum(i0, md0, gp0);
-                accum(i1, md1, gp1);   // md1.x == 0 when there is no second pixel
+                accum(i1, md1, gp1);   // zeros when there is no second pixel
             }
             // dL/dw·w = dL/dα·o·w;  ∂w/∂σ = w d²/σ³, ∂w/∂u = w (x−u)/σ², ∂w/∂v = w (y−v)/σ²
             const float s = fabsf(cur.pr.w);
@@ -358,12 +372,12 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
         }
         if (lane == 0)
 #pragma unroll
-            for (int q = 0; q < 13; ++q) reinterpret_cast<double *>(&sA[wl_][0])[q] = v[q];
+            for (int q = 0; q < 13; ++q) reinterpret_cast<double *>(&sS[wl_].A[0])[q] = v[q];
         __syncthreads();
         if (threadIdx.x < 13) {
             double s = 0.0;
 #pragma unroll
-            for (int i = 0; i < kBwdWarps; ++i) s += reinterpret_cast<const double *>(&sA[i][0])[threadIdx.x];
+            for (int i = 0; i < kBwdWarps; ++i) s += reinterpret_cast<const double *>(&sS[i].A[0])[threadIdx.x];
             p.partials[(size_t)blockIdx.x * 16 + threadIdx.x] = s;
         }
     }
