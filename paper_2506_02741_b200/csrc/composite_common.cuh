@@ -197,20 +197,23 @@ __device__ __forceinline__ float pair_d2(float xf, float yf, float u, float v) {
 __device__ __forceinline__ unsigned lane_mask(const float4 A, const uint2 r, int sx, int sy) {
     const int x0 = max((int)(r.x & 0xffffu), sx), x1 = min((int)(r.x >> 16), sx + 7);
     const int y0 = max((int)(r.y & 0xffffu), sy), y1 = min((int)(r.y >> 16), sy + 3);
+    const float fsy = (float)sy;
     unsigned m = 0;
-    if (x0 > x1) return 0u;
-    for (int y = y0; y <= y1; ++y) {
-        const float dy = __fsub_rn((float)y, A.y);
+    // the sub-tile's 4 rows, branch-free (lanes are entries with different row ranges: a loop
+    // over each entry's rows diverged); a row outside the rect or the disc selects 0
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float dy = __fsub_rn(fsy + (float)j, A.y);
         const float dy2 = __fmul_rn(dy, dy);
-        if (!(dy2 <= A.z)) continue;
         // the exact test accepts |dx| up to √(r2 + ½ulp(9σ²)) (dx² + dy² rounds down onto 9σ²):
         // widen by A.z·2⁻²³ ≥ ½ulp before the root, then by 0.01 px for the approximate rsqrt
-        const float r2 = A.z - dy2 + A.z * 1.1920929e-7f;           // ≥ 0
+        const float r2 = A.z - dy2 + A.z * 1.1920929e-7f;           // ≥ 0 on a kept row
         const float hw = r2 * rsqrt_approx(fmaxf(r2, 1e-30f)) + 0.01f; // √r2 (+ ≤ 2⁻²² rel.) + margin
         const int xa = max(x0, (int)ceilf(A.x - hw)), xb = min(x1, (int)floorf(A.x + hw));
-        if (xa > xb) continue;
-        const unsigned row = (0xffu >> (7 - (xb - sx))) & (0xffu << (xa - sx));
-        m |= row << (8 * (y - sy));
+        const bool ok = sy + j >= y0 && sy + j <= y1 && dy2 <= A.z && xa <= xb;
+        const unsigned lo = (unsigned)min(max(xa - sx, 0), 7), hi = (unsigned)min(max(xb - sx, 0), 7);
+        const unsigned row = (0xffu >> (7u - hi)) & (0xffu << lo);
+        m |= ok ? row << (8 * j) : 0u;
     }
     return m;
 }
