@@ -771,7 +771,9 @@ __global__ void __launch_bounds__(NT, 2048 / NT) k_tile_sort_bucket(const uint32
     static_assert((1 << kLogNB) == NB, "NB must be 1024 … 8192");
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t base = tile_start[tile];
-    uint32_t *K = sm, *V = sm + CAP, *K2 = sm + 2 * CAP, *V2 = sm + 3 * CAP, *H = sm + 4 * CAP;
+    // KV2: the bucketed (key, gid) pairs interleaved, so the rank loop compares one 64-bit word
+    uint32_t *K = sm, *V = sm + CAP, *H = sm + 4 * CAP;
+    unsigned long long *KV2 = reinterpret_cast<unsigned long long *>(sm + 2 * CAP);
     uint8_t *B = reinterpret_cast<uint8_t *>(sm + 4 * CAP + NB), *B2 = B + CAP;
     uint32_t kmin = 0xffffffffu, kmax = 0u;
     for (int i = tid; i < n; i += NT) {
@@ -850,20 +852,17 @@ __global__ void __launch_bounds__(NT, 2048 / NT) k_tile_sort_bucket(const uint32
     for (int i = tid; i < n; i += NT) {
         const uint32_t k = K[i];
         const uint32_t pos = atomicAdd(&H[(k - kmin) >> shift], 1u);  // H[b] becomes the segment end
-        K2[pos] = k;
-        V2[pos] = V[i];
+        KV2[pos] = ((unsigned long long)k << 32) | V[i];
         B2[pos] = B[i];
     }
     __syncthreads();
     for (int p = tid; p < n; p += NT) {
-        const uint32_t k = K2[p], v = V2[p];
+        const unsigned long long kv = KV2[p];   // (key, gid): the order is that of the 64-bit word
+        const uint32_t k = (uint32_t)(kv >> 32), v = (uint32_t)kv;
         const uint32_t b = (k - kmin) >> shift;
         const int s0 = b ? (int)H[b - 1] : 0, s1 = (int)H[b];
         int rank = 0;
-        for (int j = s0; j < s1; ++j) {
-            const uint32_t kj = K2[j];
-            rank += (kj < k || (kj == k && V2[j] < v)) ? 1 : 0;
-        }
+        for (int j = s0; j < s1; ++j) rank += KV2[j] < kv ? 1 : 0;
         V[s0 + rank] = v;
         B[s0 + rank] = B2[p];
     }
