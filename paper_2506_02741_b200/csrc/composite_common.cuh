@@ -183,6 +183,13 @@ __device__ __forceinline__ float pair_alpha(float d2, float escale, float o, flo
     return d2 <= dcl ? kAlphaMax : fminf(o * w, kAlphaMax);
 }
 
+// pair_alpha with dcl = −1 (the forward): d² ≥ 0 never passes d² ≤ −1, so the same value
+// without the compare and select the compiler cannot drop
+__device__ __forceinline__ float pair_alpha_value(float d2, float escale, float o, float &w) {
+    w = fast_exp2(d2 * escale);
+    return fminf(o * w, kAlphaMax);
+}
+
 // d² of pixel (xf, yf) to centre (u, v), DESIGN.md §3 step 7 (no FMA contraction)
 __device__ __forceinline__ float pair_d2(float xf, float yf, float u, float v) {
     const float dx = __fsub_rn(xf, u), dy = __fsub_rn(yf, v);

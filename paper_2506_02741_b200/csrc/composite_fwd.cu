@@ -107,8 +107,10 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
     // lane state: batch b, its remaining candidate bits cur (bit 31 − j = entry j, so the lowest
     // remaining entry is the highest set bit, one FLO), the address of the batch's entry 31,
     // and 1 + the sub-list position of its entry 31.
-    // Finished (terminated, walked the whole list, or outside the image) ⇔ cur == 0 && b + 1 ≥ nb.
-    int b = inside ? -1 : nb;
+    // Finished (terminated, walked the whole list, or outside the image) ⇔ cur == 0 && b + 1 ≥ nb
+    // (terminated and outside lanes park at b = kDoneB).
+    constexpr int kDoneB = 0x3fffffff;   // b of a finished lane: b + 1 ≥ nb and ≥ built
+    int b = inside ? -1 : kDoneB;
     unsigned cur = 0u;
     int soff = 0;
     int lbase = 0;
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
             const float d2 = pair_d2(pxf, pyf, A.x, A.y);
             const bool comp = has && d2 <= A.z;            // 3σ truncation and α floor, exact
             float w;
-            const float a = pair_alpha(d2, A.w, Bc.w, -1.0f, w);   // value only (clamp decision: backward)
+            const float a = pair_alpha_value(d2, A.w, Bc.w, w);   // value only (clamp decision: backward)
             const float Tn = __fmul_rn(T, __fsub_rn(1.0f, a));
             const bool term = comp && Tn < kTMin;
             const bool acc = comp && !term;
@@ -158,9 +160,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
                 ne += (has && d2 <= s9) ? 1u : 0u;
                 nc += acc ? 1u : 0u;
             }
-            if (term) {
+            if (term) {   // finished: past every batch (a constant, so nb need not stay live)
                 cur = 0u;
-                b = nb;
+                b = kDoneB;
             }
         }
         // lanes whose next word was empty: catch up before the warp-level check
