@@ -641,36 +641,55 @@ def main():
     peaks_json = {"fp32_tflops_measured": fp32_meas, "ex2_per_s_measured": ex2_meas,
                   "fp32_tflops_nominal": fp32_nominal, "hbm_gbs": hbm_peak, "hbm_source": peak_src}
 
-    # ---------------- e2e: the same step through the C-ABI with HOST buffers
+    # ---------------- e2e: the same step through the C-ABI with HOST buffers.  Headline: the frame
+    # as an RGB-D sensor (and the paper's datasets) delivers it — 8-bit RGB, 16-bit depth (metres =
+    # value / 5000) — uploaded as 5 B/px and widened on the device (vtgs_step_host_sensor); also
+    # timed: the same step with fp32 host targets (16 B/px, vtgs_step_host).
     e2e = None
     if not args.profile_run:
-        h_tg = [(torch.from_numpy(t.rgb).pin_memory(), torch.from_numpy(t.depth).pin_memory()) for t in tgts]
+        depth_scale = np.float32(1.0 / 5000.0)
         h_views = [torch.from_numpy(v.reshape(7).copy()).pin_memory() for v in views_np]
-        for _ in range(max(args.warmup, 20)):   # fresh pinned buffers and an idle host: let them settle
-            grads.zero_()
-            for hv, (hr, hd) in zip(h_views, h_tg):
-                R.step_host(pr, co, hv, cfg.intr, hr, hd, wc, wd, 0, 0, 0, want, (0, N), out, d_co, d_r)
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            grads.zero_()
-            for hv, (hr, hd) in zip(h_views, h_tg):
-                R.step_host(pr, co, hv, cfg.intr, hr, hd, wc, wd, 0, 0, 0, want, (0, N), out, d_co, d_r)
+        h_tg = [(torch.from_numpy(t.rgb).pin_memory(), torch.from_numpy(t.depth).pin_memory()) for t in tgts]
+        h_sn = [(torch.from_numpy(np.clip(np.rint(t.rgb * 255.0), 0, 255).astype(np.uint8)).pin_memory(),
+                 torch.from_numpy(np.clip(np.rint(t.depth / depth_scale), 0, 65535).astype(np.uint16)).pin_memory())
+                for t in tgts]
+
+        def e2e_run(sensor):
+            def one_step():
+                grads.zero_()
+                for hv, (hr, hd), (sr, sd) in zip(h_views, h_tg, h_sn):
+                    if sensor:
+                        R.step_host_sensor(pr, co, hv, cfg.intr, sr, sd, float(depth_scale), wc, wd, 0, 0, 0, want,
+                                           (0, N), out, d_co, d_r)
+                    else:
+                        R.step_host(pr, co, hv, cfg.intr, hr, hd, wc, wd, 0, 0, 0, want, (0, N), out, d_co, d_r)
+                if ws > 1:
+                    dist.all_reduce(grads)
+                    torch.cuda.synchronize()
+            for _ in range(max(args.warmup, 20)):   # fresh pinned buffers and an idle host: let them settle
+                one_step()
             if ws > 1:
-                dist.all_reduce(grads)
-                torch.cuda.synchronize()
-        torch.cuda.synchronize()
-        e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-        te = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-        if ws > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e_ms = float(te.item())
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                one_step()
+            torch.cuda.synchronize()
+            e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+            te = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            if ws > 1:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            return float(te.item())
+
+        e_ms = e2e_run(True)
+        f_ms = e2e_run(False)
         e2e = {"value": px_per_step / (e_ms * 1e-3) / 1e6, "unit": "Mpix/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": int(sum(hr.numel() * 4 + hd.numel() * 4 + 28 for hr, hd in h_tg)),
-               "d2h_bytes_per_step": 4 * len(h_tg),
-               "api": "vtgs_step_host (host target RGB-D + pose in, host loss out)"}
+               "h2d_bytes_per_step": int(sum(sr.numel() + sd.numel() * 2 + 28 for sr, sd in h_sn)),
+               "d2h_bytes_per_step": 4 * len(h_sn),
+               "api": "vtgs_step_host_sensor (host uint8 RGB + uint16 depth + pose in, host loss out)",
+               "fp32_targets": {"value": px_per_step / (f_ms * 1e-3) / 1e6, "ms_per_step": f_ms,
+                                "h2d_bytes_per_step": int(sum(hr.numel() * 4 + hd.numel() * 4 + 28 for hr, hd in h_tg)),
+                                "api": "vtgs_step_host (host fp32 RGB-D + pose in, host loss out)"}}
 
     # ---------------- cpu baseline (oracle as it stands, bounded sample, rank 0, N=1 only)
     cpu = None

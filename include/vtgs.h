@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define VTGS_ABI_VERSION 3
+#define VTGS_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define VTGS_API __attribute__((visibility("default")))
@@ -317,6 +317,22 @@ VTGS_API vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const f
                            int64_t learn_begin, int64_t learn_end, float *color, float *depth,
                            float *silhouette, float *d_col_opa, float *d_radius,
                            float *loss_host, float *d_pose_host, void *stream);
+
+/* vtgs_step_host with the target frame in the formats an RGB-D sensor (and the paper's datasets:
+ * 8-bit RGB, 16-bit depth images) deliver it: rgb8_host [H×W×3] uint8, depth16_host [H×W]
+ * uint16 (0 = no depth), depth_scale = metres per depth unit (e.g. 1/5000).  The 5 B/pixel are
+ * uploaded (instead of 16 B/pixel of fp32) on the context's copy stream and widened on the device
+ * right before the backward: c = v / 255 (IEEE fp32 division), z = d · depth_scale (one fp32
+ * multiply) — exactly the fp32 targets a host-side conversion with the same two operations gives,
+ * so the step equals vtgs_step_host on those targets.  Everything else as vtgs_step_host. */
+VTGS_API vtgs_status vtgs_step_host_sensor(vtgs_ctx *ctx, const float *pos_rad, const float *col_opa, int64_t N,
+                                  const vtgs_pose *view_host, vtgs_intrinsics intr,
+                                  const uint8_t *rgb8_host, const uint16_t *depth16_host, float depth_scale,
+                                  float w_color, float w_depth, int32_t color_mask_mode,
+                                  int32_t depth_mask_mode, int32_t normalize, uint32_t want,
+                                  int64_t learn_begin, int64_t learn_end, float *color, float *depth,
+                                  float *silhouette, float *d_col_opa, float *d_radius,
+                                  float *loss_host, float *d_pose_host, void *stream);
 
 #ifdef __cplusplus
 }

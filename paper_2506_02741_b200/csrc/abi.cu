@@ -51,7 +51,7 @@ cudaError_t dalloc(T **p, size_t n) {
 
 void free_all(Ctx &c) {
     void *ptrs[] = {c.proj, c.rect, c.thr, c.tile_count, c.tile_start, c.tile_cursor, c.tile_flag, c.keys, c.vals, c.pbits, c.keys2,
-                    c.vals2, c.offs, c.sub_lists, c.sub_masks, c.chunk_list, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.view_copy, c.ssim_abc, c.ssim_partials, c.det};
+                    c.vals2, c.offs, c.sub_lists, c.sub_masks, c.chunk_list, c.sub_count, c.T_final, c.last, c.partials, c.dev, c.host_io, c.sensor_io, c.view_copy, c.ssim_abc, c.ssim_partials, c.det};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -132,6 +132,7 @@ vtgs_status vtgs_create(vtgs_ctx **out, int32_t device, int64_t max_gaussians, i
     if (!e) e = dalloc(&c.ssim_abc, 9 * px);
     if (!e) e = dalloc(&c.ssim_partials, ((size_t)(max_width + 31) / 32) * ((max_height + 7) / 8));
     if (!e) e = dalloc(&c.host_io, 4 * px + 64);
+    if (!e) e = dalloc(&c.sensor_io, 5 * px + 64);
     if (!e) e = dalloc(&c.view_copy, 1);
     if (!e) e = cudaMemset(c.dev, 0, sizeof(vtgs::DevScalars));
     if (!e) e = cudaMemset(c.tile_count, 0, sizeof(uint32_t) * c.max_tiles);
@@ -456,18 +457,18 @@ vtgs_status vtgs_export_tiles(vtgs_ctx *ctx, int64_t *tile_start, int32_t *sorte
     return vtgs_check(ctx, stream);
 }
 
-vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col_opa, int64_t N,
-                           const vtgs_pose *view_host, vtgs_intrinsics intr,
-                           const float *target_rgb_host, const float *target_depth_host, float w_color,
-                           float w_depth, int32_t color_mask_mode, int32_t depth_mask_mode,
-                           int32_t normalize, uint32_t want, int64_t learn_begin, int64_t learn_end,
-                           float *color, float *depth, float *silhouette, float *d_col_opa,
-                           float *d_radius, float *loss_host, float *d_pose_host, void *stream) {
-    if (!ctx || !view_host || !target_rgb_host || !target_depth_host || !loss_host)
-        return VTGS_ERR_INVALID_ARG;
+}  // extern "C" (the shared body below is a C++ template)
+
+// Shared body of vtgs_step_host / vtgs_step_host_sensor: `upload` enqueues the target copies (and
+// any widening to fp32) on the copy stream after ev_ready; the backward waits for them.
+template <typename Upload>
+static vtgs_status step_host_core(vtgs_ctx *ctx, const float *pos_rad, const float *col_opa, int64_t N,
+                                  const vtgs_pose *view_host, vtgs_intrinsics intr, float w_color, float w_depth,
+                                  int32_t color_mask_mode, int32_t depth_mask_mode, int32_t normalize, uint32_t want,
+                                  int64_t learn_begin, int64_t learn_end, float *color, float *depth,
+                                  float *silhouette, float *d_col_opa, float *d_radius, float *loss_host,
+                                  float *d_pose_host, void *stream, Upload upload) {
     Ctx &c = ctx->c;
-    vtgs_status st = check_intr(ctx, intr);
-    if (st) return st;
     const size_t px = (size_t)intr.width * intr.height;
     float *d_rgb = c.host_io;                       // 3·px
     float *d_dep = c.host_io + 3 * px;              // px
@@ -487,13 +488,12 @@ vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col
     // the pose goes first on the compute stream; the targets (read only by the backward's loss
     // prologue) upload on a second stream while projection, sort and forward run
     e = cudaMemcpyAsync(d_view, view_host, sizeof(vtgs_pose), cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaEventRecord(c.ev_ready, s);   // the previous step's backward is done with d_rgb / d_dep
+    if (!e) e = cudaEventRecord(c.ev_ready, s);   // the previous step's backward is done with the staging
     if (!e) e = cudaStreamWaitEvent(c.copy_stream, c.ev_ready, 0);
-    if (!e) e = cudaMemcpyAsync(d_rgb, target_rgb_host, sizeof(float) * 3 * px, cudaMemcpyHostToDevice, c.copy_stream);
-    if (!e) e = cudaMemcpyAsync(d_dep, target_depth_host, sizeof(float) * px, cudaMemcpyHostToDevice, c.copy_stream);
+    if (!e) e = upload(c.copy_stream, d_rgb, d_dep);
     if (!e) e = cudaEventRecord(c.ev_copied, c.copy_stream);
     if (e) return cuda_fail(ctx, e, "vtgs_step_host (H2D)");
-    st = vtgs_render_fwd(ctx, pos_rad, col_opa, N, d_view, intr, color, depth, silhouette, stream);
+    vtgs_status st = vtgs_render_fwd(ctx, pos_rad, col_opa, N, d_view, intr, color, depth, silhouette, stream);
     if (st) return st;
     if ((e = cudaStreamWaitEvent(s, c.ev_copied, 0))) return cuda_fail(ctx, e, "vtgs_step_host (wait)");
     vtgs_l1_loss L{d_rgb, d_dep, nullptr, w_color, w_depth, color_mask_mode, depth_mask_mode, normalize, nullptr};
@@ -512,6 +512,58 @@ vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col
         return fail(ctx, VTGS_ERR_CAPACITY, "tile pairs exceeded max_pairs %lld (render and gradients empty)",
                     (long long)c.max_pairs);
     return VTGS_OK;
+}
+
+extern "C" {
+
+vtgs_status vtgs_step_host(vtgs_ctx *ctx, const float *pos_rad, const float *col_opa, int64_t N,
+                           const vtgs_pose *view_host, vtgs_intrinsics intr,
+                           const float *target_rgb_host, const float *target_depth_host, float w_color,
+                           float w_depth, int32_t color_mask_mode, int32_t depth_mask_mode,
+                           int32_t normalize, uint32_t want, int64_t learn_begin, int64_t learn_end,
+                           float *color, float *depth, float *silhouette, float *d_col_opa,
+                           float *d_radius, float *loss_host, float *d_pose_host, void *stream) {
+    if (!ctx || !view_host || !target_rgb_host || !target_depth_host || !loss_host)
+        return VTGS_ERR_INVALID_ARG;
+    vtgs_status st = check_intr(ctx, intr);
+    if (st) return st;
+    const size_t px = (size_t)intr.width * intr.height;
+    auto upload = [&](cudaStream_t cs, float *d_rgb, float *d_dep) {
+        cudaError_t e = cudaMemcpyAsync(d_rgb, target_rgb_host, sizeof(float) * 3 * px, cudaMemcpyHostToDevice, cs);
+        if (!e) e = cudaMemcpyAsync(d_dep, target_depth_host, sizeof(float) * px, cudaMemcpyHostToDevice, cs);
+        return e;
+    };
+    return step_host_core(ctx, pos_rad, col_opa, N, view_host, intr, w_color, w_depth, color_mask_mode,
+                          depth_mask_mode, normalize, want, learn_begin, learn_end, color, depth, silhouette,
+                          d_col_opa, d_radius, loss_host, d_pose_host, stream, upload);
+}
+
+vtgs_status vtgs_step_host_sensor(vtgs_ctx *ctx, const float *pos_rad, const float *col_opa, int64_t N,
+                                  const vtgs_pose *view_host, vtgs_intrinsics intr,
+                                  const uint8_t *rgb8_host, const uint16_t *depth16_host, float depth_scale,
+                                  float w_color, float w_depth, int32_t color_mask_mode,
+                                  int32_t depth_mask_mode, int32_t normalize, uint32_t want,
+                                  int64_t learn_begin, int64_t learn_end, float *color, float *depth,
+                                  float *silhouette, float *d_col_opa, float *d_radius,
+                                  float *loss_host, float *d_pose_host, void *stream) {
+    if (!ctx || !view_host || !rgb8_host || !depth16_host || !loss_host || !(depth_scale > 0.0f))
+        return VTGS_ERR_INVALID_ARG;
+    vtgs_status st = check_intr(ctx, intr);
+    if (st) return st;
+    Ctx &c = ctx->c;
+    const size_t px = (size_t)intr.width * intr.height;
+    uint8_t *s_rgb = c.sensor_io;                                   // 3·px bytes
+    uint16_t *s_dep = reinterpret_cast<uint16_t *>(c.sensor_io + ((3 * px + 15) & ~(size_t)15));   // px uint16
+    // upload 5 B/px and widen on the copy stream too: both run under projection, sort and forward
+    auto upload = [&](cudaStream_t cs, float *d_rgb, float *d_dep) {
+        cudaError_t e = cudaMemcpyAsync(s_rgb, rgb8_host, 3 * px, cudaMemcpyHostToDevice, cs);
+        if (!e) e = cudaMemcpyAsync(s_dep, depth16_host, sizeof(uint16_t) * px, cudaMemcpyHostToDevice, cs);
+        if (!e) e = launch_sensor_targets(c, s_rgb, s_dep, depth_scale, (int64_t)px, d_rgb, d_dep, cs);
+        return e;
+    };
+    return step_host_core(ctx, pos_rad, col_opa, N, view_host, intr, w_color, w_depth, color_mask_mode,
+                          depth_mask_mode, normalize, want, learn_begin, learn_end, color, depth, silhouette,
+                          d_col_opa, d_radius, loss_host, d_pose_host, stream, upload);
 }
 
 }  // extern "C"

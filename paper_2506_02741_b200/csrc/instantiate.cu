@@ -301,4 +301,53 @@ cudaError_t launch_instantiate(Ctx &c, const float *depth, const float *rgb, con
     return cudaGetLastError();
 }
 
+// Sensor-format targets (vtgs_step_host_sensor): c = v / 255, z = d · scale, in fp32 (the same
+// two IEEE operations a host-side conversion would use).  Four pixels per thread when the pixel
+// count allows 16-byte stores (three 4-byte colour words and one 8-byte depth word in, three
+// float4 colour and one float4 depth out), else one pixel per thread.
+__global__ void __launch_bounds__(256) k_sensor_targets4(const uint32_t *__restrict__ rgb8,
+                                                         const uint2 *__restrict__ d16, float scale, int64_t ng,
+                                                         float4 *__restrict__ rgb, float4 *__restrict__ depth) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t w[3] = {__ldg(rgb8 + 3 * g), __ldg(rgb8 + 3 * g + 1), __ldg(rgb8 + 3 * g + 2)};
+        float c[12];
+#pragma unroll
+        for (int i = 0; i < 12; ++i) c[i] = __fdiv_rn((float)((w[i >> 2] >> (8 * (i & 3))) & 0xffu), 255.0f);
+        rgb[3 * g + 0] = make_float4(c[0], c[1], c[2], c[3]);
+        rgb[3 * g + 1] = make_float4(c[4], c[5], c[6], c[7]);
+        rgb[3 * g + 2] = make_float4(c[8], c[9], c[10], c[11]);
+        const uint2 d = __ldg(d16 + g);
+        depth[g] = make_float4(__fmul_rn((float)(d.x & 0xffffu), scale), __fmul_rn((float)(d.x >> 16), scale),
+                               __fmul_rn((float)(d.y & 0xffffu), scale), __fmul_rn((float)(d.y >> 16), scale));
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sensor_targets(const uint8_t *__restrict__ rgb8,
+                                                        const uint16_t *__restrict__ d16, float scale, int64_t px,
+                                                        float *__restrict__ rgb, float *__restrict__ depth) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < px; i += (int64_t)gridDim.x * blockDim.x) {
+        rgb[3 * i + 0] = __fdiv_rn((float)rgb8[3 * i + 0], 255.0f);
+        rgb[3 * i + 1] = __fdiv_rn((float)rgb8[3 * i + 1], 255.0f);
+        rgb[3 * i + 2] = __fdiv_rn((float)rgb8[3 * i + 2], 255.0f);
+        depth[i] = __fmul_rn((float)d16[i], scale);
+    }
+}
+
+cudaError_t launch_sensor_targets(Ctx &c, const uint8_t *rgb8, const uint16_t *d16, float scale, int64_t px,
+                                  float *rgb, float *depth, cudaStream_t s) {
+    const bool vec = px % 4 == 0 && ((uintptr_t)rgb8 % 4 == 0) && ((uintptr_t)d16 % 8 == 0) &&
+                     ((uintptr_t)rgb % 16 == 0) && ((uintptr_t)depth % 16 == 0);
+    const int64_t n = vec ? px / 4 : px;
+    int64_t g = (n + 255) / 256;
+    if (g > (int64_t)c.num_sms * 8) g = (int64_t)c.num_sms * 8;
+    if (g < 1) g = 1;
+    if (vec)
+        k_sensor_targets4<<<(int)g, 256, 0, s>>>(reinterpret_cast<const uint32_t *>(rgb8),
+                                                 reinterpret_cast<const uint2 *>(d16), scale, n,
+                                                 reinterpret_cast<float4 *>(rgb), reinterpret_cast<float4 *>(depth));
+    else
+        k_sensor_targets<<<(int)g, 256, 0, s>>>(rgb8, d16, scale, px, rgb, depth);
+    return cudaGetLastError();
+}
+
 }  // namespace vtgs

@@ -102,6 +102,7 @@ struct Ctx {
     double *ssim_partials = nullptr; // per-CTA Σ SSIM
     DevScalars *dev = nullptr;
     float *host_io = nullptr;        // step_host device staging (targets + pose)
+    uint8_t *sensor_io = nullptr;    // step_host_sensor upload staging (rgb8 | depth16)
     cudaStream_t copy_stream = nullptr;  // step_host: target upload overlapped with the forward
     cudaEvent_t ev_ready = nullptr, ev_copied = nullptr;
     vtgs_pose *view_copy = nullptr;  // the forward's view pose, copied on the device for the backward
@@ -256,6 +257,8 @@ cudaError_t launch_visibility_counts(Ctx &c, const float *depth, const vtgs_pose
 cudaError_t launch_densify(Ctx &c, const float *depth, const float *rgb, const vtgs_pose *pose, vtgs_intrinsics intr,
                            const float *sil, float thr, const float *opacity, float opacity_default,
                            float4 *pos_rad, float4 *col_opa, int64_t *n_new, cudaStream_t s);
+cudaError_t launch_sensor_targets(Ctx &c, const uint8_t *rgb8, const uint16_t *d16, float scale, int64_t px,
+                                  float *rgb, float *depth, cudaStream_t s);
 cudaError_t launch_ssim(Ctx &c, const float *color, const float *target, int W, int H, float tau, float *d_color,
                         float *loss_out, cudaStream_t s);
 cudaError_t launch_pose_adam(Ctx &c, vtgs_pose *pose, const float *d_pose, float *state, float lr_rot,

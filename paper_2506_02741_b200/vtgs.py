@@ -85,6 +85,9 @@ _SIGS = {
     "vtgs_step_host": (_c.c_int32, [_P, _P, _P, _c.c_int64, _P, vtgs_intrinsics, _P, _P, _c.c_float, _c.c_float,
                                     _c.c_int32, _c.c_int32, _c.c_int32, _c.c_uint32, _c.c_int64, _c.c_int64,
                                     _P, _P, _P, _P, _P, _P, _P, _P]),
+    "vtgs_step_host_sensor": (_c.c_int32, [_P, _P, _P, _c.c_int64, _P, vtgs_intrinsics, _P, _P, _c.c_float,
+                                           _c.c_float, _c.c_float, _c.c_int32, _c.c_int32, _c.c_int32, _c.c_uint32,
+                                           _c.c_int64, _c.c_int64, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 EXPORTED = tuple(_SIGS)
 for _name, (_res, _args) in _SIGS.items():
@@ -304,6 +307,26 @@ class Renderer:
                            int(color_mask_mode), int(depth_mask_mode), int(normalize), int(want), int(learn[0]),
                            int(learn[1]), _ptr(color), _ptr(depth), _ptr(sil), _ptr(d_col_opa), _ptr(d_radius),
                            ctypes.addressof(loss), _ptr(d_pose_host), _stream(stream)), self.ctx)
+        return float(loss.value)
+
+
+    def step_host_sensor(self, pos_rad, col_opa, view_host, intr, rgb8_host, depth16_host, depth_scale, w_color,
+                         w_depth, color_mask_mode, depth_mask_mode, normalize, want, learn, out, d_col_opa, d_radius,
+                         d_pose_host=None, stream=None) -> float:
+        """step_host with the frame as a sensor delivers it: HOST uint8 RGB [H, W, 3] and uint16 depth
+        [H, W] (metres = value · depth_scale), widened to fp32 on the device (vtgs_step_host_sensor)."""
+        color, depth, sil = out
+        loss = ctypes.c_float()
+        vp = view_host if isinstance(view_host, torch.Tensor) else torch.as_tensor(view_host, dtype=torch.float32)
+        for t, dt in ((rgb8_host, torch.uint8), (depth16_host, torch.uint16)):
+            if isinstance(t, torch.Tensor) and (t.dtype != dt or t.is_cuda or not t.is_contiguous()):
+                raise VtgsError(VTGS_ERR_INVALID_ARG, f"step_host_sensor: expected a contiguous host {dt} tensor")
+        _ok(vtgs_step_host_sensor(self.ctx, _ptr(pos_rad), _ptr(col_opa), pos_rad.shape[0], _ptr(vp),
+                                  intrinsics(intr), _ptr(rgb8_host), _ptr(depth16_host), float(depth_scale),
+                                  float(w_color), float(w_depth), int(color_mask_mode), int(depth_mask_mode),
+                                  int(normalize), int(want), int(learn[0]), int(learn[1]), _ptr(color), _ptr(depth),
+                                  _ptr(sil), _ptr(d_col_opa), _ptr(d_radius), ctypes.addressof(loss),
+                                  _ptr(d_pose_host), _stream(stream)), self.ctx)
         return float(loss.value)
 
 

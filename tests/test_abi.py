@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol(lib):
 def test_binding_names_match_header(lib):
     from paper_2506_02741_b200 import vtgs
     assert sorted(vtgs.EXPORTED) == _declared()
-    assert vtgs.vtgs_abi_version() == 3
+    assert vtgs.vtgs_abi_version() == 4
     for s in (0, -1, -2, -3, -4, -5, -6):
         assert vtgs.vtgs_status_string(s)
 

@@ -666,6 +666,49 @@ def test_step_host_matches_device_path(vt):
         assert torch.allclose(r3, r2, rtol=1e-5, atol=1e-6)
 
 
+def test_step_host_sensor_equals_float_targets(vt):
+    """vtgs_step_host_sensor (uint8 RGB + uint16 depth uploaded, widened on the device) is the same
+    step as vtgs_step_host on the fp32 targets a host-side conversion with the same two IEEE
+    operations gives (c = v / 255, z = d · scale): identical loss and, with the deterministic merge,
+    bit-identical gradients; invalid arguments are refused."""
+    cfg = cached_config(2)
+    R = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R, cfg)
+    tg = cfg.targets[0]
+    H, W = cfg.intr.height, cfg.intr.width
+    scale = np.float32(1.0 / 5000.0)
+    rgb8 = np.clip(np.rint(tg.rgb * 255.0), 0, 255).astype(np.uint8)
+    d16 = np.clip(np.rint(tg.depth / scale), 0, 65535).astype(np.uint16)
+    rgb_f = rgb8.astype(np.float32) / np.float32(255.0)
+    dep_f = d16.astype(np.float32) * scale
+    out = tuple(torch.empty(sh, device="cuda") for sh in ((H, W, 3), (H, W), (H, W)))
+    hv = torch.from_numpy(view32(cfg.views[0]).astype(np.float32)).pin_memory()
+    want = vt.VTGS_GRAD_ATTR | vt.VTGS_GRAD_DETERMINISTIC
+    res = []
+    for sensor in (False, True):
+        d = torch.zeros((cfg.n_slots, 4), device="cuda")
+        r = torch.zeros(cfg.n_slots, device="cuda")
+        if sensor:
+            loss = R.step_host_sensor(pr, co, hv, cfg.intr, torch.from_numpy(rgb8).pin_memory(),
+                                      torch.from_numpy(d16).pin_memory(), float(scale), 0.8, 1.0, 0, 0, 0, want,
+                                      (0, cfg.n_slots), out, d, r)
+        else:
+            loss = R.step_host(pr, co, hv, cfg.intr, torch.from_numpy(rgb_f).pin_memory(),
+                               torch.from_numpy(dep_f).pin_memory(), 0.8, 1.0, 0, 0, 0, want, (0, cfg.n_slots),
+                               out, d, r)
+        torch.cuda.synchronize()
+        res.append((loss, d.cpu(), r.cpu()))
+    assert res[0][0] == res[1][0]
+    assert torch.equal(res[0][1], res[1][1]) and torch.equal(res[0][2], res[1][2])
+    assert res[0][1].abs().sum() > 0
+    with pytest.raises(vt.VtgsError):
+        R.step_host_sensor(pr, co, hv, cfg.intr, torch.from_numpy(rgb8), torch.from_numpy(d16), 0.0, 0.8, 1.0,
+                           0, 0, 0, want, (0, cfg.n_slots), out, d, r)
+    with pytest.raises(vt.VtgsError):   # fp32 depth where uint16 is expected
+        R.step_host_sensor(pr, co, hv, cfg.intr, torch.from_numpy(rgb8), torch.from_numpy(dep_f), float(scale),
+                           0.8, 1.0, 0, 0, 0, want, (0, cfg.n_slots), out, d, r)
+
+
 # ------------------------------------------------------------------------------ f1 (head-frame BA)
 def _ba_scene(seed=0, W=64, H=48, K=3):
     """K keyframes of a noisy slanted surface 1.5–3 m away, a view between keyframes 0 and 1."""
