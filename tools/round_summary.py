@@ -93,7 +93,9 @@ def main():
                f"- path floor: {b['path_floor']['t_floor_ms'] * 1e3:.1f} µs → the step runs at "
                f"{b['path_floor']['frac']:.3f} of it; step DRAM (ncu) {b['path_floor'].get('step_dram_bytes_ncu')} B = "
                f"{b['path_floor'].get('dram_over_algorithmic')} × the algorithmic bytes",
-               f"- e2e (vtgs_step_host, host RGB-D in, loss out): {b['e2e']['value']:.1f} Mpix/s" if b.get("e2e") else "",
+               (f"- e2e ({b['e2e'].get('api', 'vtgs_step_host')}): {b['e2e']['value']:.1f} Mpix/s"
+                + (f"; fp32 targets ({b['e2e']['fp32_targets']['api']}): {b['e2e']['fp32_targets']['value']:.1f} Mpix/s"
+                   if b['e2e'].get('fp32_targets') else "")) if b.get("e2e") else "",
                f"- cpu_baseline: {json.dumps(b.get('cpu_baseline'))}",
                f"- peaks: {json.dumps(b.get('peaks'))}",
                f"- context scratch: {b.get('context_scratch_bytes', 0) / 1e9:.2f} GB", "",
