@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--ssim", type=float, default=0.0,
                     help="add Eq. 2's SSIM term with this weight tau (0.2 in the paper) to the mapping step")
     ap.add_argument("--no-graph", action="store_true", help="run every timed step eagerly (no CUDA graph)")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="renderer contexts / CUDA streams the views of a step alternate over "
+                         "(0 = 2 for the batched configs 4 / 5, 1 otherwise)")
     return ap.parse_args()
 
 
@@ -274,6 +277,39 @@ def measured_traffic(workload, kernel):
         return None
 
 
+class RendererGroup:
+    """The bench's view of the k renderer contexts a mapping step alternates its views over
+    (BatchedMapper): calls that configure go to every context; the work counters are those of the
+    context that rendered the step's last view (the single-context meaning: the last forward's);
+    launches and per-kernel profiles are summed."""
+
+    def __init__(self, rs):
+        self.rs = list(rs)
+        self.last = None   # index of the context that renders the last view (set by the caller)
+
+    def __getattr__(self, name):   # everything else (instantiate, step_host, ...) on context 0
+        return getattr(self.rs[0], name)
+
+    def set_work_counters(self, on):
+        for r in self.rs:
+            r.set_work_counters(on)
+
+    def set_profiling(self, on):
+        for r in self.rs:
+            r.set_profiling(on)
+
+    def stats(self):
+        ss = [r.stats() for r in self.rs]
+        d = dict(ss[self.last if self.last is not None else -1])
+        d["launches"] = sum(x["launches"] for x in ss)
+        d["overflow"] = max(x["overflow"] for x in ss)
+        return d
+
+    def profile(self):
+        ps = [r.profile() for r in self.rs]
+        return {k: (sum(p[k][0] for p in ps), sum(p[k][1] for p in ps)) for k in ps[0]}
+
+
 def context_scratch_bytes(N, P, W, H):
     """Device scratch a vtgs context allocates (csrc/abi.cu vtgs_create): per slot proj 16 + rect 8
     + thresholds 8 B; per pair keys / values / fallback-sort scratch 21 B + 8 sub-lists and masks
@@ -438,7 +474,9 @@ def main():
     # config 5 (40 keyframes, 32.6M slots): one view needs ≤ 0.72 pairs per slot (23.5M), so the
     # context holds N pairs — its scratch stays under 4 GB; the others take the default 2N
     max_pairs = N + 262144 if args.config == 5 else 0
-    R = vtgs.Renderer(local, N, W, H, max_pairs=max_pairs)
+    n_streams = args.streams or (2 if args.config in (4, 5) else 1)
+    R_list = [vtgs.Renderer(local, N, W, H, max_pairs=max_pairs) for _ in range(n_streams)]
+    R = RendererGroup(R_list)
     scratch_bytes = context_scratch_bytes(N, max_pairs or 2 * N + 262144, W, H)
     # the section's Gaussians: every rank instantiates the same keyframes (no broadcast needed)
     pr, co = R.instantiate(torch.from_numpy(cfg.depth_stack()).to(dev), torch.from_numpy(cfg.rgb_stack()).to(dev),
@@ -459,10 +497,11 @@ def main():
         tgts = [cfg.targets[k] for k in mine]
         n_views_total = len(cfg.views)
         scaling = "strong"
+    R.last = (len(views_np) - 1) % n_streams
     view_np = views_np[0]
     tgt = tgts[0]
     wc, wd = cfg.loss_weights
-    mapper = BatchedMapper(R, pr, co, cfg.intr, [vtgs.pose_tensor(v, dev) for v in views_np],
+    mapper = BatchedMapper(R_list, pr, co, cfg.intr, [vtgs.pose_tensor(v, dev) for v in views_np],
                            [dict(rgb=torch.from_numpy(t.rgb).to(dev), depth=torch.from_numpy(t.depth).to(dev))
                             for t in tgts], wc, wd, w_ssim=args.ssim)
     grads = mapper.grads.flat
@@ -709,7 +748,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded procedural rooms, ray-cast RGB-D; stands in for Replica/TUM/ScanNet)",
-            "config": workload_config(cfg, args, n_views_total, len(views_np)),
+            "config": dict(workload_config(cfg, args, n_views_total, len(views_np)),
+                           streams=f"{n_streams} renderer context(s) / CUDA stream(s), views alternating"),
             "gaussians_per_s": gps,
             "roofline": roofline,
             "path_floor": path_floor,
@@ -719,7 +759,8 @@ def main():
             "graph": (f"the other {replays} timed steps replay one captured CUDA graph of the step ({per_step_launches} launches)"
                       if graph is not None else "eager"),
             "work": {"n_pairs": P, "e_eval": stats["e_eval"], "e_comp": stats["e_comp"], "max_tile": stats["max_tile"]},
-            "context_scratch_bytes": scratch_bytes,
+            "context_scratch_bytes": scratch_bytes,          # per renderer context
+            "contexts": n_streams,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk,

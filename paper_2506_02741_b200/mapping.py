@@ -55,7 +55,13 @@ def allreduce_grads(buf: GradBuffer, group: Optional[dist.ProcessGroup] = None) 
 
 class BatchedMapper:
     """Per-rank driver of one mapping step over a shard of views: the fused masked-L1 terms of
-    Eq. 2, plus its SSIM term τ·L_S when `w_ssim` = τ > 0 (τ = 0.2 at P:262)."""
+    Eq. 2, plus its SSIM term τ·L_S when `w_ssim` = τ > 0 (τ = 0.2 at P:262).
+
+    `renderer` may be a list of renderer contexts: view i then renders on context i mod k, each on
+    its own CUDA stream forked from (and joined back into) the caller's, so consecutive views'
+    kernels overlap on the GPU (one view's tail waves under the next view's first ones).  The
+    views write the shared gradient buffer with float atomics only (commutative), so the result is
+    the same sum; the deterministic merge finalises per context and is not combined with k > 1."""
 
     def __init__(self, renderer, pos_rad: torch.Tensor, col_opa: torch.Tensor, intr,
                  views: Sequence[torch.Tensor], targets: Sequence[dict], w_color: float, w_depth: float,
@@ -63,7 +69,8 @@ class BatchedMapper:
                  w_ssim: float = 0.0):
         from . import vtgs
         self.vt = vtgs
-        self.R = renderer
+        self.Rs = list(renderer) if isinstance(renderer, (list, tuple)) else [renderer]
+        self.R = self.Rs[0]
         self.pos_rad, self.col_opa, self.intr = pos_rad, col_opa, intr
         self.views = list(views)
         self.targets = list(targets)
@@ -74,12 +81,28 @@ class BatchedMapper:
         self.grads = GradBuffer(n, pos_rad.device)
         H, W = intr.height, intr.width
         dev = pos_rad.device
-        self.out = (torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev),
-                    torch.empty((H, W), device=dev))
+        k = len(self.Rs)
+        self.outs = [(torch.empty((H, W, 3), device=dev), torch.empty((H, W), device=dev),
+                      torch.empty((H, W), device=dev)) for _ in range(k)]
+        self.out = self.outs[0]
         self.loss = torch.zeros(max(len(self.views), 1), device=dev)
         self.w_ssim = float(w_ssim)
         self.ssim_loss = torch.zeros(max(len(self.views), 1), device=dev)
-        self.d_ssim = torch.zeros((H, W, 3), device=dev) if self.w_ssim > 0 else None
+        self.d_ssims = [torch.zeros((H, W, 3), device=dev) if self.w_ssim > 0 else None for _ in range(k)]
+        self.d_ssim = self.d_ssims[0]
+        self.streams = [torch.cuda.Stream(dev) for _ in range(k)] if k > 1 else None
+
+    def _view(self, i, v, t):
+        j = i % len(self.Rs)
+        R, out, d_ssim = self.Rs[j], self.outs[j], self.d_ssims[j]
+        R.render_fwd(self.pos_rad, self.col_opa, v, self.intr, out=out)
+        if d_ssim is not None:
+            d_ssim.zero_()
+            R.ssim_loss(out[0], t["rgb"], self.w_ssim, d_color=d_ssim, loss_out=self.ssim_loss[i:i + 1])
+        R.render_bwd(self.vt.VTGS_GRAD_ATTR, d_col_opa=self.grads.d_col_opa, d_radius=self.grads.d_radius,
+                     loss=dict(target_rgb=t["rgb"], target_depth=t["depth"], w_color=self.w_color,
+                               w_depth=self.w_depth, extra_dcolor=d_ssim),
+                     learn=self.learn, loss_out=self.loss[i:i + 1])
 
     def step(self, allreduce: bool = True, check: Optional[bool] = None) -> GradBuffer:
         """Zero the gradients, render + backprop every local view (accumulating), all-reduce.
@@ -88,18 +111,21 @@ class BatchedMapper:
         if check is None:
             check = not getattr(self, "_checked", False)
         self.grads.zero_()
-        for i, (v, t) in enumerate(zip(self.views, self.targets)):
-            self.R.render_fwd(self.pos_rad, self.col_opa, v, self.intr, out=self.out)
-            if self.d_ssim is not None:
-                self.d_ssim.zero_()
-                self.R.ssim_loss(self.out[0], t["rgb"], self.w_ssim, d_color=self.d_ssim,
-                                 loss_out=self.ssim_loss[i:i + 1])
-            self.R.render_bwd(self.vt.VTGS_GRAD_ATTR, d_col_opa=self.grads.d_col_opa, d_radius=self.grads.d_radius,
-                              loss=dict(target_rgb=t["rgb"], target_depth=t["depth"], w_color=self.w_color,
-                                        w_depth=self.w_depth, extra_dcolor=self.d_ssim),
-                              learn=self.learn, loss_out=self.loss[i:i + 1])
+        if self.streams is None:
+            for i, (v, t) in enumerate(zip(self.views, self.targets)):
+                self._view(i, v, t)
+        else:   # fork: every context's stream starts after the zeroing; join before the all-reduce
+            cur = torch.cuda.current_stream(self.pos_rad.device)
+            for s in self.streams:
+                s.wait_stream(cur)
+            for i, (v, t) in enumerate(zip(self.views, self.targets)):
+                with torch.cuda.stream(self.streams[i % len(self.streams)]):
+                    self._view(i, v, t)
+            for s in self.streams:
+                cur.wait_stream(s)
         if check:
-            self.R.check()
+            for j, R in enumerate(self.Rs):
+                R.check(stream=self.streams[j] if self.streams else None)
             self._checked = True
         if allreduce:
             allreduce_grads(self.grads, self.group)
