@@ -512,8 +512,8 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
-        mapper.step(allreduce=ws > 1)
+    def step(serial=False):
+        mapper.step(allreduce=ws > 1, serial=serial)
 
     # measured roofline denominators of the ALU-bound kernels (FMA chain, MUFU ex2), this process
     fp32_meas, ex2_meas = vtgs.measure_peaks(local)
@@ -585,8 +585,8 @@ def main():
         if graph is not None and not prof_i:
             graph.replay()
             replays += 1
-        else:
-            step()
+        else:   # the profiled steps run their views serially: per-kernel events need no overlap
+            step(serial=prof_i)
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     if clocks:
@@ -755,7 +755,8 @@ def main():
             "path_floor": path_floor,
             "peaks": peaks_json,
             "stages": stage_json,
-            "stage_timing": f"CUDA events around every kernel on every {PROFILE_EVERY}th timed step ({(args.steps + PROFILE_EVERY - 1) // PROFILE_EVERY} of {args.steps}, run eagerly), on the launching stream",
+            "stage_timing": f"CUDA events around every kernel on every {PROFILE_EVERY}th timed step ({(args.steps + PROFILE_EVERY - 1) // PROFILE_EVERY} of {args.steps}, run eagerly"
+                            + (", views serially on one context's stream" if n_streams > 1 else "") + "), on the launching stream",
             "graph": (f"the other {replays} timed steps replay one captured CUDA graph of the step ({per_step_launches} launches)"
                       if graph is not None else "eager"),
             "work": {"n_pairs": P, "e_eval": stats["e_eval"], "e_comp": stats["e_comp"], "max_tile": stats["max_tile"]},

@@ -104,14 +104,16 @@ class BatchedMapper:
                                w_depth=self.w_depth, extra_dcolor=d_ssim),
                      learn=self.learn, loss_out=self.loss[i:i + 1])
 
-    def step(self, allreduce: bool = True, check: Optional[bool] = None) -> GradBuffer:
+    def step(self, allreduce: bool = True, check: Optional[bool] = None, serial: bool = False) -> GradBuffer:
         """Zero the gradients, render + backprop every local view (accumulating), all-reduce.
         `check` (default: on the first step) synchronises once and raises VtgsError if a view's
-        tile pairs exceeded the context's capacity (the render would silently be empty)."""
+        tile pairs exceeded the context's capacity (the render would silently be empty).
+        `serial` runs the views one after another on the caller's stream even with several
+        contexts (per-kernel event timing is only meaningful without concurrent kernels)."""
         if check is None:
             check = not getattr(self, "_checked", False)
         self.grads.zero_()
-        if self.streams is None:
+        if self.streams is None or serial:
             for i, (v, t) in enumerate(zip(self.views, self.targets)):
                 self._view(i, v, t)
         else:   # fork: every context's stream starts after the zeroing; join before the all-reduce
@@ -125,7 +127,7 @@ class BatchedMapper:
                 cur.wait_stream(s)
         if check:
             for j, R in enumerate(self.Rs):
-                R.check(stream=self.streams[j] if self.streams else None)
+                R.check(stream=self.streams[j] if self.streams and not serial else None)
             self._checked = True
         if allreduce:
             allreduce_grads(self.grads, self.group)
