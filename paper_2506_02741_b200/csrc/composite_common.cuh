@@ -93,12 +93,6 @@ constexpr float kNegHalfLog2e = -0.5f * kLog2e;
 // instructions in every kernel, so the forward and the backward use the same bits
 __device__ __forceinline__ float exp_scale(float s2) { return kNegHalfLog2e * rcp_approx(s2); }
 
-// the oracle's raw α = fl(o·w) with the correctly rounded w (fp64 exp, rounded once)
-__device__ __forceinline__ float exact_raw_alpha(float d2, float s2, float o) {
-    const float w = __double2float_rn(exp((double)__fdiv_rn(__fmul_rn(-0.5f, d2), s2)));
-    return __fmul_rn(o, w);
-}
-
 __device__ __forceinline__ float f32_next(float x) { return __uint_as_float(__float_as_uint(x) + 1u); }   // x ≥ 0
 __device__ __forceinline__ float f32_prev(float x) { return __uint_as_float(__float_as_uint(x) - 1u); }   // x > 0
 
