@@ -34,7 +34,10 @@ constexpr int kFwdWarps = 2;  // warps (8×4 sub-tiles) per CTA: small CTAs reti
 // (R batches ahead of the slowest live lane).  Compared with walking batch by batch in lock
 // step (the warp runs max-over-lanes candidates per batch), the warp runs ≈ max-over-lanes of
 // the whole-list candidate count — tools/sim_batches.py: lane efficiency 0.27 → 0.87 at R = 16.
-constexpr int kInner = 6;                      // lane-independent steps between warp checks
+#ifndef VTGS_FWD_INNER
+#define VTGS_FWD_INNER 6
+#endif
+constexpr int kInner = VTGS_FWD_INNER;         // lane-independent steps between warp checks
 
 template <int R, bool STATS>
 struct FwdRing {

@@ -18,6 +18,8 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # VTGS_LIB=checked loads the bounds-checked build (libvtgs_checked.so, tests/test_gpu_variants.py)
 LIB_PATH = os.path.join(_HERE, "libvtgs_checked.so" if os.environ.get("VTGS_LIB") == "checked" else "libvtgs.so")
+# A/B of compile-time variants (tools/gpu_lib_ab.sh): an explicit path to another in-tree build
+LIB_PATH = os.environ.get("VTGS_LIB_PATH", LIB_PATH)
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2506_02741_b200.build` "
                       "(there is no CPU fallback)")
