@@ -169,8 +169,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
     const char *sbase = reinterpret_cast<const char *>(&sS[wl_]);
     const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
     const unsigned lane = lane_id();
-    const int sx = tx * kTile + (sub & 1) * 8, sy = ty * kTile + (sub >> 1) * 4;
-    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const int sx = sub_x0(tx, sub), sy = sub_y0(ty, sub);
+    const int px = sx + pix_dx((int)lane), py = sy + pix_dy((int)lane);
     const bool inside = px < p.W && py < p.H;
     const float pxf = (float)px, pyf = (float)py;
     const int n = (int)p.tile_count[tile];
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
                 dc1 = fmaf(gp.y, md.x, dc1);
                 dc2 = fmaf(gp.z, md.x, dc2);
                 dzd = fmaf(gp.w, md.x, dzd);
-                const float dx = (float)(sx + (i & 7)) - ux, dy = (float)(sy + (i >> 3)) - uy;
+                const float dx = (float)(sx + pix_dx(i)) - ux, dy = (float)(sy + pix_dy(i)) - uy;
                 const float d2 = dx * dx + dy * dy;
                 const float dw = md.y;  // dL/dα · w  (= ∂L/∂o contribution; 0 when α clamped)
                 dop += dw;
@@ -419,8 +419,8 @@ __global__ void __launch_bounds__(kPoseRingWarps * 32) k_composite_bwd_pose_ring
     const int sub = gsub & 7;
     const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
     const unsigned lane = lane_id();
-    const int sx = tx * kTile + (sub & 1) * 8, sy = ty * kTile + (sub >> 1) * 4;
-    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const int sx = sub_x0(tx, sub), sy = sub_y0(ty, sub);
+    const int px = sx + pix_dx((int)lane), py = sy + pix_dy((int)lane);
     const bool inside = px < p.W && py < p.H;
     const float pxf = (float)px, pyf = (float)py;
     const int n = (int)p.tile_count[tile];
@@ -603,8 +603,8 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_ring(BwdArgs p
     const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
     const unsigned lane = lane_id();
     const unsigned lmlt = lanemask_lt();
-    const int sx = tx * kTile + (sub & 1) * 8, sy = ty * kTile + (sub >> 1) * 4;
-    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const int sx = sub_x0(tx, sub), sy = sub_y0(ty, sub);
+    const int px = sx + pix_dx((int)lane), py = sy + pix_dy((int)lane);
     const bool inside = px < p.W && py < p.H;
     const float pxf = (float)px, pyf = (float)py;
     const int n = (int)p.tile_count[tile];
@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_ring(BwdArgs p
                     dc0 = fmaf(gp.x, md.x, dc0);
                     dc1 = fmaf(gp.y, md.x, dc1);
                     dc2 = fmaf(gp.z, md.x, dc2);
-                    const float dx = (float)(sx + (i & 7)) - ux, dy = (float)(sy + (i >> 3)) - uy;
+                    const float dx = (float)(sx + pix_dx(i)) - ux, dy = (float)(sy + pix_dy(i)) - uy;
                     const float d2 = dx * dx + dy * dy;
                     dop += md.y;
                     sw2 = fmaf(md.y, d2, sw2);

@@ -20,6 +20,23 @@ namespace vtgs {
 
 constexpr unsigned kFullMask = 0xffffffffu;
 
+// Sub-tile geometry: each 16×16 tile is split into 8 sub-tiles of kSubW × kSubH pixels, one warp
+// each, lane = pixel (y − sy)·kSubW + (x − sx).  Default 4 × 8 (4 columns × 2 rows of sub-tiles,
+// s = column + 4·row): depth-sorted batches spread over a tall sub-tile's pixels a little more
+// evenly than over a wide one (the lane models of tests/models/sim_bwd_ring.py: lock-step
+// phase-1 steps −10 %, ring steps −6 %).  -DVTGS_SUB_8x4 builds the round-1 shape (8 × 4).
+#ifdef VTGS_SUB_8x4
+constexpr int kSubW = 8, kSubH = 4;
+#else
+constexpr int kSubW = 4, kSubH = 8;
+#endif
+constexpr int kSubCols = kTile / kSubW;
+static_assert(kSubW * kSubH == 32 && kTile % kSubW == 0 && kTile % kSubH == 0, "a warp per sub-tile");
+__device__ __forceinline__ int sub_x0(int tx, int s) { return tx * kTile + (s % kSubCols) * kSubW; }
+__device__ __forceinline__ int sub_y0(int ty, int s) { return ty * kTile + (s / kSubCols) * kSubH; }
+__device__ __forceinline__ int pix_dx(int i) { return i % kSubW; }   // pixel / lane index → offsets
+__device__ __forceinline__ int pix_dy(int i) { return i / kSubW; }
+
 // One sub-list entry held in registers (gathered one batch ahead).
 struct EntryRegs {
     uint32_t g;
@@ -190,6 +207,7 @@ __device__ __forceinline__ float pair_d2(float xf, float yf, float u, float v) {
     return __fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy));
 }
 
+#ifdef VTGS_SUB_8x4
 // Mask of the warp's 32 pixels (bit = (y−sy)·8 + (x−sx)) inside the entry's rect and,
 // conservatively, inside its disc d² ≤ 9σ².  The exact fp32 test is re-done per pixel in the
 // compositing loops; this mask only has to be a superset of the pixels that pass it: row y
@@ -218,6 +236,35 @@ __device__ __forceinline__ unsigned lane_mask(const float4 A, const uint2 r, int
     }
     return m;
 }
+#else
+// Mask of the warp's 32 pixels (bit = (y−sy)·4 + (x−sx)) inside the entry's rect and,
+// conservatively, inside its disc d² ≤ D_c.  The exact fp32 test is re-done per pixel in the
+// compositing loops; this mask only has to be a superset of the pixels that pass it: column x is
+// kept iff fl(dx·dx) ≤ D_c (the same fp32 dx² the exact test adds to a non-negative dy²), and its
+// rows are widened by 0.01 px around v ± √(D_c − dx²) — the 8 × 4 shape's row test with x and y
+// exchanged (the exact test is symmetric in them).  Branch-free over the sub-tile's 4 columns.
+__device__ __forceinline__ unsigned lane_mask(const float4 A, const uint2 r, int sx, int sy) {
+    const int x0 = max((int)(r.x & 0xffffu), sx), x1 = min((int)(r.x >> 16), sx + 3);
+    const int y0 = max((int)(r.y & 0xffffu), sy), y1 = min((int)(r.y >> 16), sy + 7);
+    const float fsx = (float)sx;
+    unsigned m = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float dx = __fsub_rn(fsx + (float)j, A.x);
+        const float dx2 = __fmul_rn(dx, dx);
+        // the exact test accepts |dy| up to √(r2 + ½ulp(D_c)) (dx² + dy² rounds down onto D_c):
+        // widen by A.z·2⁻²³ ≥ ½ulp before the root, then by 0.01 px for the approximate rsqrt
+        const float r2 = A.z - dx2 + A.z * 1.1920929e-7f;
+        const float hh = r2 * rsqrt_approx(fmaxf(r2, 1e-30f)) + 0.01f;
+        const int ya = max(y0, (int)ceilf(A.y - hh)), yb = min(y1, (int)floorf(A.y + hh));
+        const bool ok = sx + j >= x0 && sx + j <= x1 && dx2 <= A.z && ya <= yb;
+        const unsigned lo = (unsigned)min(max(ya - sy, 0), 7), hi = (unsigned)min(max(yb - sy, 0), 7);
+        const unsigned col = 0x11111111u & (0xffffffffu << (4 * lo)) & (0xffffffffu >> (28 - 4 * hi));
+        m |= ok ? col << j : 0u;
+    }
+    return m;
+}
+#endif
 
 // The entry's ±3σ pixel rect recomputed from its projection with exactly k_project_count's fp32
 // operations (|proj.w| is the clamped σ it used), so the compositing kernels need not gather it.
@@ -244,6 +291,7 @@ __device__ __forceinline__ unsigned transpose32(unsigned x, unsigned lane) {
     return x;
 }
 
+#ifdef VTGS_SUB_8x4
 // Bit s (s = 2k + c) set iff the rect touches sub-tile (c, k) = pixels
 // [tx0 + 8c, tx0 + 8c + 7] × [ty0 + 4k, ty0 + 4k + 3] of the tile at (tx0, ty0).
 __device__ __forceinline__ unsigned subtile_bits(uint2 r, int tx0, int ty0) {
@@ -255,5 +303,18 @@ __device__ __forceinline__ unsigned subtile_bits(uint2 r, int tx0, int ty0) {
     const unsigned rows = (0xffu >> (6 - 2 * k1)) & (0xffu << (2 * k0)) & 0x55u;   // bit 2k per row k
     return ((cols & 1u) ? rows : 0u) | ((cols & 2u) ? rows << 1 : 0u);
 }
+#else
+// Bit s (s = c + 4k) set iff the rect touches sub-tile (c, k) = pixels
+// [tx0 + 4c, tx0 + 4c + 3] × [ty0 + 8k, ty0 + 8k + 7] of the tile at (tx0, ty0).
+__device__ __forceinline__ unsigned subtile_bits(uint2 r, int tx0, int ty0) {
+    const int x0 = (int)(r.x & 0xffffu), x1 = (int)(r.x >> 16);
+    const int y0 = (int)(r.y & 0xffffu), y1 = (int)(r.y >> 16);
+    // sub-tile columns c0 .. c1 and rows k0 .. k1 the rect touches (it overlaps the tile)
+    const int c0 = max(x0 - tx0, 0) >> 2, c1 = min(x1 - tx0, 15) >> 2;
+    const int k0 = max(y0 - ty0, 0) >> 3, k1 = min(y1 - ty0, 15) >> 3;
+    const unsigned cols = (0xfu >> (3 - c1)) & (0xfu << c0);
+    return (k0 == 0 ? cols : 0u) | (k1 == 1 ? cols << 4 : 0u);
+}
+#endif
 
 }  // namespace vtgs

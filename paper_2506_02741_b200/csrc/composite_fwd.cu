@@ -61,8 +61,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32, MINB) k_composite_fwd_ring(Fwd
     const int ty = tile / p.ntx, tx = tile - ty * p.ntx;
     const int w = gsub & 7;
     const unsigned lane = lane_id();
-    const int sx = tx * kTile + (w & 1) * 8, sy = ty * kTile + (w >> 1) * 4;
-    const int px = sx + (lane & 7), py = sy + (lane >> 3);
+    const int sx = sub_x0(tx, w), sy = sub_y0(ty, w);
+    const int px = sx + pix_dx((int)lane), py = sy + pix_dy((int)lane);
     const bool inside = px < p.W && py < p.H;
     const float pxf = (float)px, pyf = (float)py;
     const int n = (int)p.tile_count[tile];

@@ -19,7 +19,8 @@ import oracle  # noqa: E402
 from synth.scenes import cached_config  # noqa: E402
 
 
-def main(n_sub=300, seed=0):
+def main(n_sub=300, seed=0, sw=8):
+    sh = 32 // sw   # sub-tile shape sw × sh (8×4 built; 4×8 modelled)
     cfg = cached_config(2)
     intr = cfg.intr
     pr, co, _ = oracle.instantiate(cfg.depth_stack(), cfg.rgb_stack(), cfg.pose_stack(), intr, cfg.opacity)
@@ -30,7 +31,7 @@ def main(n_sub=300, seed=0):
     ntx = (intr.width + 15) // 16
     T = len(start) - 1
     rng = np.random.default_rng(seed)
-    confs = [(R, C) for R in (2, 4, 8) for C in (512, 768, 1024)]
+    confs = [(R, C) for R in (4,) for C in (1 << 20,)]
     steps = {c: 0 for c in confs}
     lock = 0
     wins = [(2, 1024), (4, 1024), (4, 2048), (8, 2048)]
@@ -41,10 +42,10 @@ def main(n_sub=300, seed=0):
         t = rng.integers(T)
         s = rng.integers(8)
         ty, tx = divmod(int(t), ntx)
-        sx, sy = tx * 16 + (s & 1) * 8, ty * 16 + (s >> 1) * 4
+        sx, sy = tx * 16 + (s % (16 // sw)) * sw, ty * 16 + (s // (16 // sw)) * sh
         lst = gid[start[t]:start[t + 1]]
         r = rect[lst]
-        ov = (r[:, 0] <= sx + 7) & (r[:, 2] >= sx) & (r[:, 1] <= sy + 3) & (r[:, 3] >= sy)
+        ov = (r[:, 0] <= sx + sw - 1) & (r[:, 2] >= sx) & (r[:, 1] <= sy + sh - 1) & (r[:, 3] >= sy)
         sub = lst[ov]
         if len(sub) == 0:
             continue
@@ -53,7 +54,7 @@ def main(n_sub=300, seed=0):
         o = co[sub, 3]
         bits = np.zeros((32, len(sub)), dtype=bool)
         for lane in range(32):
-            x, y = sx + (lane & 7), sy + (lane >> 3)
+            x, y = sx + (lane % sw), sy + (lane // sw)
             if x >= intr.width or y >= intr.height:
                 continue
             inr = (rr[:, 0] <= x) & (rr[:, 2] >= x) & (rr[:, 1] <= y) & (rr[:, 3] >= y)
@@ -124,4 +125,4 @@ def main(n_sub=300, seed=0):
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]) if len(sys.argv) > 1 else 300)
+    main(int(sys.argv[1]) if len(sys.argv) > 1 else 300, 0, int(sys.argv[2]) if len(sys.argv) > 2 else 8)
