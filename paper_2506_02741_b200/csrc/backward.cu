@@ -141,7 +141,7 @@ __device__ __forceinline__ PixelUp pixel_upstream(const BwdArgs &p, int px, int 
 //             per-Gaussian reduction with no shuffles; attribute gradients leave with one
 //             float4 + one float global atomic per (Gaussian, sub-tile), the pose chain is
 //             applied per (Gaussian, sub-tile) into the lane's 12 accumulators.
-// One warp per 8×4 sub-tile, kBwdWarps warps per CTA, no block barriers.
+// One warp per sub-tile (4×8, composite_common.cuh), kBwdWarps warps per CTA, no block barriers.
 constexpr int kBwdWarps = 2;
 struct __align__(16) BwdStage {
     float4 A[32];   // u, v, D_c, escale

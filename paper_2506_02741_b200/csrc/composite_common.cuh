@@ -1,6 +1,6 @@
 // composite_common.cuh — machinery shared by the forward and backward compositing kernels.
 //
-// Work decomposition (DESIGN.md §4 K6/K7).  Every 16×16 tile is split into eight 8×4 sub-tiles
+// Work decomposition (DESIGN.md §4 K6/K7).  Every 16×16 tile is split into eight 4×8 sub-tiles
 // and the tile sort also emits, per sub-tile, the (depth-ordered) sub-list of the tile entries
 // whose footprint rect touches that sub-tile.  One WARP owns one sub-tile (lane = pixel) and
 // walks its sub-list independently of every other warp — no block barriers, so a warp whose

@@ -1,7 +1,7 @@
 // (4) Per-tile front-to-back compositing of colour, depth and silhouette — PAPER.md:146
 // (Eq. 1 `splat`), α floor 1/255 from north_star (4).
 // Decision arithmetic exactly as DESIGN.md §3 step 7.  Work decomposition: composite_common.cuh
-// (one warp per 8×4 sub-tile, lane = pixel, per-lane candidate lists by bit transpose).
+// (one warp per 4×8 sub-tile, lane = pixel, per-lane candidate lists by bit transpose).
 #include <stdlib.h>
 
 #include "composite_common.cuh"
@@ -25,7 +25,7 @@ struct FwdArgs {
     int64_t N;          // Gaussians (checked build)
 };
 
-constexpr int kFwdWarps = 2;  // warps (8×4 sub-tiles) per CTA: small CTAs retire independently
+constexpr int kFwdWarps = 2;  // warps (sub-tiles) per CTA: small CTAs retire independently
 
 // Ring walk.  The warp builds 32-entry batches of its sub-list into a ring of R slots (entry
 // data A = (u, v, 9σ², o), B = (c_r, c_g, c_b, z), and per lane the bit column of the entries

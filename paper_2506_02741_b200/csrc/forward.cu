@@ -365,7 +365,7 @@ __device__ __forceinline__ int block_sort_zgid(uint32_t *K0, uint32_t *V0, uint3
     return npass & 1;
 }
 
-// Sub-lists of the sorted tile list: sub-tile s (8×4 pixels, composite_common.cuh) gets, in
+// Sub-lists of the sorted tile list: sub-tile s (4×8 pixels, composite_common.cuh) gets, in
 // tile-list order, every entry whose rect touches it.  Stored at out + s·n (capacity n each);
 // counts at sub_count[0..7].  Stable block-wide compaction, 256 entries per round.
 __device__ __forceinline__ void build_sublists(const uint32_t *V, int n, const uint2 *__restrict__ rect, int tx0,

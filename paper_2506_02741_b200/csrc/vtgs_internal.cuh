@@ -87,13 +87,13 @@ struct Ctx {
     uint32_t *tile_flag = nullptr;   // [2·max_tiles] work lists: radix sort (> 8192 / degenerate) | 4097..8192
     uint32_t *keys = nullptr;        // bucket: z bits   [max_pairs]
     uint32_t *vals = nullptr;        // bucket: gid      [max_pairs] — sorted in place
-    uint8_t *pbits = nullptr;        // bucket: the 8×4 sub-tiles of its tile the pair's rect touches [max_pairs]
+    uint8_t *pbits = nullptr;        // bucket: the 8 sub-tiles of its tile the pair's rect touches [max_pairs]
     uint32_t *keys2 = nullptr;       // fallback sort scratch [max_pairs]
     uint32_t *vals2 = nullptr;
     uint32_t *offs = nullptr;        // fallback sort ranks [max_pairs]
     uint32_t *chunk_list = nullptr;  // the long-tile plans' chunk descriptors, 12 u32 each [12·(max_pairs/2048 + max_tiles + 1)]
     uint32_t *sub_masks = nullptr;   // per sub-list entry: the pixels that composited it (forward → backward) [8·max_pairs]
-    uint32_t *sub_lists = nullptr;   // per tile 8 sub-lists (8×4 sub-tiles), capacity 8·n_tile [8·max_pairs]
+    uint32_t *sub_lists = nullptr;   // per tile 8 sub-lists (4×8 sub-tiles), capacity 8·n_tile [8·max_pairs]
     uint32_t *sub_count = nullptr;   // [8·max_tiles]
     float *T_final = nullptr;        // per pixel
     uint32_t *last = nullptr;        // per pixel: 1 + sub-list position of the last composited entry
