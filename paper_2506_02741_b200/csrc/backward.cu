@@ -361,7 +361,20 @@ __global__ void __launch_bounds__(kBwdWarps * 32, MINB) k_composite_bwd(BwdArgs 
         __syncwarp();
     }
 
-    if (POSE || LOSS) {   // fixed-order reduction: lanes → warp → CTA (one partial per CTA)
+    if (!POSE && LOSS) {   // loss only (mapping): lanes → warp → CTA, one contiguous double per CTA
+        double v = lossv;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
+        if (lane == 0) reinterpret_cast<double *>(&sS[wl_].A[0])[0] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < kBwdWarps; ++i) s += reinterpret_cast<const double *>(&sS[i].A[0])[0];
+            p.partials[blockIdx.x] = s;   // k_loss_finalize: row order, coalesced
+        }
+    }
+    if (POSE) {   // fixed-order reduction: lanes → warp → CTA (one partial per CTA)
         // each warp's 13 doubles go into its own (now dead) row of sA: no extra shared memory
         // (K7's occupancy is shared-memory bound: 11 two-warp CTAs per SM need ≤ 19.9 KB each)
         double v[13] = {h0, h1, h2, K00, K01, K02, K10, K11, K12, K20, K21, K22, lossv};
@@ -814,18 +827,18 @@ __global__ void __launch_bounds__(kBwdWarps * 32) k_composite_bwd_ring(BwdArgs p
     __syncwarp();
     while (flushed < built) reduce(flushed++);
 
-    if (LOSS) {   // fixed-order loss reduction: lanes → warp → CTA (the rows k_loss_finalize sums)
+    if (LOSS) {   // fixed-order loss reduction: lanes → warp → CTA (the contiguous rows k_loss_finalize sums)
         double v = up.lossv;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFullMask, v, o);
         __shared__ double sRedL[kBwdWarps];
         if (lane == 0) sRedL[wl_] = v;
         __syncthreads();
-        if (threadIdx.x == 0) {   // k_loss_finalize reads column 12 only
+        if (threadIdx.x == 0) {
             double s = 0.0;
 #pragma unroll
             for (int i = 0; i < kBwdWarps; ++i) s += sRedL[i];
-            p.partials[(size_t)blockIdx.x * 16 + 12] = s;
+            p.partials[blockIdx.x] = s;   // k_loss_finalize: row order, coalesced
         }
     }
 }
@@ -972,7 +985,8 @@ __global__ void __launch_bounds__(kFinThreads) k_pose_finalize(const double *__r
     }
 }
 
-// Loss only (mapping): the fixed-order sum of one column of the per-CTA partials, one CTA.
+// Loss only (mapping): the fixed-order sum of the per-CTA loss partials (one contiguous double per
+// backward CTA, so the loads coalesce), one CTA.
 constexpr int kLossThreads = 1024;
 __global__ void __launch_bounds__(kLossThreads) k_loss_finalize(const double *__restrict__ partials, int T,
                                                                 float *__restrict__ loss_out) {
@@ -984,12 +998,12 @@ __global__ void __launch_bounds__(kLossThreads) k_loss_finalize(const double *__
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
         const int t = tid + u * kLossThreads;
-        x[u] = t < T ? __ldg(partials + (size_t)t * 16 + 12) : 0.0;
+        x[u] = t < T ? __ldg(partials + t) : 0.0;
     }
     double acc = 0.0;
 #pragma unroll
     for (int u = 0; u < kU; ++u) acc += x[u];
-    for (int t = tid + kU * kLossThreads; t < T; t += kLossThreads) acc += __ldg(partials + (size_t)t * 16 + 12);
+    for (int t = tid + kU * kLossThreads; t < T; t += kLossThreads) acc += __ldg(partials + t);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
     if ((tid & 31) == 0) red[tid >> 5] = acc;

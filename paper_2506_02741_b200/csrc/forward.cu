@@ -242,6 +242,8 @@ __global__ void __launch_bounds__(256) k_emit_pairs(const float4 *__restrict__ p
             }
         }
         int kx = 0, ky = 0;   // (tile column, row) offsets stepped incrementally (no integer division)
+        // (two tiles per iteration, both cursor atomics in flight together, measured slower:
+        // emit 0.055 → 0.060 ms at config 2, 0.179 → 0.211 ms at config 5)
         for (int k = 0; __any_sync(kFull, k < cnt); ++k) {
             const int tile = k < cnt ? (ty0 + ky) * ntx + tx0 + kx : -1;
             const int tcx = tx0 + kx, tcy = ty0 + ky;
@@ -875,6 +877,14 @@ __global__ void __launch_bounds__(NT, 2048 / NT) k_tile_sort_bucket(const uint32
 
 
 
+// threads per tile CTA and depth buckets of the bucket sort (compile-time A/B: -DVTGS_SORT_NT=…)
+#ifndef VTGS_SORT_NT
+#define VTGS_SORT_NT 1024
+#endif
+#ifndef VTGS_SORT_NB
+#define VTGS_SORT_NB 4096
+#endif
+constexpr int kSortNT = VTGS_SORT_NT, kSortNB = VTGS_SORT_NB;
 constexpr int kSortCapBig = 8192;
 constexpr size_t kSortSmem = 4 * kSortCap * sizeof(uint32_t) + kSortCap * sizeof(uint16_t);
 constexpr size_t kSortSmemBig = 4 * kSortCapBig * sizeof(uint32_t) + kSortCapBig * sizeof(uint16_t);
@@ -927,11 +937,11 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
             // One launch for every list ≤ kSortCap (short and long tiles' CTAs interleave; two
             // launches split at 2,048 left each one's tail exposed: 0.143 → 0.136 ms at config 2)
             // (its CTAs of longer lists plan their depth chunks of ≤ kSortCap entries instead)
-            k_tile_sort_bucket<-1, kSortCap, 4096, 1024><<<T, 1024, bucket_smem(kSortCap, 4096), s>>>(
+            k_tile_sort_bucket<-1, kSortCap, kSortNB, kSortNT><<<T, kSortNT, bucket_smem(kSortCap, kSortNB), s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T,
                 c.chunk_list, c.keys2, c.vals2, c.offs);
             // the chunks of the long lists, sorted on chip
-            k_tile_sort_bucket<0, kSortCap, 4096, 1024, true><<<2 * c.num_sms, 1024, bucket_smem(kSortCap, 4096), s>>>(
+            k_tile_sort_bucket<0, kSortCap, kSortNB, kSortNT, true><<<2 * c.num_sms, kSortNT, bucket_smem(kSortCap, kSortNB), s>>>(
                 c.tile_count, c.tile_start, c.keys, c.vals, c.pbits, c.sub_lists, c.sub_count, c.tile_flag, c.dev, T,
                 c.chunk_list, c.keys2, c.vals2, c.offs);
             ++c.launches;
@@ -959,12 +969,12 @@ cudaError_t forward_set_attributes() {
                                          (int)kSortSmem);
 
     if (!e)
-        e = cudaFuncSetAttribute(k_tile_sort_bucket<-1, kSortCap, 4096, 1024>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, 4096));
+        e = cudaFuncSetAttribute(k_tile_sort_bucket<-1, kSortCap, kSortNB, kSortNT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, kSortNB));
 
     if (!e)
-        e = cudaFuncSetAttribute(k_tile_sort_bucket<0, kSortCap, 4096, 1024, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, 4096));
+        e = cudaFuncSetAttribute(k_tile_sort_bucket<0, kSortCap, kSortNB, kSortNT, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bucket_smem(kSortCap, kSortNB));
     if (!e)
         e = cudaFuncSetAttribute(k_tile_sort<kSortCap, kSortCapBig, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSortSmemBig);

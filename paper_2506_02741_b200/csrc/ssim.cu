@@ -3,7 +3,7 @@
 // Gaussian, σ = 1.5, C1 = 0.01², C2 = 0.03², per channel, zero padding, L_S = 1 − mean SSIM).
 //
 // Two separable stencil passes over shared-memory tiles (64×16 output pixels per CTA of 256
-// threads, 5-pixel halo), the 3 channels in turn.  Both passes are register-blocked: in the
+// threads, 5-pixel halo), one colour channel per CTA (grid z).  Both passes are register-blocked: in the
 // horizontal pass a thread produces 8 consecutive outputs of a row from 18 staged inputs, in the
 // vertical pass 4 consecutive outputs of a column from 14 staged row sums.
 //   K_ssim_moments: 11-tap sums of x, y, x², y², xy → SSIM_p and the three per-pixel chain
@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(kSsThreads, 4) k_ssim_moments(const float *__r
     const int vc = threadIdx.x & (kSsTX - 1), vr = (threadIdx.x / kSsTX) * kVSeg;
     const int hr = threadIdx.x % kSsH, hq0 = (threadIdx.x / kSsH) * kHSeg;   // horizontal task
     double ssum = 0.0;
-    for (int c = 0; c < 3; ++c) {
+    {   // one channel per CTA (blockIdx.z): 3× the CTAs, a smaller last wave
+        const int c = blockIdx.z;
         ss_load<2>(sin, srcs, c, 0, true, ox, oy, W, H);
         __syncthreads();
         if (threadIdx.x < kHTasks) {   // horizontal pass: 8 consecutive outputs of one row
@@ -126,11 +127,11 @@ __global__ void __launch_bounds__(kSsThreads, 4) k_ssim_moments(const float *__r
     for (int o = 16; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ssum;
     __syncthreads();
-    const int nblk = gridDim.x * gridDim.y;
+    const int nblk = gridDim.x * gridDim.y * gridDim.z;
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int i = 0; i < kSsThreads / 32; ++i) t += red[i];
-        partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+        partials[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = t;
         last = false;
         if (loss_out) {   // the last CTA to finish sums the partials (no finalize launch)
             __threadfence();
@@ -166,7 +167,8 @@ __global__ void __launch_bounds__(kSsThreads) k_ssim_grad(const float *__restric
     const float *srcs[3] = {abc, abc + 3 * npx, abc + 6 * npx};
     const int vc = threadIdx.x & (kSsTX - 1), vr = (threadIdx.x / kSsTX) * kVSeg;
     const int hr = threadIdx.x % kSsH, hq0 = (threadIdx.x / kSsH) * kHSeg;
-    for (int c = 0; c < 3; ++c) {
+    {   // one channel per CTA (blockIdx.z): 3× the CTAs, a smaller last wave
+        const int c = blockIdx.z;
         ss_load<3>(sa, srcs, c, npx, false, ox, oy, W, H);
         __syncthreads();
         if (threadIdx.x < kHTasks) {
@@ -224,7 +226,7 @@ cudaError_t ssim_set_constants() {
 
 cudaError_t launch_ssim(Ctx &c, const float *color, const float *target, int W, int H, float tau, float *d_color,
                         float *loss_out, cudaStream_t s) {
-    const dim3 grid((W + kSsTX - 1) / kSsTX, (H + kSsTY - 1) / kSsTY);
+    const dim3 grid((W + kSsTX - 1) / kSsTX, (H + kSsTY - 1) / kSsTY, 3);
     const double n3 = 3.0 * (double)W * H;
     const float dLdS = (float)(-(double)tau / n3);
     cudaError_t e;
