@@ -910,7 +910,11 @@ cudaError_t launch_forward(Ctx &c, cudaStream_t s) {
     int64_t gN64 = (N + 255) / 256;
     if (gN64 > (int64_t)1 << 30) gN64 = (int64_t)1 << 30;
     const int gE = (int)gN64;
-    const int gN = (int)(gN64 < (int64_t)c.num_sms * 16 ? gN64 : (int64_t)c.num_sms * 16);
+#ifndef VTGS_PROJ_CTAS_PER_SM
+#define VTGS_PROJ_CTAS_PER_SM 16
+#endif
+    const int64_t gcap = (int64_t)c.num_sms * VTGS_PROJ_CTAS_PER_SM;
+    const int gN = (int)(gN64 < gcap ? gN64 : gcap);
     if (N > 0) {
         LaunchScope ls(&c, kProject, s);
         k_project_count<<<gN, 256, 0, s>>>(c.pos_rad, c.col_opa, N, c.view, c.intr, ntx, c.proj, c.rect, c.thr,
