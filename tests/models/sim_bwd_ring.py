@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Offline model of the backward's phase-1 lane utilisation (design tool, uses the oracle).
 
-Same sample of 8×4 sub-tiles of config 2 as tests/models/sim_batches.py.  Per pixel the phase-1
+Same sample of sub-tiles of config 2 as tests/models/sim_batches.py (shape sw × 32/sw, argv[2]).  Per pixel the phase-1
 candidates are the entries at sub-list positions < its `last` whose rect and 3σ disc contain it,
 walked back to front.  Compared: the lock-step walk per 32-entry batch (today's k_composite_bwd)
 and a ring of 32-entry batches whose (pixel, entry) pair storage is a circular buffer of C pairs
@@ -20,7 +20,7 @@ from synth.scenes import cached_config  # noqa: E402
 
 
 def main(n_sub=300, seed=0, sw=8):
-    sh = 32 // sw   # sub-tile shape sw × sh (8×4 built; 4×8 modelled)
+    sh = 32 // sw   # sub-tile shape sw × sh (4×8 built; 8×4 the round-1 shape; 2×16 modelled)
     cfg = cached_config(2)
     intr = cfg.intr
     pr, co, _ = oracle.instantiate(cfg.depth_stack(), cfg.rgb_stack(), cfg.pose_stack(), intr, cfg.opacity)
