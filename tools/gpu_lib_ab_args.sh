@@ -8,6 +8,6 @@ for lib in "$@"; do
   out=gpurun_out/${TAG}_$(basename $lib .so)_$rep
   VTGS_LIB_PATH=$lib timeout 300 python bench.py --no-cpu-baseline --steps 60 $ARGS > $out.json 2> $out.err
   python -c "
-import json; d=json.loads(open('$out.json').read().strip().splitlines()[-1]); print('$lib', round(d['ms_per_step'],4), {k: round(v['ms_per_launch'],4) for k, v in d['stages'].items()})"
+import json; d=json.loads(open('$out.json').read().strip().splitlines()[-1]); st=d.get('stages') or {k: {'ms_per_launch': v} for k, v in d.get('stages_eager_frame_ms', {}).items()}; print('$lib', round(d['ms_per_step'],4), {k: round(v['ms_per_launch'],4) for k, v in st.items()})"
 done
 done
