@@ -164,6 +164,7 @@ vtgs_status vtgs_destroy(vtgs_ctx *ctx) {
     if (ctx->c.copy_stream) cudaStreamDestroy(ctx->c.copy_stream);
     if (ctx->c.ev_ready) cudaEventDestroy(ctx->c.ev_ready);
     if (ctx->c.ev_copied) cudaEventDestroy(ctx->c.ev_copied);
+    if (ctx->c.host_ret) cudaFreeHost(ctx->c.host_ret);
     free_all(ctx->c);
     delete ctx;
     return VTGS_OK;
@@ -483,6 +484,9 @@ static vtgs_status step_host_core(vtgs_ctx *ctx, const float *pos_rad, const flo
         e = cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking);
         if (!e) e = cudaEventCreateWithFlags(&c.ev_ready, cudaEventDisableTiming);
         if (!e) e = cudaEventCreateWithFlags(&c.ev_copied, cudaEventDisableTiming);
+        // pinned: a device→host copy into pageable memory is staged by the driver after the stream
+        // drains, a copy into pinned memory is a DMA the synchronisation below already covers
+        if (!e) e = cudaHostAlloc((void **)&c.host_ret, 16 * sizeof(float), cudaHostAllocDefault);
         if (e) return cuda_fail(ctx, e, "vtgs_step_host (copy stream)");
     }
     // the pose goes first on the compute stream; the targets (read only by the backward's loss
@@ -501,13 +505,19 @@ static vtgs_status step_host_core(vtgs_ctx *ctx, const float *pos_rad, const flo
                          learn_end, d_col_opa, d_radius, nullptr, (want & VTGS_GRAD_POSE) ? d_dpose : nullptr, d_loss,
                          stream);
     if (st) return st;
-    e = cudaMemcpyAsync(loss_host, d_loss, sizeof(float), cudaMemcpyDeviceToHost, s);
-    if (!e && d_pose_host && (want & VTGS_GRAD_POSE))
-        e = cudaMemcpyAsync(d_pose_host, d_dpose, sizeof(float) * 7, cudaMemcpyDeviceToHost, s);
-    unsigned int overflow = 0;   // the forward's device-side capacity flag, read with the loss
-    if (!e) e = cudaMemcpyAsync(&overflow, &c.dev->overflow, sizeof(unsigned int), cudaMemcpyDeviceToHost, s);
+    // loss, d_pose and the forward's device-side capacity flag land in the pinned host_ret
+    float *hr = c.host_ret;
+    const bool want_pose = d_pose_host && (want & VTGS_GRAD_POSE);
+    e = cudaMemcpyAsync(hr, d_loss, sizeof(float), cudaMemcpyDeviceToHost, s);
+    if (!e && want_pose) e = cudaMemcpyAsync(hr + 8, d_dpose, sizeof(float) * 7, cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaMemcpyAsync(hr + 1, &c.dev->overflow, sizeof(unsigned int), cudaMemcpyDeviceToHost, s);
     if (!e) e = cudaStreamSynchronize(s);
     if (e) return cuda_fail(ctx, e, "vtgs_step_host (D2H)");
+    *loss_host = hr[0];
+    if (want_pose)
+        for (int i = 0; i < 7; ++i) d_pose_host[i] = hr[8 + i];
+    unsigned int overflow;
+    memcpy(&overflow, hr + 1, sizeof(overflow));
     if (overflow)
         return fail(ctx, VTGS_ERR_CAPACITY, "tile pairs exceeded max_pairs %lld (render and gradients empty)",
                     (long long)c.max_pairs);

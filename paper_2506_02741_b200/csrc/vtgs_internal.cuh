@@ -105,6 +105,7 @@ struct Ctx {
     uint8_t *sensor_io = nullptr;    // step_host_sensor upload staging (rgb8 | depth16)
     cudaStream_t copy_stream = nullptr;  // step_host: target upload overlapped with the forward
     cudaEvent_t ev_ready = nullptr, ev_copied = nullptr;
+    float *host_ret = nullptr;   // step_host: pinned landing buffer of the loss / d_pose / overflow read-back (16 floats)
     vtgs_pose *view_copy = nullptr;  // the forward's view pose, copied on the device for the backward
     unsigned long long *det = nullptr;  // VTGS_GRAD_DETERMINISTIC fixed-point accumulators [det_cap][5]
     int64_t det_cap = 0;
