@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--ssim", type=float, default=0.0,
                     help="add Eq. 2's SSIM term with this weight tau (0.2 in the paper) to the mapping step")
     ap.add_argument("--no-graph", action="store_true", help="run every timed step eagerly (no CUDA graph)")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="mapping: attribute gradients merged deterministically (VTGS_GRAD_DETERMINISTIC)")
     ap.add_argument("--streams", type=int, default=0,
                     help="renderer contexts / CUDA streams the views of a step alternate over "
                          "(0 = 2 for the batched configs 4 / 5, 1 otherwise)")
@@ -324,7 +326,8 @@ def workload_config(cfg, args, n_views=1, views_per_rank=1):
             "views_per_rank": views_per_rank,
             "loss": f"{cfg.loss_weights[0]}*L1(C) + {cfg.loss_weights[1]}*U*L1(D)"
                     + (f" + {args.ssim}*L_S(C)" if getattr(args, "ssim", 0.0) > 0 else "") + ", sum form",
-            "grads": "colour, opacity, radius", "seed": args.seed,
+            "grads": "colour, opacity, radius" + (" (deterministic int64 merge)" if getattr(args, "deterministic", False)
+                                                   else ""), "seed": args.seed,
             "l2": "flushed between timed steps (256 MiB write outside the step events)",
             "parallelism": f"dp{args.gpus} (view-sharded mapping, one NCCL all-reduce of the 5N fp32 gradient buffer per step)"}
 
@@ -503,7 +506,7 @@ def main():
     wc, wd = cfg.loss_weights
     mapper = BatchedMapper(R_list, pr, co, cfg.intr, [vtgs.pose_tensor(v, dev) for v in views_np],
                            [dict(rgb=torch.from_numpy(t.rgb).to(dev), depth=torch.from_numpy(t.depth).to(dev))
-                            for t in tgts], wc, wd, w_ssim=args.ssim)
+                            for t in tgts], wc, wd, w_ssim=args.ssim, deterministic=args.deterministic)
     grads = mapper.grads.flat
     d_co, d_r = mapper.grads.d_col_opa, mapper.grads.d_radius
     out = mapper.out

@@ -66,7 +66,7 @@ class BatchedMapper:
     def __init__(self, renderer, pos_rad: torch.Tensor, col_opa: torch.Tensor, intr,
                  views: Sequence[torch.Tensor], targets: Sequence[dict], w_color: float, w_depth: float,
                  learn: Sequence[int] = (0, 1 << 62), group: Optional[dist.ProcessGroup] = None,
-                 w_ssim: float = 0.0):
+                 w_ssim: float = 0.0, deterministic: bool = False):
         from . import vtgs
         self.vt = vtgs
         self.Rs = list(renderer) if isinstance(renderer, (list, tuple)) else [renderer]
@@ -91,6 +91,10 @@ class BatchedMapper:
         self.d_ssims = [torch.zeros((H, W, 3), device=dev) if self.w_ssim > 0 else None for _ in range(k)]
         self.d_ssim = self.d_ssims[0]
         self.streams = [torch.cuda.Stream(dev) for _ in range(k)] if k > 1 else None
+        if deterministic and k > 1:
+            raise ValueError("the deterministic merge finalises per context: use one renderer context")
+        # VTGS_GRAD_DETERMINISTIC: int64 fixed-point merge of the attribute gradients
+        self.want = vtgs.VTGS_GRAD_ATTR | (vtgs.VTGS_GRAD_DETERMINISTIC if deterministic else 0)
 
     def _view(self, i, v, t):
         j = i % len(self.Rs)
@@ -99,7 +103,7 @@ class BatchedMapper:
         if d_ssim is not None:
             d_ssim.zero_()
             R.ssim_loss(out[0], t["rgb"], self.w_ssim, d_color=d_ssim, loss_out=self.ssim_loss[i:i + 1])
-        R.render_bwd(self.vt.VTGS_GRAD_ATTR, d_col_opa=self.grads.d_col_opa, d_radius=self.grads.d_radius,
+        R.render_bwd(self.want, d_col_opa=self.grads.d_col_opa, d_radius=self.grads.d_radius,
                      loss=dict(target_rgb=t["rgb"], target_depth=t["depth"], w_color=self.w_color,
                                w_depth=self.w_depth, extra_dcolor=d_ssim),
                      learn=self.learn, loss_out=self.loss[i:i + 1])

@@ -666,6 +666,29 @@ def test_step_host_matches_device_path(vt):
         assert torch.allclose(r3, r2, rtol=1e-5, atol=1e-6)
 
 
+def test_batched_mapper_deterministic_merge(vt):
+    """BatchedMapper(deterministic=True) — the bench's `--deterministic` step — over five views:
+    two steps give bit-identical 5N gradient buffers (int64 fixed-point merge), equal to the
+    float-atomic step within the summation-order bound of the test above."""
+    from paper_2506_02741_b200.mapping import BatchedMapper
+    from synth.scenes import perturb_pose
+    cfg = cached_config(1)
+    R0 = _renderer(vt, cfg)
+    pr, co = gpu_instantiate(R0, cfg)
+    rng = np.random.default_rng(4)
+    views = [vt.pose_tensor(np.asarray(perturb_pose(cfg.keyframes[0].pose, 1.0 * k, 0.01 * k, rng),
+                                       dtype=np.float32), "cuda") for k in range(5)]
+    tg = cfg.targets[0]
+    tgts = [dict(rgb=torch.from_numpy(tg.rgb).cuda(), depth=torch.from_numpy(tg.depth).cuda()) for _ in views]
+    det = BatchedMapper(R0, pr, co, cfg.intr, views, tgts, 0.8, 1.0, deterministic=True)
+    a = det.step(allreduce=False).flat.clone()
+    b = det.step(allreduce=False).flat.clone()
+    flt = BatchedMapper(R0, pr, co, cfg.intr, views, tgts, 0.8, 1.0).step(allreduce=False).flat.clone()
+    torch.cuda.synchronize()
+    assert a.abs().sum() > 0 and torch.equal(a, b)
+    assert float((a - flt).norm()) <= 1e-5 * float(flt.norm())
+
+
 def test_batched_mapper_two_contexts_equals_one(vt):
     """BatchedMapper with its views alternating over two renderer contexts / CUDA streams (the
     bench's configs 4 / 5) gives the same 5N gradient sum and per-view losses as one context: the
