@@ -35,6 +35,9 @@ __device__ __forceinline__ int hm_col(int r, int q) { return q ^ (r & 31); }
 template <int NQ>
 __device__ __forceinline__ void ss_load(float (*s)[kSsH][kSsWp], const float *const *src, int c, size_t stride_q,
                                         bool interleaved, int ox, int oy, int W, int H) {
+    // fully unrolled (≤ 8 iterations): every load of the tile is in flight at once (the rolled
+    // loop waited on each iteration's loads — long-scoreboard stalls in the adjoint kernel)
+#pragma unroll
     for (int i = threadIdx.x; i < kSsH * kSsW; i += kSsThreads) {
         const int r = i / kSsW, q = i - r * kSsW;
         const int gx = ox + q - kSsR, gy = oy + r - kSsR;
